@@ -1,0 +1,84 @@
+/* Oracle: Shampoo statistics, diagonal accumulator and graft numerator (row a2).
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain C, fp64, no BLAS,
+ * compiled with -O2 -ffp-contract=off.  Shares nothing with the CUDA path.
+ *
+ * Follows Alg. 1 of the paper:
+ *     L_t <- beta2 L_{t-1} + (1-beta2) G G^T   (beta2 < 1)   else L_{t-1} + G G^T
+ *     R_t <- beta2 R_{t-1} + (1-beta2) G^T G
+ *     D_t <- D_{t-1} + G o G                    (always a sum)
+ * written as (decay, weight) = (beta2, 1-beta2) or (1, 1), reading #6.
+ *
+ * Arithmetic contract (reading #15; bit-exact target for the GPU):
+ *   acc = 0.0; for k ascending: acc = acc + (double)a_k * (double)b_k
+ *     (each product of two floats is exact in double, so fused and unfused
+ *      multiply-add give the same bits)
+ *   t1 = weight*acc; t2 = decay*(double)S_ij; S_ij = S_ji = (float)(t1 + t2)
+ *   D_ij = (float)((double)D_ij + (double)g_ij*(double)g_ij)
+ * Graft numerator of a block (floor 1e-30 of S:437 = reading #11):
+ *   num_b = sum_ij g_ij^2 / max((double)D_new_ij, 1e-30)  (row-major order)
+ */
+#include <math.h>
+#include <stdint.h>
+
+/* 1 if every G entry of the block is finite, else 0 ("non-finite gradient
+ * entries -> rejected, state unchanged"). */
+int oracle_block_finite(const float* G, int64_t ldg, int64_t row0, int64_t col0, int rows, int cols) {
+  for (int i = 0; i < rows; ++i)
+    for (int j = 0; j < cols; ++j)
+      if (!isfinite(G[(row0 + i) * ldg + col0 + j])) return 0;
+  return 1;
+}
+
+/* L_b (rows x rows, leading dim ldl) <- decay*L_b + weight * G_b G_b^T. */
+void oracle_stats_left(const float* G, int64_t ldg, int64_t row0, int64_t col0, int rows, int cols,
+                       float* L, int64_t ldl, double decay, double weight) {
+  for (int i = 0; i < rows; ++i) {
+    const float* gi = G + (row0 + i) * ldg + col0;
+    for (int j = i; j < rows; ++j) {
+      const float* gj = G + (row0 + j) * ldg + col0;
+      double acc = 0.0;
+      for (int k = 0; k < cols; ++k) acc = acc + (double)gi[k] * (double)gj[k];
+      double t1 = weight * acc;
+      double t2 = decay * (double)L[(int64_t)i * ldl + j];
+      float r = (float)(t1 + t2);
+      L[(int64_t)i * ldl + j] = r;
+      L[(int64_t)j * ldl + i] = r;
+    }
+  }
+}
+
+/* R_b (cols x cols, leading dim ldr) <- decay*R_b + weight * G_b^T G_b. */
+void oracle_stats_right(const float* G, int64_t ldg, int64_t row0, int64_t col0, int rows, int cols,
+                        float* R, int64_t ldr, double decay, double weight) {
+  for (int i = 0; i < cols; ++i) {
+    for (int j = i; j < cols; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < rows; ++k) {
+        const float* gk = G + (row0 + k) * ldg + col0;
+        acc = acc + (double)gk[i] * (double)gk[j];
+      }
+      double t1 = weight * acc;
+      double t2 = decay * (double)R[(int64_t)i * ldr + j];
+      float r = (float)(t1 + t2);
+      R[(int64_t)i * ldr + j] = r;
+      R[(int64_t)j * ldr + i] = r;
+    }
+  }
+}
+
+/* D_b <- D_b + G_b o G_b; returns the block's graft numerator. */
+double oracle_diag_update(const float* G, int64_t ldg, int64_t row0, int64_t col0, int rows, int cols,
+                          float* D, int64_t ldd) {
+  double num = 0.0;
+  for (int i = 0; i < rows; ++i)
+    for (int j = 0; j < cols; ++j) {
+      double g = (double)G[(row0 + i) * ldg + col0 + j];
+      float* d = D + (row0 + i) * ldd + col0 + j;
+      float dn = (float)((double)*d + g * g);
+      *d = dn;
+      double den = (double)dn > 1e-30 ? (double)dn : 1e-30;
+      num = num + (g * g) / den;
+    }
+  return num;
+}

@@ -1,0 +1,161 @@
+"""Oracle: blocking plan, exponents, root owners and packed offsets (row a1).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain Python integers.
+
+Rule (DESIGN.md §3 readings #5, #12, #13, #17):
+* A side of a tensor is preconditioned iff ``1 < dim <= max_precond_dim``
+  ("we bypass preconditioning of excessively large dimensions").
+* Exponents: both sides kept -> p_L = p_R = 4 (L^{-1/4} G R^{-1/4});
+  one side kept -> p = 2 on that side ("G R^{-1/2} and L^{-1/2} G",
+  P:388-390); none -> 0/0 (grafted diagonal AdaGrad direction).
+* Blocking: each axis is split into ceil(dim/b) contiguous ranges, the last
+  one ragged ("divide the tensor into blocks ... treating individual block as
+  a separate tensor").  Blocks are ordered tensor by tensor (caller
+  order), row-major over the block grid.
+* Roots: a block contributes a left root (n = rows) if p_L > 0 and a right
+  root (n = cols) if p_R > 0.  Cost = n^3 * products_per_iteration(p).
+  Owners: roots sorted by (-cost, tensor_id, block_index, side) and assigned
+  longest-processing-time first to the least-loaded rank (lowest rank on
+  ties) -- "we distribute the computation across all the CPUs".
+* Packing: one fp32 buffer holds all statistics (and, at the same offsets,
+  all roots).  Rank r's segment holds the roots it owns, grouped by (n desc,
+  p desc), each matrix ``n x ld`` with ``ld = roundup(n, 4)`` and a group
+  stride ``roundup(n*ld, 64)``.  Every segment is padded to the largest one
+  (rounded up to 64 elements) so an all-gather of equal segments rebuilds the
+  whole buffer.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+
+def products_per_iteration(p: int) -> int:
+    """Matrix products per coupled-Newton iteration: X*T, log2(p) squarings
+    of T, and T^p * M (the iteration of S:131)."""
+    squarings = {1: 0, 2: 1, 4: 2, 8: 3}[p]
+    return 2 + squarings
+
+
+def _roundup(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+@dataclass
+class Block:
+    tensor_id: int
+    block_index: int  # index inside the global block list
+    row0: int
+    col0: int
+    rows: int
+    cols: int
+    p_left: int
+    p_right: int
+    owner_left: int = -1
+    owner_right: int = -1
+    left_off: int = -1
+    right_off: int = -1
+    left_ld: int = 0
+    right_ld: int = 0
+
+
+@dataclass
+class RootGroup:
+    owner: int
+    n: int
+    p: int
+    offset: int
+    count: int
+    stride: int
+
+
+@dataclass
+class Plan:
+    blocks: list = field(default_factory=list)
+    groups: list = field(default_factory=list)
+    stats_elems: int = 0
+    segment_elems: int = 0
+    loads: list = field(default_factory=list)
+
+
+def plan(shapes, block_size: int, max_precond_dim: int, world_size: int) -> Plan:
+    if block_size < 1 or max_precond_dim < 1 or world_size < 1:
+        raise ValueError("block_size, max_precond_dim and world_size must be >= 1")
+    out = Plan()
+    for t, (m, n) in enumerate(shapes):
+        if m < 1 or n < 1:
+            raise ValueError("tensor dims must be >= 1")
+        left = 1 < m <= max_precond_dim
+        right = 1 < n <= max_precond_dim
+        if left and right:
+            pl, pr = 4, 4
+        elif left:
+            pl, pr = 2, 0
+        elif right:
+            pl, pr = 0, 2
+        else:
+            pl, pr = 0, 0
+        nbr = -(-m // block_size)
+        nbc = -(-n // block_size)
+        for bi in range(nbr):
+            for bj in range(nbc):
+                r0, c0 = bi * block_size, bj * block_size
+                out.blocks.append(Block(t, len(out.blocks), r0, c0,
+                                        min(block_size, m - r0), min(block_size, n - c0), pl, pr))
+    # roots: (cost, tensor, block, side)
+    roots = []
+    for b in out.blocks:
+        if b.p_left:
+            roots.append((b.rows ** 3 * products_per_iteration(b.p_left), b.tensor_id, b.block_index, 0))
+        if b.p_right:
+            roots.append((b.cols ** 3 * products_per_iteration(b.p_right), b.tensor_id, b.block_index, 1))
+    roots.sort(key=lambda r: (-r[0], r[1], r[2], r[3]))
+    loads = [0] * world_size
+    owned = [[] for _ in range(world_size)]  # (n, p, sort position, block, side)
+    for pos, (cost, _t, bidx, side) in enumerate(roots):
+        r = min(range(world_size), key=lambda i: (loads[i], i))
+        loads[r] += cost
+        b = out.blocks[bidx]
+        nn = b.rows if side == 0 else b.cols
+        pp = b.p_left if side == 0 else b.p_right
+        if side == 0:
+            b.owner_left = r
+        else:
+            b.owner_right = r
+        owned[r].append((nn, pp, pos, bidx, side))
+    # packing, segment by segment
+    seg_used = []
+    for r in range(world_size):
+        items = sorted(owned[r], key=lambda x: (-x[0], -x[1], x[2]))
+        off = 0
+        i = 0
+        while i < len(items):
+            nn, pp = items[i][0], items[i][1]
+            j = i
+            while j < len(items) and items[j][0] == nn and items[j][1] == pp:
+                j += 1
+            ld = _roundup(nn, 4)
+            stride = _roundup(nn * ld, 64)
+            out.groups.append(RootGroup(r, nn, pp, off, j - i, stride))  # offset relative to segment for now
+            for k in range(i, j):
+                _, _, _, bidx, side = items[k]
+                b = out.blocks[bidx]
+                if side == 0:
+                    b.left_off, b.left_ld = off + (k - i) * stride, ld
+                else:
+                    b.right_off, b.right_ld = off + (k - i) * stride, ld
+            off += (j - i) * stride
+            i = j
+        seg_used.append(off)
+    seg = _roundup(max(seg_used) if seg_used else 0, 64)
+    out.segment_elems = seg
+    out.stats_elems = seg * world_size
+    for g in out.groups:
+        g.offset += g.owner * seg
+    for b in out.blocks:
+        if b.left_off >= 0:
+            b.left_off += b.owner_left * seg
+        if b.right_off >= 0:
+            b.right_off += b.owner_right * seg
+    out.loads = loads
+    return out

@@ -1,0 +1,120 @@
+"""Pins for oracle.plan (row a1): paper/SPEC worked plans, tiling, exponent-sum,
+owner balance and packing invariants.  CPU only."""
+
+import json
+import os
+
+import pytest
+
+from oracle import plan as oplan
+from synth import transformer_big_shapes
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _golden():
+    with open(os.path.join(GOLDEN, "plan_cases.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _golden()["cases"], ids=lambda c: "x".join(map(str, c["shape"])) + f"_b{c['block_size']}")
+def test_paper_plans(case):
+    pl = oplan.plan([tuple(case["shape"])], case["block_size"], case["max_precond_dim"], 1)
+    got = [[b.row0, b.col0, b.rows, b.cols] for b in pl.blocks]
+    assert got == case["blocks"], case["cite"]
+    for b in pl.blocks:
+        assert (b.p_left, b.p_right) == (case["p_left"], case["p_right"]), case["cite"]
+
+
+def test_exponents_sum_to_minus_half():
+    # P:358-359 ("exponents sum up to -1/2"): -1/(2*)... each kept side contributes -1/p_side * 1/2... i.e.
+    # two-sided: -1/4 - 1/4 = -1/2 ; one-sided: -1/2.
+    for shape in [(7, 9), (1, 5), (5, 1), (9000, 7), (7, 9000), (300, 300)]:
+        pl = oplan.plan([shape], 128, 8192, 1)
+        for b in pl.blocks:
+            s = (-1.0 / b.p_left if b.p_left else 0.0) + (-1.0 / b.p_right if b.p_right else 0.0)
+            if b.p_left or b.p_right:
+                assert s == -0.5
+            else:
+                assert shape[0] in (1,) or shape[0] > 8192
+
+
+def test_tiling_invariant():
+    # blocks tile each tensor exactly and disjointly; ragged last block.
+    shapes = [(1000, 300), (1, 77), (4097, 4096), (33, 2049)]
+    pl = oplan.plan(shapes, 512, 4096, 3)
+    for t, (m, n) in enumerate(shapes):
+        cover = [[0] * n for _ in range(m)] if m * n <= 40000 else None
+        area = 0
+        for b in pl.blocks:
+            if b.tensor_id != t:
+                continue
+            assert 1 <= b.rows <= 512 and 1 <= b.cols <= 512
+            assert b.row0 % 512 == 0 and b.col0 % 512 == 0
+            area += b.rows * b.cols
+            if cover is not None:
+                for i in range(b.row0, b.row0 + b.rows):
+                    for j in range(b.col0, b.col0 + b.cols):
+                        cover[i][j] += 1
+        assert area == m * n
+        if cover is not None:
+            assert all(c == 1 for row in cover for c in row)
+
+
+def test_transformer_big_counts():
+    g = _golden()["transformer_big"]
+    shapes = [s for _, s in transformer_big_shapes()]
+    assert len(shapes) == 99
+    total = sum(m * n for m, n in shapes)
+    assert total == g["matrix_params"]
+    assert abs(total / 1e6 - g["paper_params_millions"]) / g["paper_params_millions"] < 0.001
+    pl = oplan.plan(shapes, g["block_size"], g["max_precond_dim"], 1)
+    assert len(pl.blocks) == g["n_blocks"]
+    p4 = sum((b.p_left == 4) + (b.p_right == 4) for b in pl.blocks)
+    p2 = sum((b.p_left == 2) + (b.p_right == 2) for b in pl.blocks)
+    assert (p4, p2) == (g["n_roots_p4"], g["n_roots_p2"])
+
+
+@pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
+def test_owner_balance_and_packing(W):
+    shapes = [s for _, s in transformer_big_shapes()] + [(100, 37), (2048, 256)]
+    pl = oplan.plan(shapes, 1024, 8192, W)
+    costs = []
+    intervals = []
+    for b in pl.blocks:
+        for side, p, n, off, ld, own in ((0, b.p_left, b.rows, b.left_off, b.left_ld, b.owner_left),
+                                          (1, b.p_right, b.cols, b.right_off, b.right_ld, b.owner_right)):
+            if not p:
+                assert off == -1
+                continue
+            assert 0 <= own < W
+            assert ld == -(-n // 4) * 4 and off % 64 == 0
+            seg0 = own * pl.segment_elems
+            assert seg0 <= off and off + n * ld <= seg0 + pl.segment_elems  # inside its owner's segment
+            intervals.append((off, off + n * ld))
+            costs.append(n ** 3 * oplan.products_per_iteration(p))
+    intervals.sort()
+    for a, b in zip(intervals, intervals[1:]):
+        assert a[1] <= b[0]  # no overlap
+    assert pl.stats_elems == W * pl.segment_elems
+    # LPT bound: max load - min load <= largest single cost
+    assert max(pl.loads) - min(pl.loads) <= max(costs)
+    assert sum(pl.loads) == sum(costs)
+    # groups are strided batches that cover exactly the owned roots
+    assert sum(g.count for g in pl.groups) == len(intervals)
+    for g in pl.groups:
+        assert g.stride >= g.n * (-(-g.n // 4) * 4) and g.stride % 64 == 0
+
+
+def test_round_robin_for_uniform_costs():
+    pl = oplan.plan([(1024, 1024)] * 8, 1024, 8192, 4)
+    owners = [(b.owner_left, b.owner_right) for b in pl.blocks]
+    # sorted by (tensor, block, side) with equal costs -> L0 R0 L1 R1 ... dealt round-robin
+    flat = [o for pair in owners for o in pair]
+    assert flat == [i % 4 for i in range(16)]
+
+
+def test_plan_is_deterministic():
+    shapes = [s for _, s in transformer_big_shapes()]
+    a = oplan.plan(shapes, 1024, 8192, 8)
+    b = oplan.plan(shapes, 1024, 8192, 8)
+    assert [vars(x) for x in a.blocks] == [vars(x) for x in b.blocks]
