@@ -1,0 +1,193 @@
+/* shampoo.h -- C ABI of libshampoo: the data-parallel hot path of distributed
+ * Shampoo (Anil, Gupta, Koren, Regan, Singer, "Second Order Optimization Made
+ * Practical", arXiv 2002.09018) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = line n of the paper text (reference PAPER.md), "S:n" = line
+ * n of the reference SPEC.md, "reading #k" = DESIGN.md §3 entry k.
+ *
+ * Conventions shared by every call
+ * ---------------------------------
+ *  - Pointers are DEVICE pointers unless the parameter is marked (host).
+ *  - The caller owns all memory (statistics, roots, gradients, D, P, tables,
+ *    workspaces).  The library holds no device memory and no state between
+ *    calls; calls on different streams may run concurrently from different
+ *    host threads.
+ *  - Matrices are row-major fp32 with an explicit leading dimension (in
+ *    elements).  Statistics and roots are symmetric; kernels read the upper
+ *    triangle and always write both triangles.
+ *  - Host-checkable problems (shapes, p, alignment, non-finite scalars,
+ *    workspace too small, capacity) return a non-zero status synchronously
+ *    and enqueue nothing.  Data-dependent outcomes (non-finite gradients,
+ *    non-convergence, degenerate statistics) are never return codes: they are
+ *    reported per block / per matrix in device arrays.
+ *  - Every compute call is stream-ordered, enqueues its kernels on `stream`
+ *    and returns without synchronising the host.
+ *  - No exception crosses the ABI; on error the message is available from
+ *    shampoo_last_error() (thread-local).
+ */
+#ifndef SHAMPOO_H_
+#define SHAMPOO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SHAMPOO_ABI_VERSION 1
+
+typedef enum {
+  SHAMPOO_OK = 0,
+  SHAMPOO_ERR_INVALID_ARG = 1, /* bad shape / p / alignment / scalar        */
+  SHAMPOO_ERR_UNSUPPORTED = 2, /* valid request this build cannot serve     */
+  SHAMPOO_ERR_CUDA = 3,        /* a CUDA runtime call or launch failed      */
+  SHAMPOO_ERR_WORKSPACE = 4,   /* workspace pointer null or too small       */
+  SHAMPOO_ERR_CAPACITY = 5     /* host output array too small (plan)        */
+} shampoo_status_t;
+
+typedef void* shampoo_stream_t; /* a cudaStream_t (NULL = legacy default stream) */
+
+/* One block of one parameter tensor (plan output; integer, bit-exact vs the
+ * oracle).  P:396-398: "divide the tensor into blocks and treating individual
+ * block as a separate tensor".  72 bytes. */
+typedef struct {
+  int32_t tensor_id;   /* index into the caller's tensor list                          */
+  int32_t reserved;    /* 0                                                            */
+  int64_t row0, col0;  /* block origin inside the tensor                               */
+  int32_t rows, cols;  /* extent; the last block of each axis may be ragged            */
+  int32_t p_left;      /* exponent of L_b^{-1/p}: 4 two-sided, 2 one-sided, 0 skipped  */
+  int32_t p_right;     /* exponent of R_b^{-1/p}                                       */
+  int32_t owner_left;  /* rank that updates L_b and computes its root (-1 if skipped)  */
+  int32_t owner_right; /* rank that updates R_b and computes its root (-1 if skipped)  */
+  int64_t left_off;    /* element offset of L_b (and of its root) in the packed buffer */
+  int64_t right_off;   /*   ... of R_b; -1 when the side is skipped                    */
+  int32_t left_ld;     /* leading dimension of L_b = roundup(rows, 4)                  */
+  int32_t right_ld;    /* leading dimension of R_b = roundup(cols, 4)                  */
+} shampoo_block_t;
+
+/* A strided batch of same-size roots owned by one rank (plan output). */
+typedef struct {
+  int32_t owner, n, p, count;
+  int64_t offset; /* element offset of the first matrix in the packed buffer */
+  int64_t stride; /* elements between consecutive matrices                   */
+} shampoo_group_t;
+
+/* One parameter tensor.  An array of these lives in DEVICE memory. */
+typedef struct {
+  const float* G; /* gradient, row-major m x n                                    */
+  float* D;       /* diagonal AdaGrad accumulator (same layout as G), in/out      */
+  float* P;       /* preconditioned-gradient output (same layout as G)            */
+  int64_t ldg, ldd, ldp;
+  int64_t m, n;
+} shampoo_tensor_t;
+
+/* Per-matrix result of the root solver (device array). */
+typedef struct {
+  int32_t iters;     /* coupled-Newton iterations performed                        */
+  int32_t status;    /* 0 converged (err <= tol); 1 not converged, best iterate
+                        returned; 2 non-finite input, X left untouched;
+                        3 degenerate (lambda_hat <= 0), X = I written           */
+  double lambda_max; /* power-iteration estimate lambda_hat (reading #3)          */
+  double err;        /* max_ij |M - I| of the returned iterate                     */
+} shampoo_root_info_t;
+
+int shampoo_abi_version(void);
+const char* shampoo_last_error(void);
+
+/* ------------------------------------------------------------------ a1: plan
+ * Blocking plan, exponents, owners and packing (P:356-359, P:385-390,
+ * P:396-398; rule in DESIGN.md §5 / oracle/plan.py).
+ *   shapes      (host) 2*n_tensors int64: m0, n0, m1, n1, ...
+ *   blocks      (host, out) capacity entries, or NULL to query counts only
+ *   groups      (host, out) group_capacity entries, or NULL
+ *   stats_elems (host, out) elements of the packed statistics/roots buffer
+ *               (= world_size * segment_elems; segment r holds rank r's roots)
+ * Returns SHAMPOO_ERR_CAPACITY (counts still written) if an array is too small. */
+int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
+                 int32_t world_size, shampoo_block_t* blocks, int32_t capacity, int32_t* n_blocks,
+                 shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups,
+                 int64_t* stats_elems, int64_t* segment_elems);
+
+/* ------------------------------------------------------- a2: statistics step
+ * For every block b (Alg. 1; contract in DESIGN.md §6.2):
+ *   if any G_b entry is non-finite: block_status[b] = 2, L_b/R_b/D_b untouched,
+ *                                   graft_num[b] = 0;
+ *   else  L_b <- decay*L_b + weight*G_b G_b^T   (if p_left  and (only_owner<0 or owner_left ==only_owner))
+ *         R_b <- decay*R_b + weight*G_b^T G_b   (if p_right and (only_owner<0 or owner_right==only_owner))
+ *         D_b <- D_b + G_b o G_b                (always; D may be NULL per tensor -> skipped)
+ *         graft_num[b] = sum g^2 / max(D_new, 1e-30)   (reading #11)
+ * L/R use the sequential fp64 contract (ascending-k fp64 accumulation, then
+ * t1 = weight*acc, t2 = decay*old, (float)(t1+t2)); they are BIT-EXACT with the
+ * oracle.  (decay, weight) = (beta2, 1-beta2) or (1, 1) (reading #6).
+ *   tensors, blocks : device tables (n_tensors / n_blocks entries)
+ *   stats           : packed fp32 statistics (offsets from the plan), in/out
+ *   graft_num       : double[n_blocks] out (nullable)
+ *   block_status    : int32[n_blocks] out (nullable)
+ *   workspace       : >= shampoo_stats_workspace_bytes(n_blocks), 256-B aligned
+ * G, D, P need only fp32 alignment; any ld >= n works. */
+size_t shampoo_stats_workspace_bytes(int32_t n_blocks);
+int shampoo_stats_update(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
+                         int32_t n_blocks, int32_t only_owner, float* stats, double decay, double weight,
+                         double* graft_num, int32_t* block_status, void* workspace, size_t workspace_bytes,
+                         shampoo_stream_t stream);
+
+/* --------------------------------------- a3-a6: batched inverse p-th roots
+ * X_i ~ (A_i + eps_rel*lambda_hat_i*I)^{-1/p} for a strided batch of n x n
+ * symmetric PSD fp32 matrices, by the coupled Newton iteration (
+ * S:131; readings #1-#4):
+ *   lambda_hat: `power_iters` power steps from the splitmix64 start vector;
+ *   A_hat = A + eps_rel*lambda_hat*I;  c = lambda_hat*(1+eps_rel);
+ *   M_0 = A_hat/c;  X_0 = c^{-1/p} I;
+ *   repeat: err = max|M-I|; stop if err <= tol (or stagnation / max_iter);
+ *           T = ((p+1)I - M)/p;  X <- X T;  M <- T^p M.
+ * Products run in fp64 on the FP64 tensor pipe (DMMA); results are written
+ * as fp32.  p in {1, 2, 4, 8}; 1 <= n <= 8192.
+ *   A   : batch matrices at A + i*stride_a, leading dim lda (fp32, read only)
+ *   X   : outputs at X + i*stride_x, leading dim ldx (fp32; may alias A only if
+ *         A == X with equal strides/ld -- the input is consumed first)
+ *   info: shampoo_root_info_t[batch] out
+ *   workspace: >= shampoo_root_workspace_bytes(batch, n, p, max_iter), 256-B aligned
+ * A_i must be symmetric (statistics are, by construction): the Newton setup
+ * reads its upper triangle.  Non-finite input leaves X_i untouched (status 2);
+ * lambda_hat <= 0 writes X_i = I (status 3). */
+size_t shampoo_root_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter);
+int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                     int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                     double tol, int32_t max_iter, int32_t power_iters,
+                                     shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                     shampoo_stream_t stream);
+
+/* Independent root check (config 2, north-star invariant):
+ *   residual_i = || X_i^p (A_i + eps_rel*lambda_i*I) - I ||_F   in fp64,
+ * lambda_i = info[i].lambda_max from the root call.  out: double[batch]. */
+size_t shampoo_root_residual_workspace_bytes(int32_t batch, int32_t n, int32_t p);
+int shampoo_root_residual_batched(const float* A, int64_t lda, int64_t stride_a, const float* X, int64_t ldx,
+                                  int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                  const shampoo_root_info_t* info, double* residual, void* workspace,
+                                  size_t workspace_bytes, shampoo_stream_t stream);
+
+/* ------------------------------------------- a8, a9: precondition + graft
+ * For every block b (readings #9-#11, #17):
+ *   two-sided  P_b = X_L G_b X_R;  one-sided P_b = G_b X_R or X_L G_b;
+ *   no side    P_b = D_b^{-1/2} o G_b  (grafted diagonal AdaGrad);
+ *   graft_scale[b] = sqrt(graft_num[b]) / ||P_b||_F  (0 if ||P_b|| = 0),
+ * written into tensors[t].P.  roots uses the statistics packing.  The caller
+ * applies W -= eta * graft_scale[b] * P_b (grafting).
+ *   graft_num  : double[n_blocks] from shampoo_stats_update (nullable -> no scale)
+ *   graft_scale: float[n_blocks] out (nullable)
+ *   den        : double[n_blocks] out, ||P_b||_F^2 (nullable)
+ *   workspace  : >= shampoo_precondition_workspace_bytes(blocks_host, n_blocks) */
+size_t shampoo_precondition_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks);
+int shampoo_precondition(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
+                         int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
+                         double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream);
+
+/* Number of kernel launches the last compute call on this host thread
+ * enqueued (bench accounting, "gpu_launches"). */
+int64_t shampoo_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHAMPOO_H_ */

@@ -20,6 +20,7 @@ DESIGN.md §3 (#1-#4, #16), taken from SPEC.md S:131-132 / S:163-164:
       c^{-1/4} = 1/sqrt(sqrt(c)), c^{-1/2} = 1/sqrt(c).
   iterate (reading #1), k = 0, 1, ...:
       err_k = max_ij |M_k - I|
+      if err_k is not finite                           -> X untouched   (status 2)
       if err_k <= tol                                   -> return X_k   (status 0)
       if k >= 1 and err_k >= err_{k-1} and err_{k-1} < 1e-2
                                                          -> return X_{k-1} (status 1)
@@ -128,6 +129,8 @@ def inverse_pth_root(A, p: int, eps_rel: float = 1e-6, tol: float = 1e-7, max_it
     k = 0
     while True:
         err = float(np.max(np.abs(M - I)))
+        if not np.isfinite(err):            # overflow / NaN mid-iteration: treat as non-finite input
+            return X_prev, RootInfo(k, 2, lam, err)
         if err <= tol:
             return X, RootInfo(k, 0, lam, err)
         if k >= 1 and err >= err_last and err_last < STAGNATION_GATE:

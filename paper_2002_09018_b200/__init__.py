@@ -1,0 +1,242 @@
+"""paper_2002_09018_b200 -- B200-native data-parallel hot path of distributed Shampoo
+(Anil et al., "Second Order Optimization Made Practical", arXiv 2002.09018).
+
+Thin Python binding over the C ABI of ``libshampoo.so`` (include/shampoo.h).
+PyTorch supplies device memory, streams and process groups only; every step of
+the hot path (statistics, power iteration, coupled-Newton roots, residual,
+preconditioning, grafting) runs in the library's sm_100a kernels.  There is no
+CPU fallback: importing the package raises if the library is not built.
+
+Rows of the hot path:
+  a1  make_plan                     blocking plan, exponents, owners, packing
+  a2  stats_update                  L/R statistics, D, graft numerator (bit-exact)
+  a3-a6 inverse_pth_root_batched    power iteration + ridge + coupled Newton
+        root_residual_batched       ||X^p A_hat - I||_F check
+  a7  dist.refresh_roots            owner-sharded roots + NCCL all-gather
+  a8-a9 precondition                L^{-1/p} G R^{-1/p} and the graft scale
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BLOCK_DTYPE, GROUP_DTYPE, ROOT_INFO_DTYPE, TENSOR_DTYPE, ShampooError, check, last_launch_count
+
+_lib.lib()  # fail loudly at import if the CUDA library is missing
+
+__all__ = [
+    "Plan", "make_plan", "TensorTable", "stats_update", "inverse_pth_root_batched", "root_residual_batched",
+    "precondition", "root_workspace_bytes", "ShampooError", "last_launch_count", "ROOT_INFO_DTYPE",
+]
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+_WS: dict = {}
+
+
+def workspace(nbytes: int, device, tag: str = "default") -> torch.Tensor:
+    """Cached device workspace (torch allocations are >= 512-B aligned)."""
+    key = (str(device), tag)
+    w = _WS.get(key)
+    if w is None or w.numel() < nbytes:
+        _WS.pop(key, None)
+        w = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _WS[key] = w
+    return w
+
+
+def free_workspaces():
+    _WS.clear()
+
+
+# ----------------------------------------------------------------------- a1
+@dataclass
+class Plan:
+    shapes: list
+    block_size: int
+    max_precond_dim: int
+    world_size: int
+    blocks: np.ndarray
+    groups: np.ndarray
+    stats_elems: int
+    segment_elems: int
+    _dev: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def n_blocks(self) -> int:
+        return int(self.blocks.shape[0])
+
+    def device_blocks(self, device) -> torch.Tensor:
+        key = str(device)
+        if key not in self._dev:
+            self._dev[key] = torch.from_numpy(self.blocks.view(np.uint8).copy()).to(device)
+        return self._dev[key]
+
+    def groups_of(self, owner: int):
+        return [g for g in self.groups if int(g["owner"]) == owner]
+
+
+def make_plan(shapes, block_size: int = 1024, max_precond_dim: int = 8192, world_size: int = 1) -> Plan:
+    L = _lib.lib()
+    sh = np.ascontiguousarray(np.asarray(shapes, dtype=np.int64).reshape(-1, 2))
+    nb = np.zeros(1, np.int32)
+    ng = np.zeros(1, np.int32)
+    se = np.zeros(1, np.int64)
+    sg = np.zeros(1, np.int64)
+    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, None, 0,
+                         nb.ctypes.data, None, 0, ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
+    blocks = np.zeros(int(nb[0]), BLOCK_DTYPE)
+    groups = np.zeros(int(ng[0]), GROUP_DTYPE)
+    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size,
+                         blocks.ctypes.data, blocks.shape[0], nb.ctypes.data, groups.ctypes.data, groups.shape[0],
+                         ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
+    return Plan([tuple(map(int, s)) for s in sh], block_size, max_precond_dim, world_size, blocks, groups,
+                int(se[0]), int(sg[0]))
+
+
+# ------------------------------------------------------------- tensor table
+class TensorTable:
+    """Device table of shampoo_tensor_t for lists of G (grad), D and P tensors.
+    Tensors must stay alive (and keep their storage) while the table is used."""
+
+    def __init__(self, Gs, Ds=None, Ps=None):
+        n = len(Gs)
+        Ds = Ds if Ds is not None else [None] * n
+        Ps = Ps if Ps is not None else [None] * n
+        host = np.zeros(n, TENSOR_DTYPE)
+        self.device = Gs[0].device
+        for i, (G, D, P) in enumerate(zip(Gs, Ds, Ps)):
+            for name, T in (("G", G), ("D", D), ("P", P)):
+                if T is None:
+                    continue
+                if T.dtype != torch.float32 or T.dim() != 2 or T.stride(1) != 1 or T.device != self.device:
+                    raise ValueError(f"tensor {i} {name}: need a row-major 2-D float32 tensor on {self.device}")
+                if tuple(T.shape) != tuple(G.shape):
+                    raise ValueError(f"tensor {i} {name}: shape {tuple(T.shape)} != G {tuple(G.shape)}")
+            host[i]["G"] = G.data_ptr()
+            host[i]["ldg"] = G.stride(0)
+            host[i]["m"], host[i]["n"] = G.shape
+            if D is not None:
+                host[i]["D"], host[i]["ldd"] = D.data_ptr(), D.stride(0)
+            if P is not None:
+                host[i]["P"], host[i]["ldp"] = P.data_ptr(), P.stride(0)
+        self.host = host
+        self.n = n
+        self.dev = torch.from_numpy(host.view(np.uint8).copy()).to(self.device)
+        self._keep = (list(Gs), list(Ds), list(Ps))
+
+
+# ----------------------------------------------------------------------- a2
+def stats_update(table: TensorTable, plan: Plan, stats: torch.Tensor, decay: float = 1.0, weight: float = 1.0,
+                 only_owner: int = -1, graft_num: torch.Tensor | None = None,
+                 block_status: torch.Tensor | None = None, stream=None):
+    """One statistics step over every block (one call, one launch sequence)."""
+    assert stats.dtype == torch.float32 and stats.is_contiguous() and stats.numel() >= plan.stats_elems
+    L = _lib.lib()
+    nb = plan.n_blocks
+    wsb = L.shampoo_stats_workspace_bytes(nb)
+    ws = workspace(wsb, stats.device, "stats")
+    check(L.shampoo_stats_update(table.dev.data_ptr(), table.n, plan.device_blocks(stats.device).data_ptr(), nb,
+                                 only_owner, stats.data_ptr(), float(decay), float(weight),
+                                 graft_num.data_ptr() if graft_num is not None else None,
+                                 block_status.data_ptr() if block_status is not None else None,
+                                 ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+
+
+# -------------------------------------------------------------------- a3-a6
+def root_workspace_bytes(batch: int, n: int, p: int, max_iter: int = 100) -> int:
+    return int(_lib.lib().shampoo_root_workspace_bytes(batch, n, p, max_iter))
+
+
+def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: int, stride_x: int, batch: int,
+                         n: int, p: int, info: torch.Tensor, eps_rel: float = 1e-6, tol: float = 1e-7,
+                         max_iter: int = 100, power_iters: int = 100, device=None, stream=None):
+    L = _lib.lib()
+    wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
+    ws = workspace(wsb, device if device is not None else info.device, "root")
+    check(L.shampoo_inverse_pth_root_batched(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel, tol,
+                                             max_iter, power_iters, info.data_ptr(), ws.data_ptr(), ws.numel(),
+                                             _stream_ptr(stream)))
+
+
+def new_info(batch: int, device) -> torch.Tensor:
+    return torch.zeros(batch * ROOT_INFO_DTYPE.itemsize, dtype=torch.uint8, device=device)
+
+
+def info_to_numpy(info: torch.Tensor) -> np.ndarray:
+    return info.cpu().numpy().view(ROOT_INFO_DTYPE)
+
+
+def inverse_pth_root_batched(A: torch.Tensor, p: int, X: torch.Tensor | None = None, eps_rel: float = 1e-6,
+                             tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100,
+                             info: torch.Tensor | None = None, stream=None):
+    """A: (batch, n, n) or (n, n) float32 CUDA tensor (row stride >= n, unit column stride).
+    Returns (X, info) with X like A and info a uint8 tensor of shampoo_root_info_t."""
+    squeeze = A.dim() == 2
+    A3 = A.unsqueeze(0) if squeeze else A
+    assert A3.dtype == torch.float32 and A3.is_cuda and A3.stride(2) == 1
+    batch, n, n2 = A3.shape
+    assert n == n2
+    if X is None:
+        X = torch.empty_like(A3)
+    X3 = X.unsqueeze(0) if X.dim() == 2 else X
+    if info is None:
+        info = new_info(batch, A3.device)
+    inverse_pth_root_ptr(A3.data_ptr(), A3.stride(1), A3.stride(0), X3.data_ptr(), X3.stride(1), X3.stride(0), batch,
+                         n, p, info, eps_rel, tol, max_iter, power_iters, A3.device, stream)
+    return (X3[0] if squeeze else X3), info
+
+
+def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.Tensor, eps_rel: float = 1e-6,
+                          stream=None) -> torch.Tensor:
+    A3 = A.unsqueeze(0) if A.dim() == 2 else A
+    X3 = X.unsqueeze(0) if X.dim() == 2 else X
+    batch, n, _ = A3.shape
+    L = _lib.lib()
+    out = torch.empty(batch, dtype=torch.float64, device=A3.device)
+    wsb = L.shampoo_root_residual_workspace_bytes(batch, n, p)
+    ws = workspace(wsb, A3.device, "residual")
+    check(L.shampoo_root_residual_batched(A3.data_ptr(), A3.stride(1), A3.stride(0), X3.data_ptr(), X3.stride(1),
+                                          X3.stride(0), batch, n, p, eps_rel, info.data_ptr(), out.data_ptr(),
+                                          ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+    return out
+
+
+def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, owner: int, eps_rel: float = 1e-6,
+                        tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100, infos=None, stream=None):
+    """Inverse p-th roots of every statistic owned by `owner` (one batched call per
+    (n, p) group); roots land at the statistics' offsets."""
+    out = []
+    for g in plan.groups_of(owner):
+        cnt, n, p = int(g["count"]), int(g["n"]), int(g["p"])
+        off, stride = int(g["offset"]), int(g["stride"])
+        ld = (n + 3) // 4 * 4
+        info = new_info(cnt, stats.device)
+        inverse_pth_root_ptr(stats.data_ptr() + 4 * off, ld, stride, roots.data_ptr() + 4 * off, ld, stride, cnt, n,
+                             p, info, eps_rel, tol, max_iter, power_iters, stats.device, stream)
+        out.append((g, info))
+    if infos is not None:
+        infos.extend(out)
+    return out
+
+
+# -------------------------------------------------------------------- a8-a9
+def precondition(table: TensorTable, plan: Plan, roots: torch.Tensor, graft_num: torch.Tensor | None = None,
+                 graft_scale: torch.Tensor | None = None, den: torch.Tensor | None = None, stream=None):
+    L = _lib.lib()
+    nb = plan.n_blocks
+    wsb = L.shampoo_precondition_workspace_bytes(plan.blocks.ctypes.data, nb)
+    ws = workspace(wsb, roots.device, "precondition")
+    check(L.shampoo_precondition(table.dev.data_ptr(), table.n, plan.device_blocks(roots.device).data_ptr(), nb,
+                                 roots.data_ptr(), graft_num.data_ptr() if graft_num is not None else None,
+                                 graft_scale.data_ptr() if graft_scale is not None else None,
+                                 den.data_ptr() if den is not None else None, ws.data_ptr(), ws.numel(),
+                                 _stream_ptr(stream)))

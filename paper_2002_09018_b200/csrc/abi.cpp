@@ -1,0 +1,175 @@
+// abi.cpp -- the extern "C" entry points of libshampoo (include/shampoo.h):
+// host-side validation, error reporting and dispatch to the CUDA launchers.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "internal.h"
+
+namespace shp {
+
+static thread_local char g_err[512] = "";
+static thread_local int64_t g_launches = 0;
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int set_cuda_error(const char* what, cudaError_t e) {
+  return set_error(SHAMPOO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
+              int32_t world_size, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
+              shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
+              int64_t* segment_elems);
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int check_ws(const void* ws, size_t have, size_t need) {
+  if (need == 0) return SHAMPOO_OK;
+  if (!ws || have < need)
+    return set_error(SHAMPOO_ERR_WORKSPACE, "workspace too small: have %zu bytes, need %zu", have, need);
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
+  return SHAMPOO_OK;
+}
+
+static bool valid_p(int p) { return p == 1 || p == 2 || p == 4 || p == 8; }
+
+}  // namespace shp
+
+using namespace shp;
+
+extern "C" {
+
+int shampoo_abi_version(void) { return SHAMPOO_ABI_VERSION; }
+
+const char* shampoo_last_error(void) { return g_err; }
+
+int64_t shampoo_last_launch_count(void) { return g_launches; }
+
+int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
+                 int32_t world_size, shampoo_block_t* blocks, int32_t capacity, int32_t* n_blocks,
+                 shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups, int64_t* stats_elems,
+                 int64_t* segment_elems) {
+  g_err[0] = 0;
+  return plan_impl(shapes, n_tensors, block_size, max_precond_dim, world_size, blocks, capacity, n_blocks, groups,
+                   group_capacity, n_groups, stats_elems, segment_elems);
+}
+
+size_t shampoo_stats_workspace_bytes(int32_t n_blocks) { return n_blocks > 0 ? stats_workspace_bytes(n_blocks) : 0; }
+
+int shampoo_stats_update(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
+                         int32_t n_blocks, int32_t only_owner, float* stats, double decay, double weight,
+                         double* graft_num, int32_t* block_status, void* workspace, size_t workspace_bytes,
+                         shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
+  if (n_blocks == 0) return SHAMPOO_OK;
+  if (!tensors || !blocks) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block table");
+  if (!std::isfinite(decay) || !std::isfinite(weight))
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "decay/weight must be finite");
+  if (!stats) return set_error(SHAMPOO_ERR_INVALID_ARG, "null statistics buffer");
+  if (!aligned16(stats)) return set_error(SHAMPOO_ERR_INVALID_ARG, "statistics buffer not 16-B aligned");
+  int rc = check_ws(workspace, workspace_bytes, stats_workspace_bytes(n_blocks));
+  if (rc) return rc;
+  return stats_launch(tensors, n_tensors, blocks, n_blocks, only_owner, stats, decay, weight, graft_num, block_status,
+                      workspace, static_cast<cudaStream_t>(stream), &g_launches);
+}
+
+size_t shampoo_root_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter) {
+  (void)p;
+  if (batch <= 0 || n <= 0 || max_iter < 0) return 0;
+  return root_workspace_bytes(batch, n, max_iter);
+}
+
+int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                     int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                     double tol, int32_t max_iter, int32_t power_iters,
+                                     shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                     shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (batch < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "batch < 0");
+  if (batch == 0) return SHAMPOO_OK;
+  if (n < 1 || n > 8192) return set_error(SHAMPOO_ERR_INVALID_ARG, "n = %d outside [1, 8192]", n);
+  if (!valid_p(p)) return set_error(SHAMPOO_ERR_INVALID_ARG, "p = %d not in {1, 2, 4, 8}", p);
+  if (!A || !X || !info) return set_error(SHAMPOO_ERR_INVALID_ARG, "null A, X or info");
+  if (lda < n || ldx < n) return set_error(SHAMPOO_ERR_INVALID_ARG, "leading dimension < n");
+  if (batch > 1 && (stride_a < lda * (int64_t)(n - 1) + n || stride_x < ldx * (int64_t)(n - 1) + n))
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "batch stride too small");
+  if (!std::isfinite(eps_rel) || eps_rel < 0 || !std::isfinite(tol) || tol < 0)
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "eps_rel / tol must be finite and >= 0");
+  if (max_iter < 0 || max_iter > 1000 || power_iters < 1)
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "max_iter in [0, 1000], power_iters >= 1");
+  int rc = check_ws(workspace, workspace_bytes, root_workspace_bytes(batch, n, max_iter));
+  if (rc) return rc;
+  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, eps_rel, tol, max_iter, power_iters, info,
+                     workspace, static_cast<cudaStream_t>(stream), &g_launches);
+}
+
+size_t shampoo_root_residual_workspace_bytes(int32_t batch, int32_t n, int32_t p) {
+  (void)p;
+  if (batch <= 0 || n <= 0) return 0;
+  return residual_workspace_bytes(batch, n);
+}
+
+int shampoo_root_residual_batched(const float* A, int64_t lda, int64_t stride_a, const float* X, int64_t ldx,
+                                  int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                  const shampoo_root_info_t* info, double* residual, void* workspace,
+                                  size_t workspace_bytes, shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (batch < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "batch < 0");
+  if (batch == 0) return SHAMPOO_OK;
+  if (n < 1 || n > 8192) return set_error(SHAMPOO_ERR_INVALID_ARG, "n = %d outside [1, 8192]", n);
+  if (!valid_p(p)) return set_error(SHAMPOO_ERR_INVALID_ARG, "p = %d not in {1, 2, 4, 8}", p);
+  if (!A || !X || !info || !residual) return set_error(SHAMPOO_ERR_INVALID_ARG, "null argument");
+  if (lda < n || ldx < n) return set_error(SHAMPOO_ERR_INVALID_ARG, "leading dimension < n");
+  if (!std::isfinite(eps_rel) || eps_rel < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "eps_rel");
+  int rc = check_ws(workspace, workspace_bytes, residual_workspace_bytes(batch, n));
+  if (rc) return rc;
+  return residual_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, eps_rel, info, residual, workspace,
+                         static_cast<cudaStream_t>(stream), &g_launches);
+}
+
+size_t shampoo_precondition_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks) {
+  if (!blocks_host || n_blocks <= 0) return 0;
+  return precondition_workspace_bytes(blocks_host, n_blocks);
+}
+
+int shampoo_precondition(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
+                         int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
+                         double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
+  if (n_blocks == 0) return SHAMPOO_OK;
+  if (!tensors || !blocks || !roots) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block/roots");
+  if (!workspace) return set_error(SHAMPOO_ERR_WORKSPACE, "null workspace");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
+  return precondition_launch(tensors, n_tensors, blocks, n_blocks, roots, graft_num, graft_scale, den, workspace,
+                             workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
+}
+
+}  // extern "C"

@@ -1,0 +1,39 @@
+// internal.h -- host-side helpers shared by the libshampoo translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "shampoo.h"
+
+namespace shp {
+
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(const char* what, cudaError_t e = cudaGetLastError());
+
+// root.cu
+size_t root_workspace_bytes(int batch, int n, int max_iter);
+int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
+                int n, int p, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
+                void* ws, cudaStream_t stream, int64_t* launches);
+size_t residual_workspace_bytes(int batch, int n);
+int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* X, int64_t ldx, int64_t stride_x,
+                    int batch, int n, int p, double eps_rel, const shampoo_root_info_t* info, double* residual,
+                    void* ws, cudaStream_t stream, int64_t* launches);
+
+// stats.cu
+size_t stats_workspace_bytes(int n_blocks);
+int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_block_t* blocks, int n_blocks,
+                 int only_owner, float* stats, double decay, double weight, double* graft_num, int32_t* block_status,
+                 void* ws, cudaStream_t stream, int64_t* launches);
+
+// precondition.cu
+size_t precondition_workspace_bytes(const shampoo_block_t* blocks_host, int n_blocks);
+int precondition_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_block_t* blocks, int n_blocks,
+                        const float* roots, const double* graft_num, float* graft_scale, double* den, void* ws,
+                        size_t ws_bytes, cudaStream_t stream, int64_t* launches);
+
+int num_sms();
+
+}  // namespace shp

@@ -1,0 +1,163 @@
+// plan.cpp -- blocking plan, exponents, root owners and packed offsets (row a1).
+//
+// Rule (readings #5, #12, #13, #17):
+//  * side kept iff 1 < dim <= max_precond_dim (bypass huge dims);
+//  * both kept -> p = 4 / 4; one kept -> p = 2 on it;
+//  * each axis split into ceil(dim/b) contiguous ranges, last ragged,
+//    blocks row-major over the block grid, tensors in caller order;
+//  * roots sorted by (cost desc, tensor, block, side) with cost = n^3 * products
+//    per Newton iteration, assigned LPT to the least-loaded rank;
+//  * packing: rank-major segments of equal size; inside a segment groups of
+//    equal (n, p) in (n desc, p desc) order; ld = roundup(n, 4), group stride
+//    roundup(n*ld, 64); segment size roundup(max used, 64).
+#include <algorithm>
+#include <cstring>
+#include <tuple>
+#include <vector>
+
+#include "internal.h"
+
+namespace shp {
+
+static int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static int64_t products_per_iteration(int p) {
+  switch (p) {
+    case 1: return 2;
+    case 2: return 3;
+    case 4: return 4;
+    default: return 5;
+  }
+}
+
+struct RootRef {
+  int64_t cost;
+  int32_t tensor, block, side;
+  int32_t n, p;
+};
+
+int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
+              int32_t world_size, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
+              shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
+              int64_t* segment_elems) {
+  if (!shapes || n_tensors < 0 || block_size < 1 || max_precond_dim < 1 || world_size < 1)
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: bad arguments");
+  std::vector<shampoo_block_t> blocks;
+  for (int32_t t = 0; t < n_tensors; ++t) {
+    const int64_t m = shapes[2 * t], n = shapes[2 * t + 1];
+    if (m < 1 || n < 1) return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: tensor %d has a zero dimension", t);
+    const bool left = m > 1 && m <= max_precond_dim;
+    const bool right = n > 1 && n <= max_precond_dim;
+    const int pl = left ? (right ? 4 : 2) : 0;
+    const int pr = right ? (left ? 4 : 2) : 0;
+    for (int64_t r0 = 0; r0 < m; r0 += block_size)
+      for (int64_t c0 = 0; c0 < n; c0 += block_size) {
+        shampoo_block_t b;
+        std::memset(&b, 0, sizeof b);
+        b.tensor_id = t;
+        b.row0 = r0;
+        b.col0 = c0;
+        b.rows = (int32_t)std::min<int64_t>(block_size, m - r0);
+        b.cols = (int32_t)std::min<int64_t>(block_size, n - c0);
+        b.p_left = pl;
+        b.p_right = pr;
+        b.owner_left = b.owner_right = -1;
+        b.left_off = b.right_off = -1;
+        b.left_ld = b.right_ld = 0;
+        blocks.push_back(b);
+      }
+  }
+  std::vector<RootRef> roots;
+  for (int32_t i = 0; i < (int32_t)blocks.size(); ++i) {
+    const shampoo_block_t& b = blocks[i];
+    if (b.p_left) {
+      const int64_t n = b.rows;
+      roots.push_back({n * n * n * products_per_iteration(b.p_left), b.tensor_id, i, 0, b.rows, b.p_left});
+    }
+    if (b.p_right) {
+      const int64_t n = b.cols;
+      roots.push_back({n * n * n * products_per_iteration(b.p_right), b.tensor_id, i, 1, b.cols, b.p_right});
+    }
+  }
+  std::stable_sort(roots.begin(), roots.end(), [](const RootRef& x, const RootRef& y) {
+    return std::make_tuple(-x.cost, x.tensor, x.block, x.side) < std::make_tuple(-y.cost, y.tensor, y.block, y.side);
+  });
+  // LPT owners
+  std::vector<int64_t> load(world_size, 0);
+  std::vector<std::vector<int32_t>> owned(world_size);  // indices into roots (sorted positions)
+  for (int32_t pos = 0; pos < (int32_t)roots.size(); ++pos) {
+    int r = 0;
+    for (int q = 1; q < world_size; ++q)
+      if (load[q] < load[r]) r = q;
+    load[r] += roots[pos].cost;
+    owned[r].push_back(pos);
+    shampoo_block_t& b = blocks[roots[pos].block];
+    if (roots[pos].side == 0) b.owner_left = r;
+    else b.owner_right = r;
+  }
+  // packing
+  std::vector<shampoo_group_t> groups;
+  std::vector<int64_t> used(world_size, 0);
+  for (int r = 0; r < world_size; ++r) {
+    std::vector<int32_t> items = owned[r];
+    std::stable_sort(items.begin(), items.end(), [&](int32_t a, int32_t c) {
+      const RootRef& x = roots[a];
+      const RootRef& y = roots[c];
+      return std::make_tuple(-x.n, -x.p, a) < std::make_tuple(-y.n, -y.p, c);
+    });
+    int64_t off = 0;
+    size_t i = 0;
+    while (i < items.size()) {
+      const int32_t n = roots[items[i]].n, p = roots[items[i]].p;
+      size_t j = i;
+      while (j < items.size() && roots[items[j]].n == n && roots[items[j]].p == p) ++j;
+      const int64_t ld = roundup(n, 4), stride = roundup((int64_t)n * ld, 64);
+      shampoo_group_t g;
+      g.owner = r;
+      g.n = n;
+      g.p = p;
+      g.count = (int32_t)(j - i);
+      g.offset = off;  // relative to the segment for now
+      g.stride = stride;
+      groups.push_back(g);
+      for (size_t k = i; k < j; ++k) {
+        const RootRef& rr = roots[items[k]];
+        shampoo_block_t& b = blocks[rr.block];
+        if (rr.side == 0) {
+          b.left_off = off + (int64_t)(k - i) * stride;
+          b.left_ld = (int32_t)ld;
+        } else {
+          b.right_off = off + (int64_t)(k - i) * stride;
+          b.right_ld = (int32_t)ld;
+        }
+      }
+      off += (int64_t)(j - i) * stride;
+      i = j;
+    }
+    used[r] = off;
+  }
+  const int64_t seg = roundup(world_size ? *std::max_element(used.begin(), used.end()) : 0, 64);
+  for (auto& g : groups) g.offset += (int64_t)g.owner * seg;
+  for (auto& b : blocks) {
+    if (b.left_off >= 0) b.left_off += (int64_t)b.owner_left * seg;
+    if (b.right_off >= 0) b.right_off += (int64_t)b.owner_right * seg;
+  }
+  if (n_blocks_out) *n_blocks_out = (int32_t)blocks.size();
+  if (n_groups_out) *n_groups_out = (int32_t)groups.size();
+  if (stats_elems) *stats_elems = seg * world_size;
+  if (segment_elems) *segment_elems = seg;
+  bool cap_ok = true;
+  if (out_blocks) {
+    if (capacity < (int32_t)blocks.size()) cap_ok = false;
+    else std::memcpy(out_blocks, blocks.data(), blocks.size() * sizeof(shampoo_block_t));
+  }
+  if (out_groups) {
+    if (group_capacity < (int32_t)groups.size()) cap_ok = false;
+    else std::memcpy(out_groups, groups.data(), groups.size() * sizeof(shampoo_group_t));
+  }
+  if (!cap_ok) return set_error(SHAMPOO_ERR_CAPACITY, "plan: output capacity too small (%zu blocks, %zu groups)",
+                                blocks.size(), groups.size());
+  return SHAMPOO_OK;
+}
+
+}  // namespace shp

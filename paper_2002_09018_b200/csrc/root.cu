@@ -1,0 +1,652 @@
+// root.cu -- batched epsilon-regularised inverse p-th roots by the coupled
+// Newton iteration (rows a3-a6), one cooperative persistent kernel per batch.
+//
+// Method ("Schur-Newton ... a sequence of matrix-vector and
+// matrix-matrix products", double precision; iteration of S:131; readings
+// #1-#4, #16, #18 of DESIGN.md):
+//   lambda_hat : power_iters power steps from the splitmix64 start vector
+//   A_hat = A + eps_rel*lambda_hat*I ; c = lambda_hat*(1+eps_rel)
+//   M_0 = A_hat / c ; X_0 = c^{-1/p} I
+//   k = 0, 1, ...: err_k = max|M_k - I| ; stop on err_k <= tol, stagnation
+//                  (err_k >= err_{k-1} < 1e-2 -> X_{k-1}) or k == max_iter
+//                  T_k = ((p+1)I - M_k)/p ; X_{k+1} = X_k T_k ; M_{k+1} = T_k^p M_k
+//
+// B200 design:
+//  * All iterates are symmetric polynomials in A_hat, so every product computes
+//    only the upper-triangle 128x128 tiles and mirror-stores them.
+//  * Products run on the FP64 tensor pipe (DMMA.8x8x4) through dmma_gemm.cuh.
+//  * One cooperative launch runs power iteration, setup, all iterations and
+//    the final fp32 write; grid.sync separates dependent products.  Each CTA
+//    keeps an identical copy of the active-matrix list (derived from the err
+//    history in global memory), so converged matrices stop issuing tiles with
+//    no host round trip.
+//  * The M-update epilogue fuses T_{k+1} = ((p+1)I - M_{k+1})/p and the
+//    max|M_{k+1} - I| reduction (warp max + one 64-bit atomicMax per warp).
+#include <cooperative_groups.h>
+
+#include "dmma_gemm.cuh"
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace shp {
+
+constexpr int kBufs = 7;  // X0, X1, M0, M1, T, S0, S1
+enum { BX0 = 0, BX1 = 1, BM0 = 2, BM1 = 3, BT = 4, BS0 = 5, BS1 = 6 };
+constexpr double kStagnationGate = 1e-2;
+constexpr int kMaxBatchPerLaunch = 2048;
+
+struct RootArgs {
+  const float* A;
+  int64_t lda, stride_a;
+  float* X;
+  int64_t ldx, stride_x;
+  int batch, n, np, p, max_iter, power_iters;
+  double eps_rel, tol;
+  shampoo_root_info_t* info;
+  double* bufs;  // batch * kBufs * np * np
+  double* lam;   // batch
+  double* errh;  // batch * (max_iter + 1)
+  int4* res;     // batch: {result buffer, iters, status, -}
+};
+
+SHP_DEV double* buf(const RootArgs& a, int mat, int b) {
+  return a.bufs + ((int64_t)mat * kBufs + b) * (int64_t)a.np * a.np;
+}
+
+// ------------------------------------------------------------ decisions
+enum { D_CONTINUE = 0, D_CONVERGED = 1, D_STAGNATED = 2, D_MAXITER = 3, D_NONFINITE = 4 };
+
+SHP_DEV int decide(const RootArgs& a, int mat, int k) {
+  const double* e = a.errh + (int64_t)mat * (a.max_iter + 1);
+  double ek = e[k];
+  if (!isfinite(ek)) return D_NONFINITE;
+  if (ek <= a.tol) return D_CONVERGED;
+  if (k >= 1) {
+    double ep = e[k - 1];
+    if (ek >= ep && ep < kStagnationGate) return D_STAGNATED;
+  }
+  if (k == a.max_iter) return D_MAXITER;
+  return D_CONTINUE;
+}
+
+// ------------------------------------------------------- power iteration
+SHP_DEV uint64_t splitmix64(uint64_t i) {
+  uint64_t z = i + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Deterministic block reduction (fixed lane/warp order); result broadcast.
+SHP_DEV double block_sum(double v, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = warp_sum_fixed(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) s = __dadd_rn(s, red[w]);
+  return s;
+}
+
+// One CTA: lambda_hat of matrix `mat` (smem: v[n], w[n], red[8]).
+SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
+  const int n = a.n;
+  double* v = smem;
+  double* w = smem + n;
+  double* red = smem + 2 * n;
+  const float* A = a.A + (int64_t)mat * a.stride_a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double part = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads) {
+    double x = (double)(splitmix64((uint64_t)i) >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    v[i] = x;
+    part = fma(x, x, part);
+  }
+  double nv = sqrt(block_sum(part, red));
+  for (int i = threadIdx.x; i < n; i += kThreads) v[i] = v[i] / nv;
+  __syncthreads();
+  double lam = 0.0;
+  const bool vec4 = ((a.lda & 3) == 0) && ((n & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  for (int it = 0; it < a.power_iters; ++it) {
+    for (int r = warp; r < n; r += kThreads / 32) {
+      const float* row = A + (int64_t)r * a.lda;
+      double acc = 0.0;
+      if (vec4) {
+#pragma unroll 4
+        for (int c = 4 * lane; c < n; c += 128) {
+          float4 q = __ldg(reinterpret_cast<const float4*>(row + c));
+          acc = fma((double)q.x, v[c], acc);
+          acc = fma((double)q.y, v[c + 1], acc);
+          acc = fma((double)q.z, v[c + 2], acc);
+          acc = fma((double)q.w, v[c + 3], acc);
+        }
+      } else {
+#pragma unroll 4
+        for (int c = lane; c < n; c += 32) acc = fma((double)__ldg(row + c), v[c], acc);
+      }
+      acc = warp_sum_fixed(acc);
+      if (lane == 0) w[r] = acc;
+    }
+    __syncthreads();
+    double pl = 0.0, pw = 0.0;
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+      pl = fma(v[i], w[i], pl);
+      pw = fma(w[i], w[i], pw);
+    }
+    lam = block_sum(pl, red);
+    double nw = sqrt(block_sum(pw, red));
+    if (!(nw != 0.0)) break;  // also stops on NaN (lam is then NaN)
+    for (int i = threadIdx.x; i < n; i += kThreads) v[i] = w[i] / nw;
+    __syncthreads();
+  }
+  __syncthreads();
+  return lam;
+}
+
+SHP_DEV double c_pow_neg_inv_p(double c, int p) {
+  switch (p) {
+    case 1: return 1.0 / c;
+    case 2: return 1.0 / sqrt(c);
+    case 4: return 1.0 / sqrt(sqrt(c));
+    default: return 1.0 / sqrt(sqrt(sqrt(c)));
+  }
+}
+
+SHP_DEV bool lam_ok(double lam) { return isfinite(lam) && lam > 0.0; }
+
+// ------------------------------------------------------------ epilogues
+enum { EPI_STORE = 0, EPI_MUPDATE = 1 };
+
+template <int MODE>
+SHP_DEV void epilogue(const RootArgs& a, const Acc& acc, int mat, int ti, int tj, double* dst, double* tdst,
+                      double* err_slot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int np = a.np, n = a.n;
+  const bool mirror = ti != tj;
+  const double inv_p = 1.0 / (double)a.p;
+  const double pp1 = (double)(a.p + 1);
+  double emax = 0.0;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const int i = ti * kTileM + acc_row(warp, lane, mt);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = tj * kTileM + acc_col(warp, lane, nt, 0);
+      const double c0 = acc.c[mt][nt][0], c1 = acc.c[mt][nt][1];
+      *reinterpret_cast<double2*>(dst + (int64_t)i * np + j) = make_double2(c0, c1);
+      if (mirror) {
+        dst[(int64_t)j * np + i] = c0;
+        dst[(int64_t)(j + 1) * np + i] = c1;
+      }
+      if (MODE == EPI_MUPDATE) {
+        const bool iv = i < n;
+        const bool v0 = iv && j < n, v1 = iv && j + 1 < n;
+        const double d0 = (i == j) ? 1.0 : 0.0, d1 = (i == j + 1) ? 1.0 : 0.0;
+        const double t0 = v0 ? (pp1 * d0 - c0) * inv_p : 0.0;
+        const double t1 = v1 ? (pp1 * d1 - c1) * inv_p : 0.0;
+        *reinterpret_cast<double2*>(tdst + (int64_t)i * np + j) = make_double2(t0, t1);
+        if (mirror) {
+          tdst[(int64_t)j * np + i] = t0;
+          tdst[(int64_t)(j + 1) * np + i] = t1;
+        }
+        if (v0) emax = fmax_nan(emax, fabs(c0 - d0));
+        if (v1) emax = fmax_nan(emax, fabs(c1 - d1));
+      }
+    }
+  }
+  if (MODE == EPI_MUPDATE) {
+    emax = warp_max(emax);
+    if (lane == 0) atomic_max_nonneg(err_slot, emax);
+  }
+}
+
+// Ordered compaction of the active list: keep act[pos] iff the matrix may
+// continue at check k.  Every CTA computes the same result from global state.
+SHP_DEV int compact(const RootArgs& a, int* act, int nact, int k, int* cnt, bool first) {
+  const int per = (nact + kThreads - 1) / kThreads;
+  const int b0 = threadIdx.x * per;
+  int mine[kMaxBatchPerLaunch / kThreads];
+  int nm = 0;
+  for (int q = 0; q < per; ++q) {
+    const int pos = b0 + q;
+    if (pos < nact) {
+      const int mat = act[pos];
+      const bool keep = (!first || lam_ok(a.lam[mat])) && decide(a, mat, k) == D_CONTINUE;
+      if (keep) mine[nm++] = mat;
+    }
+  }
+  cnt[threadIdx.x] = nm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int i = 0; i < kThreads; ++i) {
+      const int c = cnt[i];
+      cnt[i] = s;
+      s += c;
+    }
+    cnt[kThreads] = s;
+  }
+  __syncthreads();
+  const int out = cnt[threadIdx.x];
+  for (int q = 0; q < nm; ++q) act[out + q] = mine[q];
+  const int total = cnt[kThreads];
+  __syncthreads();
+  return total;
+}
+
+// ---------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int np = a.np, T = np / kTileM, tiles = T * (T + 1) / 2;
+  const int64_t np2 = (int64_t)np * np;
+
+  // ---- phase 0: power iteration (one CTA per matrix) + err history reset
+  for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
+    double* e = a.errh + (int64_t)mat * (a.max_iter + 1);
+    for (int k = threadIdx.x; k <= a.max_iter; k += kThreads) e[k] = 0.0;
+    double lam = power_iteration(a, mat, smem);
+    if (threadIdx.x == 0) a.lam[mat] = lam;
+  }
+  grid.sync();
+
+  // ---- phase 1: setup M_0, T_0, X_0 and err_0
+  {
+    const int64_t total = (int64_t)a.batch * np2;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < total; base += (int64_t)gridDim.x * kThreads) {
+      const int64_t idx = base + threadIdx.x;
+      double e = 0.0;
+      int mat = -1;
+      if (idx < total) {
+        mat = (int)(idx / np2);
+        const int64_t rem = idx - (int64_t)mat * np2;
+        const int i = (int)(rem / np), j = (int)(rem - (int64_t)i * np);
+        const double lam = a.lam[mat];
+        if (lam_ok(lam)) {
+          const double c = lam * (1.0 + a.eps_rel);
+          const bool valid = i < a.n && j < a.n;
+          double m = 0.0, t = 0.0, x = 0.0;
+          if (valid) {
+            // upper triangle (statistics are symmetric by construction)
+            const int r = i < j ? i : j, q = i < j ? j : i;
+            double av = (double)a.A[(int64_t)mat * a.stride_a + (int64_t)r * a.lda + q];
+            if (i == j) av = __dadd_rn(av, __dmul_rn(a.eps_rel, lam));  // (eps*lam) rounded, then added
+            m = av / c;
+            const double d = (i == j) ? 1.0 : 0.0;
+            t = ((double)(a.p + 1) * d - m) * (1.0 / (double)a.p);
+            x = (i == j) ? c_pow_neg_inv_p(c, a.p) : 0.0;
+            e = fabs(m - d);
+          }
+          buf(a, mat, BM0)[rem] = m;
+          buf(a, mat, BT)[rem] = t;
+          buf(a, mat, BX0)[rem] = x;
+        }
+      }
+      // warp-level max over the (possibly two) matrices touched by this warp
+      const int mat0 = __shfl_sync(0xffffffffu, mat, 0);
+      const bool same = __all_sync(0xffffffffu, mat == mat0 || mat < 0);
+      if (same) {
+        double w = warp_max(e);
+        if (lane == 0 && mat0 >= 0 && lam_ok(a.lam[mat0])) atomic_max_nonneg(a.errh + (int64_t)mat0 * (a.max_iter + 1), w);
+      } else if (mat >= 0 && lam_ok(a.lam[mat])) {
+        atomic_max_nonneg(a.errh + (int64_t)mat * (a.max_iter + 1), e);
+      }
+    }
+  }
+  grid.sync();
+
+  // ---- iterations
+  int* act = reinterpret_cast<int*>(smem + kGemmSmemDoubles);
+  int* cnt = act + kMaxBatchPerLaunch;  // 257 ints scratch
+  __shared__ int s_nact;
+  // initial active list: lam ok and decide(k=0) == continue
+  for (int i = threadIdx.x; i < a.batch; i += kThreads) act[i] = i;
+  __syncthreads();
+  s_nact = compact(a, act, a.batch, 0, cnt, /*first=*/true);
+  int nact = s_nact;
+  Acc acc;
+  for (int k = 0; nact > 0; ++k) {
+    const int xs = k & 1;  // X_k in BX0 + xs, M_k in BM0 + xs
+    const int tb = (a.p == 1) ? ((k & 1) ? BS0 : BT) : BT;
+    const int tb_next = (a.p == 1) ? ((k & 1) ? BT : BS0) : BT;
+    // P1: X_{k+1} = X_k T ; S0 = T T (p >= 2)
+    {
+      const int jobs = (a.p >= 2) ? 2 : 1;
+      const int items = nact * tiles * jobs;
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int pos = it / (tiles * jobs), rem = it - pos * tiles * jobs;
+        const int t = rem / jobs, job = rem - t * jobs;
+        const int mat = act[pos];
+        int ti, tj;
+        upper_tile(t, T, ti, tj);
+        const double* Aop = (job == 0) ? buf(a, mat, BX0 + xs) : buf(a, mat, tb);
+        const double* Bop = buf(a, mat, tb);
+        F64Rows la{Aop + (int64_t)ti * kTileM * np, np};
+        F64Rows lb{Bop + (int64_t)tj * kTileM * np, np};
+        gemm_tile(acc, la, lb, np / kTileK, smem);
+        double* dst = (job == 0) ? buf(a, mat, BX0 + (xs ^ 1)) : buf(a, mat, BS0);
+        epilogue<EPI_STORE>(a, acc, mat, ti, tj, dst, nullptr, nullptr);
+      }
+      grid.sync();
+    }
+    // squarings: S1 = S0^2 (p >= 4); S0 = S1^2 (p == 8)
+    for (int sq = 0; sq < ((a.p == 8) ? 2 : (a.p == 4 ? 1 : 0)); ++sq) {
+      const int src = (sq == 0) ? BS0 : BS1, dstb = (sq == 0) ? BS1 : BS0;
+      const int items = nact * tiles;
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int pos = it / tiles, t = it - pos * tiles;
+        const int mat = act[pos];
+        int ti, tj;
+        upper_tile(t, T, ti, tj);
+        const double* S = buf(a, mat, src);
+        F64Rows la{S + (int64_t)ti * kTileM * np, np};
+        F64Rows lb{S + (int64_t)tj * kTileM * np, np};
+        gemm_tile(acc, la, lb, np / kTileK, smem);
+        epilogue<EPI_STORE>(a, acc, mat, ti, tj, buf(a, mat, dstb), nullptr, nullptr);
+      }
+      grid.sync();
+    }
+    // P3: M_{k+1} = T^p M_k ; T_{k+1} ; err_{k+1}
+    {
+      const int tp = (a.p == 1) ? tb : (a.p == 2 ? BS0 : (a.p == 4 ? BS1 : BS0));
+      const int items = nact * tiles;
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int pos = it / tiles, t = it - pos * tiles;
+        const int mat = act[pos];
+        int ti, tj;
+        upper_tile(t, T, ti, tj);
+        F64Rows la{buf(a, mat, tp) + (int64_t)ti * kTileM * np, np};
+        F64Rows lb{buf(a, mat, BM0 + xs) + (int64_t)tj * kTileM * np, np};
+        gemm_tile(acc, la, lb, np / kTileK, smem);
+        epilogue<EPI_MUPDATE>(a, acc, mat, ti, tj, buf(a, mat, BM0 + (xs ^ 1)), buf(a, mat, tb_next),
+                              a.errh + (int64_t)mat * (a.max_iter + 1) + (k + 1));
+      }
+      grid.sync();
+    }
+    // next active list (ordered compaction; identical in every CTA)
+    nact = compact(a, act, nact, k + 1, cnt, false);
+  }
+
+  // ---- finalize: per-matrix decision, then fp32 output
+  for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const double lam = a.lam[mat];
+      int status, iters = 0, rbuf = -1;
+      double err = __longlong_as_double(0x7ff8000000000000LL);
+      if (!isfinite(lam)) {
+        status = 2;
+      } else if (!(lam > 0.0)) {
+        status = 3;
+      } else {
+        int k = 0;
+        for (;; ++k) {
+          int d = decide(a, mat, k);
+          if (d == D_CONTINUE) continue;
+          const double* e = a.errh + (int64_t)mat * (a.max_iter + 1);
+          if (d == D_CONVERGED) { status = 0; iters = k; rbuf = BX0 + (k & 1); err = e[k]; }
+          else if (d == D_STAGNATED) { status = 1; iters = k - 1; rbuf = BX0 + ((k - 1) & 1); err = e[k - 1]; }
+          else if (d == D_MAXITER) { status = 1; iters = k; rbuf = BX0 + (k & 1); err = e[k]; }
+          else { status = 2; iters = k; rbuf = -1; err = e[k]; }
+          break;
+        }
+      }
+      a.res[mat] = make_int4(rbuf, iters, status, 0);
+      shampoo_root_info_t inf;
+      inf.iters = iters;
+      inf.status = status;
+      inf.lambda_max = lam;
+      inf.err = err;
+      a.info[mat] = inf;
+    }
+  }
+  grid.sync();
+  {
+    const int n = a.n;
+    const int64_t nn = (int64_t)n * n, total = (int64_t)a.batch * nn;
+    for (int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kThreads) {
+      const int mat = (int)(idx / nn);
+      const int64_t rem = idx - (int64_t)mat * nn;
+      const int i = (int)(rem / n), j = (int)(rem - (int64_t)i * n);
+      const int4 r = a.res[mat];
+      float* out = a.X + (int64_t)mat * a.stride_x + (int64_t)i * a.ldx + j;
+      if (r.z == 3) *out = (i == j) ? 1.0f : 0.0f;
+      else if (r.x >= 0) *out = (float)buf(a, mat, r.x)[(int64_t)i * np + j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int padded(int n) { return (n + kTileM - 1) / kTileM * kTileM; }
+
+size_t root_workspace_bytes(int batch, int n, int max_iter) {
+  const size_t np = (size_t)padded(n);
+  return align256((size_t)batch * kBufs * np * np * sizeof(double)) + align256((size_t)batch * sizeof(double)) +
+         align256((size_t)batch * (max_iter + 1) * sizeof(double)) + align256((size_t)batch * sizeof(int4));
+}
+
+size_t root_smem_bytes(int n) {
+  size_t gemm = (size_t)kGemmSmemDoubles * sizeof(double) + (kMaxBatchPerLaunch + kThreads + 1) * sizeof(int);
+  size_t pi = (2 * (size_t)n + 8) * sizeof(double);
+  return gemm > pi ? gemm : pi;
+}
+
+int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
+                int n, int p, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
+                void* ws, cudaStream_t stream, int64_t* launches) {
+  static size_t configured_smem = 0;
+  const size_t smem = root_smem_bytes(n);
+  if (smem > configured_smem) {
+    if (cudaFuncSetAttribute(root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(root_kernel)");
+    configured_smem = smem;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, root_kernel, kThreads, smem) != cudaSuccess || per_sm < 1)
+    return set_error(SHAMPOO_ERR_UNSUPPORTED, "root_kernel cannot be resident (smem %zu)", smem);
+  const int np = padded(n);
+  char* w = static_cast<char*>(ws);
+  const size_t full = root_workspace_bytes(batch, n, max_iter);
+  (void)full;
+  for (int b0 = 0; b0 < batch; b0 += kMaxBatchPerLaunch) {
+    const int bc = (batch - b0 < kMaxBatchPerLaunch) ? batch - b0 : kMaxBatchPerLaunch;
+    RootArgs a;
+    a.A = A + (int64_t)b0 * stride_a;
+    a.lda = lda;
+    a.stride_a = stride_a;
+    a.X = X + (int64_t)b0 * stride_x;
+    a.ldx = ldx;
+    a.stride_x = stride_x;
+    a.batch = bc;
+    a.n = n;
+    a.np = np;
+    a.p = p;
+    a.max_iter = max_iter;
+    a.power_iters = power_iters;
+    a.eps_rel = eps_rel;
+    a.tol = tol;
+    a.info = info + b0;
+    char* q = w;
+    a.bufs = reinterpret_cast<double*>(q);
+    q += align256((size_t)bc * kBufs * np * np * sizeof(double));
+    a.lam = reinterpret_cast<double*>(q);
+    q += align256((size_t)bc * sizeof(double));
+    a.errh = reinterpret_cast<double*>(q);
+    q += align256((size_t)bc * (max_iter + 1) * sizeof(double));
+    a.res = reinterpret_cast<int4*>(q);
+    void* args[] = {&a};
+    const int grid = num_sms() * per_sm;
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kThreads), args, smem, stream);
+    if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_kernel)", e);
+    ++*launches;
+  }
+  return SHAMPOO_OK;
+}
+
+// ======================================================= residual check
+// residual_i = || X_i^p (A_i + eps*lambda_i I) - I ||_F in fp64 (config 2's
+// "residual check"; the north star's invariant).  Cooperative kernel:
+// convert -> log2(p) symmetric squarings -> full product with A_hat -> sums.
+constexpr int kResBufs = 4;  // Y0 (X), Y1, Y2, Ahat
+
+struct ResArgs {
+  const float* A;
+  int64_t lda, stride_a;
+  const float* X;
+  int64_t ldx, stride_x;
+  int batch, n, np, p;
+  double eps_rel;
+  const shampoo_root_info_t* info;
+  double* out;
+  double* bufs;  // batch * 4 * np^2
+  double* part;  // batch * T^2
+};
+
+SHP_DEV double* rbuf(const ResArgs& a, int mat, int b) {
+  return a.bufs + ((int64_t)mat * kResBufs + b) * (int64_t)a.np * a.np;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int np = a.np, n = a.n, T = np / kTileM, tiles = T * (T + 1) / 2;
+  const int64_t np2 = (int64_t)np * np, total = (int64_t)a.batch * np2;
+  for (int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kThreads) {
+    const int mat = (int)(idx / np2);
+    const int64_t rem = idx - (int64_t)mat * np2;
+    const int i = (int)(rem / np), j = (int)(rem - (int64_t)i * np);
+    const bool valid = i < n && j < n;
+    double x = 0.0, ah = 0.0;
+    if (valid) {
+      x = (double)a.X[(int64_t)mat * a.stride_x + (int64_t)i * a.ldx + j];
+      const int r = i < j ? i : j, q = i < j ? j : i;
+      ah = (double)a.A[(int64_t)mat * a.stride_a + (int64_t)r * a.lda + q];
+      if (i == j) ah = __dadd_rn(ah, __dmul_rn(a.eps_rel, a.info[mat].lambda_max));
+    }
+    rbuf(a, mat, 0)[rem] = x;
+    rbuf(a, mat, 3)[rem] = ah;
+  }
+  grid.sync();
+  int src = 0;
+  Acc acc;
+  for (int q = a.p; q > 1; q >>= 1) {
+    const int dst = (src == 1) ? 2 : 1;
+    for (int it = blockIdx.x; it < a.batch * tiles; it += gridDim.x) {
+      const int mat = it / tiles, t = it - mat * tiles;
+      int ti, tj;
+      upper_tile(t, T, ti, tj);
+      const double* S = rbuf(a, mat, src);
+      F64Rows la{S + (int64_t)ti * kTileM * np, np};
+      F64Rows lb{S + (int64_t)tj * kTileM * np, np};
+      gemm_tile(acc, la, lb, np / kTileK, smem);
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      double* D = rbuf(a, mat, dst);
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const int i = ti * kTileM + acc_row(warp, lane, mt);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int j = tj * kTileM + acc_col(warp, lane, nt, 0);
+          *reinterpret_cast<double2*>(D + (int64_t)i * np + j) = make_double2(acc.c[mt][nt][0], acc.c[mt][nt][1]);
+          if (ti != tj) {
+            D[(int64_t)j * np + i] = acc.c[mt][nt][0];
+            D[(int64_t)(j + 1) * np + i] = acc.c[mt][nt][1];
+          }
+        }
+      }
+    }
+    grid.sync();
+    src = dst;
+  }
+  __shared__ double red[kThreads / 32];
+  for (int it = blockIdx.x; it < a.batch * T * T; it += gridDim.x) {
+    const int mat = it / (T * T), t = it - mat * T * T;
+    const int ti = t / T, tj = t - ti * T;
+    F64Rows la{rbuf(a, mat, src) + (int64_t)ti * kTileM * np, np};
+    F64Rows lb{rbuf(a, mat, 3) + (int64_t)tj * kTileM * np, np};
+    gemm_tile(acc, la, lb, np / kTileK, smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double s = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int i = ti * kTileM + acc_row(warp, lane, mt);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = tj * kTileM + acc_col(warp, lane, nt, e);
+          if (i < n && j < n) {
+            const double d = acc.c[mt][nt][e] - ((i == j) ? 1.0 : 0.0);
+            s = fma(d, d, s);
+          }
+        }
+    }
+    s = warp_sum_fixed(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t2 = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) t2 = __dadd_rn(t2, red[w]);
+      a.part[(int64_t)mat * T * T + t] = t2;
+    }
+    __syncthreads();
+  }
+  grid.sync();
+  for (int mat = blockIdx.x * kThreads + threadIdx.x; mat < a.batch; mat += gridDim.x * kThreads) {
+    double s = 0.0;
+    for (int t = 0; t < T * T; ++t) s = __dadd_rn(s, a.part[(int64_t)mat * T * T + t]);
+    a.out[mat] = sqrt(s);
+  }
+}
+
+size_t residual_workspace_bytes(int batch, int n) {
+  const size_t np = (size_t)padded(n), T = np / kTileM;
+  return align256((size_t)batch * kResBufs * np * np * sizeof(double)) + align256((size_t)batch * T * T * sizeof(double));
+}
+
+int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* X, int64_t ldx, int64_t stride_x,
+                    int batch, int n, int p, double eps_rel, const shampoo_root_info_t* info, double* residual,
+                    void* ws, cudaStream_t stream, int64_t* launches) {
+  const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(residual_kernel)");
+    configured = true;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, residual_kernel, kThreads, smem) != cudaSuccess || per_sm < 1)
+    return set_error(SHAMPOO_ERR_UNSUPPORTED, "residual_kernel cannot be resident");
+  ResArgs a;
+  a.A = A;
+  a.lda = lda;
+  a.stride_a = stride_a;
+  a.X = X;
+  a.ldx = ldx;
+  a.stride_x = stride_x;
+  a.batch = batch;
+  a.n = n;
+  a.np = padded(n);
+  a.p = p;
+  a.eps_rel = eps_rel;
+  a.info = info;
+  a.out = residual;
+  const size_t np = (size_t)a.np;
+  char* q = static_cast<char*>(ws);
+  a.bufs = reinterpret_cast<double*>(q);
+  q += align256((size_t)batch * kResBufs * np * np * sizeof(double));
+  a.part = reinterpret_cast<double*>(q);
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)residual_kernel, dim3(num_sms() * per_sm), dim3(kThreads),
+                                              args, smem, stream);
+  if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(residual_kernel)", e);
+  ++*launches;
+  return SHAMPOO_OK;
+}
+
+}  // namespace shp

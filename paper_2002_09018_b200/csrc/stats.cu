@@ -1,0 +1,241 @@
+// stats.cu -- per-step Shampoo statistics (row a2): L/R EMA update under the
+// sequential fp64 contract (bit-exact with the oracle), the diagonal AdaGrad
+// accumulator D and the per-block graft numerator.
+//
+// Alg. 1:  L <- decay*L + weight*G G^T ; R <- decay*R + weight*G^T G ;
+//                      D <- D + G o G ;  num_b = sum g^2 / max(D, 1e-30)
+// Contract (oracle/csrc/oracle_stats.c): acc = sum_k ascending of
+// (double)a_k*(double)b_k in fp64; t1 = weight*acc; t2 = decay*old; (float)(t1+t2).
+//
+// Launch sequence (one step, all blocks of all tensors):
+//   memset(flags) -> check (non-finite G per block) -> prep (tile prefix sums)
+//   -> stats (persistent DMMA tiles, L and R, owned blocks only)
+//   -> diag (D update + per-chunk graft partials) -> finish (fixed-order sums)
+#include "dmma_gemm.cuh"
+#include "internal.h"
+
+namespace shp {
+
+constexpr int kChunks = 64;  // row chunks per block for the elementwise passes
+
+struct StatsWs {
+  int* flag;         // n_blocks (non-finite marker)
+  int64_t* prefix;   // n_blocks + 1 (stats tiles)
+  double* part;      // n_blocks * kChunks
+};
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t stats_workspace_bytes(int n_blocks) {
+  return al((size_t)n_blocks * sizeof(int)) + al((size_t)(n_blocks + 1) * sizeof(int64_t)) +
+         al((size_t)n_blocks * kChunks * sizeof(double));
+}
+
+static StatsWs carve(void* ws, int n_blocks) {
+  char* q = static_cast<char*>(ws);
+  StatsWs w;
+  w.flag = reinterpret_cast<int*>(q);
+  q += al((size_t)n_blocks * sizeof(int));
+  w.prefix = reinterpret_cast<int64_t*>(q);
+  q += al((size_t)(n_blocks + 1) * sizeof(int64_t));
+  w.part = reinterpret_cast<double*>(q);
+  return w;
+}
+
+SHP_DEV int tiles_of(int n) { return (n + kTileM - 1) / kTileM; }
+SHP_DEV int64_t upper_count(int n) {
+  const int64_t T = tiles_of(n);
+  return T * (T + 1) / 2;
+}
+
+// ----------------------------------------------------- non-finite check
+__global__ void __launch_bounds__(kThreads) check_kernel(const shampoo_tensor_t* tensors,
+                                                         const shampoo_block_t* blocks, int* flag) {
+  const int b = blockIdx.x / kChunks, c = blockIdx.x % kChunks;
+  const shampoo_block_t blk = blocks[b];
+  const shampoo_tensor_t ten = tensors[blk.tensor_id];
+  const int rows_per = (blk.rows + kChunks - 1) / kChunks;
+  const int r0 = c * rows_per, r1 = min(blk.rows, r0 + rows_per);
+  if (r0 >= r1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int bad = 0;
+  for (int r = r0 + warp; r < r1; r += kThreads / 32) {
+    const float* row = ten.G + (blk.row0 + r) * ten.ldg + blk.col0;
+    for (int col = lane; col < blk.cols; col += 32) bad |= !isfinite(__ldg(row + col));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag + b, 1);
+}
+
+// ----------------------------------------------------- tile prefix sums
+// Single CTA of 1024 threads: chunked exclusive scan of per-block tile counts.
+__global__ void __launch_bounds__(1024) prep_kernel(const shampoo_block_t* blocks, int n_blocks, int only_owner,
+                                                    int64_t* prefix) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int per = (n_blocks + 1023) / 1024;
+  const int b0 = t * per, b1 = min(n_blocks, b0 + per);
+  int64_t s = 0;
+  for (int b = b0; b < b1; ++b) {
+    const shampoo_block_t blk = blocks[b];
+    if (blk.p_left && (only_owner < 0 || blk.owner_left == only_owner)) s += upper_count(blk.rows);
+    if (blk.p_right && (only_owner < 0 || blk.owner_right == only_owner)) s += upper_count(blk.cols);
+  }
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const int64_t v = part[i];
+      part[i] = acc;
+      acc += v;
+    }
+    prefix[n_blocks] = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int b = b0; b < b1; ++b) {
+    prefix[b] = acc;
+    const shampoo_block_t blk = blocks[b];
+    if (blk.p_left && (only_owner < 0 || blk.owner_left == only_owner)) acc += upper_count(blk.rows);
+    if (blk.p_right && (only_owner < 0 || blk.owner_right == only_owner)) acc += upper_count(blk.cols);
+  }
+}
+
+SHP_DEV int find_block(const int64_t* prefix, int n_blocks, int64_t item) {
+  int lo = 0, hi = n_blocks - 1;  // largest b with prefix[b] <= item
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------ statistics
+__global__ void __launch_bounds__(kThreads, 1)
+    stats_kernel(const shampoo_tensor_t* tensors, const shampoo_block_t* blocks, int n_blocks, int only_owner,
+                 float* stats, double decay, double weight, const int* flag, const int64_t* prefix) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t total = prefix[n_blocks];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Acc acc;
+  for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
+    const int b = find_block(prefix, n_blocks, item);
+    const shampoo_block_t blk = blocks[b];
+    if (flag[b]) continue;  // uniform across the CTA
+    int64_t local = item - prefix[b];
+    const bool has_l = blk.p_left && (only_owner < 0 || blk.owner_left == only_owner);
+    int side = 1;
+    if (has_l) {
+      const int64_t nl = upper_count(blk.rows);
+      if (local < nl) side = 0;
+      else local -= nl;
+    }
+    const int nvalid = side == 0 ? blk.rows : blk.cols;
+    const int K = side == 0 ? blk.cols : blk.rows;
+    int ti, tj;
+    upper_tile((int)local, tiles_of(nvalid), ti, tj);
+    const shampoo_tensor_t ten = tensors[blk.tensor_id];
+    const float* gb = ten.G + blk.row0 * ten.ldg + blk.col0;
+    F32Panel la{gb, ten.ldg, side, ti * kTileM, nvalid, K};
+    F32Panel lb{gb, ten.ldg, side, tj * kTileM, nvalid, K};
+    gemm_tile(acc, la, lb, (K + kTileK - 1) / kTileK, smem);
+    // epilogue: EMA with the fixed rounding sequence, upper triangle + mirror
+    float* S = stats + (side == 0 ? blk.left_off : blk.right_off);
+    const int64_t ld = side == 0 ? blk.left_ld : blk.right_ld;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int i = ti * kTileM + acc_row(warp, lane, mt);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = tj * kTileM + acc_col(warp, lane, nt, e);
+          if (i < nvalid && j < nvalid && i <= j) {
+            const double old = (double)S[(int64_t)i * ld + j];
+            const double t1 = __dmul_rn(weight, acc.c[mt][nt][e]);
+            const double t2 = __dmul_rn(decay, old);
+            const float r = __double2float_rn(__dadd_rn(t1, t2));
+            S[(int64_t)i * ld + j] = r;
+            if (i != j) S[(int64_t)j * ld + i] = r;
+          }
+        }
+    }
+  }
+}
+
+// ------------------------------------------------ D update + graft partials
+__global__ void __launch_bounds__(kThreads) diag_kernel(const shampoo_tensor_t* tensors,
+                                                        const shampoo_block_t* blocks, const int* flag,
+                                                        double* part) {
+  const int b = blockIdx.x / kChunks, c = blockIdx.x % kChunks;
+  __shared__ double red[kThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const shampoo_block_t blk = blocks[b];
+  const shampoo_tensor_t ten = tensors[blk.tensor_id];
+  const int rows_per = (blk.rows + kChunks - 1) / kChunks;
+  const int r0 = c * rows_per, r1 = min(blk.rows, r0 + rows_per);
+  double num = 0.0;
+  if (!flag[b] && ten.D != nullptr && r0 < r1) {
+    for (int r = r0 + warp; r < r1; r += kThreads / 32) {
+      const float* grow = ten.G + (blk.row0 + r) * ten.ldg + blk.col0;
+      float* drow = ten.D + (blk.row0 + r) * ten.ldd + blk.col0;
+      for (int col = lane; col < blk.cols; col += 32) {
+        const double g = (double)__ldg(grow + col);
+        const double gg = __dmul_rn(g, g);
+        const float dn = __double2float_rn(__dadd_rn((double)drow[col], gg));
+        drow[col] = dn;
+        const double den = (double)dn > 1e-30 ? (double)dn : 1e-30;
+        num = __dadd_rn(num, __ddiv_rn(gg, den));
+      }
+    }
+  }
+  num = warp_sum_fixed(num);
+  if (lane == 0) red[warp] = num;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s = __dadd_rn(s, red[w]);
+    part[(int64_t)b * kChunks + c] = s;
+  }
+}
+
+__global__ void finish_kernel(int n_blocks, const int* flag, const double* part, double* graft_num,
+                              int32_t* block_status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_blocks) return;
+  double s = 0.0;
+  for (int c = 0; c < kChunks; ++c) s = __dadd_rn(s, part[(int64_t)b * kChunks + c]);
+  if (graft_num) graft_num[b] = flag[b] ? 0.0 : s;
+  if (block_status) block_status[b] = flag[b] ? 2 : 0;
+}
+
+int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_block_t* blocks, int n_blocks,
+                 int only_owner, float* stats, double decay, double weight, double* graft_num, int32_t* block_status,
+                 void* ws, cudaStream_t stream, int64_t* launches) {
+  (void)n_tensors;
+  if (n_blocks == 0) return SHAMPOO_OK;
+  StatsWs w = carve(ws, n_blocks);
+  static bool configured = false;
+  const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
+  if (!configured) {
+    if (cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(stats_kernel)");
+    configured = true;
+  }
+  if (cudaMemsetAsync(w.flag, 0, (size_t)n_blocks * sizeof(int), stream) != cudaSuccess)
+    return set_cuda_error("cudaMemsetAsync");
+  const unsigned eg = (unsigned)n_blocks * kChunks;
+  check_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.flag);
+  prep_kernel<<<1, 1024, 0, stream>>>(blocks, n_blocks, only_owner, w.prefix);
+  stats_kernel<<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, only_owner, stats, decay, weight,
+                                                      w.flag, w.prefix);
+  diag_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.flag, w.part);
+  finish_kernel<<<(n_blocks + 255) / 256, 256, 0, stream>>>(n_blocks, w.flag, w.part, graft_num, block_status);
+  *launches += 5;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("stats kernels", e);
+  return SHAMPOO_OK;
+}
+
+}  // namespace shp

@@ -83,7 +83,8 @@ def wishart(n: int, seed: int, k: int | None = None) -> np.ndarray:
     (the "very large condition numbers" of P:211-214 / Fig. 2)."""
     k = max(1, n // 2) if k is None else k
     W = rng(seed).standard_normal((n, k))
-    return (W @ W.T).astype(np.float32)
+    S = W @ W.T
+    return ((S + S.T) * 0.5).astype(np.float32)  # exactly symmetric, like every statistic
 
 
 def spectrum(n: int, seed: int, decades: float = 8.0) -> np.ndarray:
@@ -92,7 +93,8 @@ def spectrum(n: int, seed: int, decades: float = 8.0) -> np.ndarray:
     Q, R = np.linalg.qr(g.standard_normal((n, n)))
     Q = Q * np.sign(np.diag(R))
     lam = 10.0 ** (-decades * np.arange(n) / max(1, n - 1))
-    return ((Q * lam) @ Q.T).astype(np.float32)
+    S = (Q * lam) @ Q.T
+    return ((S + S.T) * 0.5).astype(np.float32)
 
 
 def psd_batch(n: int, count: int, seed: int, kind: str = "mixed") -> np.ndarray:
@@ -123,7 +125,8 @@ def wishart_batch_device(n: int, count: int, seed: int, device, k: int | None = 
     for s in range(0, count, chunk):
         e = min(count, s + chunk)
         W = torch.randn((e - s, n, k), generator=gen, device=device, dtype=torch.float64)
-        out[s:e] = torch.bmm(W, W.transpose(1, 2)).to(torch.float32)
+        S = torch.bmm(W, W.transpose(1, 2))
+        out[s:e] = ((S + S.transpose(1, 2)) * 0.5).to(torch.float32)
     return out
 
 

@@ -1,0 +1,124 @@
+"""C-ABI checks that need no GPU: the in-tree library loads, exports every
+function declared in include/shampoo.h, its host-side plan is bit-exact with
+the oracle plan, and host-checkable errors return status codes without
+touching the device."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import plan as oplan
+from synth import transformer_big_shapes
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def shp():
+    from paper_2002_09018_b200 import build
+    build.build()
+    import paper_2002_09018_b200 as shp
+    return shp
+
+
+def test_library_exports_every_declared_symbol(shp):
+    from paper_2002_09018_b200 import _lib
+    header = open(os.path.join(ROOT, "include", "shampoo.h")).read()
+    declared = sorted(set(re.findall(r"\b(shampoo_[a-z_0-9]+)\s*\(", header)))
+    assert len(declared) >= 12
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(_lib.EXPORTED) == declared
+    assert L.shampoo_abi_version() == 1
+
+
+def _fields_equal(lib_plan, o):
+    assert lib_plan.n_blocks == len(o.blocks)
+    for b, ob in zip(lib_plan.blocks, o.blocks):
+        got = (int(b["tensor_id"]), int(b["row0"]), int(b["col0"]), int(b["rows"]), int(b["cols"]),
+               int(b["p_left"]), int(b["p_right"]), int(b["owner_left"]), int(b["owner_right"]),
+               int(b["left_off"]), int(b["right_off"]), int(b["left_ld"]), int(b["right_ld"]))
+        want = (ob.tensor_id, ob.row0, ob.col0, ob.rows, ob.cols, ob.p_left, ob.p_right, ob.owner_left,
+                ob.owner_right, ob.left_off, ob.right_off, ob.left_ld, ob.right_ld)
+        assert got == want
+    assert lib_plan.stats_elems == o.stats_elems and lib_plan.segment_elems == o.segment_elems
+    got_g = [tuple(int(g[k]) for k in ("owner", "n", "p", "offset", "count", "stride")) for g in lib_plan.groups]
+    want_g = [(g.owner, g.n, g.p, g.offset, g.count, g.stride) for g in o.groups]
+    assert got_g == want_g
+
+
+CASES = [
+    ([s for _, s in transformer_big_shapes()], 1024, 8192),
+    ([s for _, s in transformer_big_shapes()], 1024, 4096),
+    ([s for _, s in transformer_big_shapes()], 128, 8192),
+    ([(32000, 1024)], 1024, 8192),
+    ([(1, 10), (10, 1), (1, 1), (7, 9), (1000, 300), (9000, 7)], 64, 8192),
+    ([(512, 2048)], 1024, 4096),
+]
+
+
+@pytest.mark.parametrize("W", [1, 2, 3, 8])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_plan_bit_exact_vs_oracle(shp, case, W):
+    shapes, b, mpd = CASES[case]
+    _fields_equal(shp.make_plan(shapes, b, mpd, W), oplan.plan(shapes, b, mpd, W))
+
+
+def test_plan_capacity_and_invalid(shp):
+    from paper_2002_09018_b200 import _lib
+    L = _lib.lib()
+    sh = np.array([[4, 4]], np.int64)
+    nb = np.zeros(1, np.int32)
+    ng = np.zeros(1, np.int32)
+    se = np.zeros(1, np.int64)
+    sg = np.zeros(1, np.int64)
+    blocks = np.zeros(1, _lib.BLOCK_DTYPE)
+    rc = L.shampoo_plan(sh.ctypes.data, 1, 2, 8192, 1, blocks.ctypes.data, 1, nb.ctypes.data, None, 0,
+                        ng.ctypes.data, se.ctypes.data, sg.ctypes.data)
+    assert rc == 5 and nb[0] == 4  # CAPACITY, counts still written
+    bad = np.array([[0, 4]], np.int64)
+    assert L.shampoo_plan(bad.ctypes.data, 1, 2, 8192, 1, None, 0, nb.ctypes.data, None, 0, ng.ctypes.data,
+                          se.ctypes.data, sg.ctypes.data) == 1
+    assert b"zero dimension" in L.shampoo_last_error()
+
+
+def test_host_checked_errors_need_no_device(shp):
+    from paper_2002_09018_b200 import _lib
+    L = _lib.lib()
+    fake = 1 << 40  # never dereferenced: validation fails first
+    # p not in {1,2,4,8}
+    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 3, 1e-6, 1e-7, 100, 100, fake, fake,
+                                              1 << 30, None) == 1
+    assert b"p = 3" in L.shampoo_last_error()
+    # n out of range
+    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 0, 4, 1e-6, 1e-7, 100, 100, fake, fake,
+                                              1 << 30, None) == 1
+    # non-finite eps
+    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 4, float("nan"), 1e-7, 100, 100, fake,
+                                              fake, 1 << 30, None) == 1
+    # workspace too small
+    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 4, 1e-6, 1e-7, 100, 100, fake, fake,
+                                              16, None) == 4
+    # statistics: non-finite decay
+    assert L.shampoo_stats_update(fake, 1, fake, 1, -1, fake, float("inf"), 1.0, None, None, fake, 1 << 30,
+                                  None) == 1
+    # empty batch is a no-op
+    assert L.shampoo_inverse_pth_root_batched(None, 0, 0, None, 0, 0, 0, 8, 4, 1e-6, 1e-7, 100, 100, None, None, 0,
+                                              None) == 0
+    # workspace sizes are pure host functions
+    assert L.shampoo_root_workspace_bytes(2, 1024, 4, 100) >= 2 * 7 * 1024 * 1024 * 8
+    assert L.shampoo_stats_workspace_bytes(10) > 0
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2002_09018_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+                assert "liboracle" not in src and "oracle_stats" not in re.sub(r"(#|//).*", "", src), f
