@@ -1,0 +1,344 @@
+"""bench.py -- the hot path of distributed Shampoo on B200, one JSON line.
+
+Workload (BASELINE.json configs[2], the configuration the metric is quoted on):
+Transformer-Big (99 matrix parameters, 375.1M of P:494's 375.4M), block size
+1024, max_precond_dim 8192 -> 360 blocks, 528 inverse-4th roots + 96
+inverse-square roots of 1024^2 statistics.  One STEP = the whole hot path:
+  a2 statistics (owned blocks) + D + graft numerator
+  a3-a6 root refresh of every owned statistic (power iteration + coupled Newton)
+  a7 NCCL all-gather of the packed roots (N > 1)
+  a8-a9 preconditioned gradient + graft scale for every block.
+value = inverse-4th-roots of 1024^2 blocks completed per second of step time
+(whole job, all ranks; the step time also contains everything else above).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "inverse-4th-roots/sec @1024² blocks (1/2/4/8 B200); Shampoo step ms, Transformer-Big"
+UNIT = "roots/s"
+BLOCK = 1024
+MAX_PRECOND = 8192
+KAPPA_REFRESH = 500  # root refresh interval of the paper's Transformer runs
+FP64_DMMA_PEAK_TFLOPS = 37.1  # measured: tools/microbench/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tol", type=float, default=1e-7)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_root_baseline(seconds: float = 12.0, n: int = 1024):
+    """The CPU fp64 oracle (as it stands) on a bounded sample of the workload."""
+    import threadpoolctl
+
+    from oracle import root as oroot
+    A = synth.wishart(n, synth.BASE_SEED + 2).astype(np.float64)
+    info = threadpoolctl.threadpool_info()
+    cores = max([int(i.get("num_threads", 1)) for i in info] + [1])
+    t0 = time.perf_counter()
+    done = 0
+    iters = []
+    while True:
+        _, inf = oroot.inverse_pth_root(A, 4)
+        iters.append(inf.iters)
+        done += 1
+        if time.perf_counter() - t0 >= seconds or done >= 8:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} inverse-4th-roots of a {n}^2 Wishart statistic (kappa~1e6), numpy fp64 "
+                      f"coupled Newton, {np.mean(iters):.0f} iterations, {dt:.1f} s"}
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cpu = oracle_root_baseline(seconds=6.0)
+    samples = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        from oracle import root as oroot
+        A = synth.wishart(BLOCK, synth.BASE_SEED + 2 + i).astype(np.float64)
+        oroot.inverse_pth_root(A, 4)
+        if i >= args.warmup:
+            samples.append(time.perf_counter() - t0)
+    t = float(np.mean(samples))
+    value = 1.0 / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "transformer_big_b1024_root_sample", "step": "one 1024^2 inverse-4th-root "
+                       "(bounded sample of the Transformer-Big refresh)", "block_size": BLOCK},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu["cores"], "kind": "oracle",
+                             "sample": f"one 1024^2 Wishart inverse-4th-root per step, {args.steps} timed steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2002_09018_b200 as shp
+    from paper_2002_09018_b200 import dist as sdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    names_shapes = synth.transformer_big_shapes()
+    shapes = [s for _, s in names_shapes]
+    plan = shp.make_plan(shapes, BLOCK, MAX_PRECOND, world)
+    n_p4 = int(sum((plan.blocks["p_left"] == 4).sum() + (plan.blocks["p_right"] == 4).sum() for _ in [0]))
+    # gradients (device), vocab tensors row-sparse (Zipf ids), others low-rank + noise
+    Gs = []
+    for i, (name, (m, n)) in enumerate(names_shapes):
+        seed = synth.BASE_SEED + 3 + i
+        if m == synth.VOCAB:
+            Gs.append(synth.vocab_gradient_device(m, n, seed, dev))
+        else:
+            Gs.append(synth.lowrank_gradient_device(m, n, seed, dev))
+    Ds = [torch.zeros_like(G) for G in Gs]
+    Ps = [torch.zeros_like(G) for G in Gs]
+    table = shp.TensorTable(Gs, Ds, Ps)
+    stats = torch.zeros(plan.stats_elems, dtype=torch.float32, device=dev)
+    roots = torch.zeros_like(stats)
+    nb = plan.n_blocks
+    gnum = torch.zeros(nb, dtype=torch.float64, device=dev)
+    gscale = torch.zeros(nb, dtype=torch.float32, device=dev)
+    # statistics accumulated over 8 steps before the timed refreshes (config 3 recipe)
+    for _ in range(8):
+        shp.stats_update(table, plan, stats, 1.0, 1.0, rank if world > 1 else -1, gnum)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        shp.stats_update(table, plan, stats, 1.0, 1.0, rank if world > 1 else -1, gnum)
+        launches[0] += shp.last_launch_count()
+        if ev:
+            ev[1].record(stream)
+        infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol)
+        launches[0] += len(infos)
+        if ev:
+            ev[2].record(stream)
+        sdist.all_gather_roots(plan, roots, rank, world)
+        if ev:
+            ev[3].record(stream)
+        shp.precondition(table, plan, roots, gnum, gscale)
+        launches[0] += shp.last_launch_count()
+        if ev:
+            ev[4].record(stream)
+        return infos
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: barrier + sync on both sides, CUDA events on the launching stream
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    # per-group root launch timing (the dominant kernel) on the same stream
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches[0] = 0
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    all_infos = []
+    for k in range(args.steps):
+        all_infos.append(step(evs[k]))
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    phase = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(args.steps)])
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    total_ms = float(t_local.item())
+    ms_per_step = total_ms / args.steps
+
+    # dominant kernel: the p=4 root launch (one cooperative kernel per call), timed alone on the stream
+    g4 = [g for g in plan.groups_of(rank) if int(g["p"]) == 4 and int(g["n"]) == BLOCK]
+    roof = None
+    iters_mean = None
+    if g4:
+        g = g4[0]
+        cnt, off, stride = int(g["count"]), int(g["offset"]), int(g["stride"])
+        info = shp.new_info(cnt, dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        shp.inverse_pth_root_ptr(stats.data_ptr() + 4 * off, BLOCK, stride, roots.data_ptr() + 4 * off, BLOCK, stride,
+                                 cnt, BLOCK, 4, info, tol=args.tol, device=dev)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kms = e0.elapsed_time(e1)
+        inf = shp.info_to_numpy(info)
+        iters_mean = float(inf["iters"].mean())
+        n = BLOCK
+        # algorithmic flops: 4 symmetric products per iteration, n^2 (n+1) flops each (upper triangle
+        # incl. diagonal x 2n), + the power iteration (100 x 2 n^2)
+        flops = float(inf["iters"].sum()) * 4 * n * n * (n + 1) + cnt * 100 * 2.0 * n * n
+        achieved = flops / (kms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+                "kernel": f"root_kernel (FP64 DMMA coupled Newton, batch {cnt} x 1024^2, p=4)",
+                "kernel_ms": kms, "flops_per_launch": flops,
+                "peak_source": "FP64 DMMA.8x8x4 peak measured on this pool's B200 by tools/microbench/fp64_pipes.cu "
+                               "(MEASURED_PEAKS.json has no FP64 entry)"}
+
+    n_p4_total = n_p4  # every p=4 root of the plan is computed once per step (owner-sharded)
+    value = n_p4_total / (ms_per_step * 1e-3)
+
+    # e2e: through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hostG = [torch.empty(G.shape, dtype=torch.float32, pin_memory=True) for G in Gs]
+        for h, G in zip(hostG, Gs):
+            h.copy_(G)
+        hostP = [torch.empty(P.shape, dtype=torch.float32, pin_memory=True) for P in Ps]
+        hscale = torch.empty(nb, dtype=torch.float32, pin_memory=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            for h, G in zip(hostG, Gs):
+                G.copy_(h, non_blocking=True)
+            step()
+            for h, P in zip(hostP, Ps):
+                h.copy_(P, non_blocking=True)
+            hscale.copy_(gscale, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item()) / args.steps
+        bi = sum(G.numel() * 4 for G in Gs)
+        bo = sum(P.numel() * 4 for P in Ps) + nb * 4
+        e2e = {"value": n_p4_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "ms_per_step": e2e_ms}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = oracle_root_baseline()
+        ph = phase.mean(axis=0)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "transformer_big_b1024_full_step", "model": "Transformer-Big (P:494) shapes",
+                       "block_size": BLOCK, "max_precond_dim": MAX_PRECOND, "blocks": nb,
+                       "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
+                       "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
+                       "parallelism": f"root-shard{world}", "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
+            "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather": ph[2], "precondition": ph[3]},
+            "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,
+            "root_phase_roots_per_s": n_p4_total / (ph[1] * 1e-3),
+            "newton_iters_mean": iters_mean,
+            "gpu_launches": launches[0],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

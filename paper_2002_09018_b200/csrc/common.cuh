@@ -25,15 +25,22 @@ SHP_DEV void dmma884(double& d0, double& d1, double a, double b) {
 }
 
 // ------------------------------------------------------- shared memory tile
-// Operand tiles are stored as fp64 [kTileM rows][kTileK k] with the 16-byte
-// chunk c of row r at chunk c ^ (r & 7) (128B XOR swizzle).  A fragment read
-// (8 rows x 4 consecutive k) then touches 8 distinct (pair of) chunks: two
-// wavefronts for 256 bytes, i.e. conflict-free.
+// Operand tiles are stored as fp64 [kTileM rows][kTileK k] (128 B per row);
+// the 16-byte chunk c of row r lives at chunk c ^ X(r), X(r) = 2*(r&3) + ((r>>2)&1).
+// * DMMA fragment reads (LDS.64, 8 rows x 4 consecutive k) are served per
+//   half-warp: rows q = 0..3 XOR with 0,2,4,6 and rows 4..7 with 1,3,5,7, so the
+//   8 (row, chunk) pairs of each half-warp hit 8 distinct chunk positions
+//   (1 wavefront per half, the minimum for 256 B).
+// * Row-wise stores (8 consecutive rows, same logical chunk) see 8 distinct
+//   X values: conflict-free as well.
 constexpr int kTileM = 128;
 constexpr int kTileK = 16;
 constexpr int kTileElems = kTileM * kTileK;  // doubles per operand tile
 
-SHP_DEV int swz(int r, int k) { return r * kTileK + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1)); }
+SHP_DEV int swx(int r) { return ((r & 3) << 1) | ((r >> 2) & 1); }
+SHP_DEV int swz(int r, int k) { return r * kTileK + ((((k >> 1) ^ swx(r)) << 1) | (k & 1)); }
+// element offset of 16-byte chunk c of row r
+SHP_DEV int swc(int r, int c) { return r * kTileK + ((c ^ swx(r)) << 1); }
 
 // ------------------------------------------------------------ misc helpers
 SHP_DEV unsigned long long dbits(double x) { return (unsigned long long)__double_as_longlong(x); }

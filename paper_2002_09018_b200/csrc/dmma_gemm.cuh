@@ -55,7 +55,7 @@ struct F64Rows {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       int id = t + kThreads * q, row = id >> 3, c = id & 7;
-      *reinterpret_cast<double2*>(s + row * kTileK + ((c ^ (row & 7)) << 1)) = r[q];
+      *reinterpret_cast<double2*>(s + swc(row, c)) = r[q];
     }
   }
 };
@@ -82,14 +82,11 @@ struct F32Panel {
         for (int e = 0; e < 4; ++e) r[4 * q + e] = (m < m_valid && k + e < k_valid) ? __ldg(src + e) : 0.0f;
       }
     } else {
+      // thread -> (m = t & 127, k = 8*(t >> 7) .. +7): per k, a warp reads 32
+      // consecutive m (coalesced); the thread then owns 8 consecutive k of row m.
+      const int m = m0 + (t & 127), kb = kt * kTileK + 8 * (t >> 7);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        int id = t + kThreads * q, kk = id >> 5, c = id & 31;
-        int k = kt * kTileK + kk, m = m0 + 4 * c;
-        const float* src = base + (int64_t)k * ld + m;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) r[4 * q + e] = (k < k_valid && m + e < m_valid) ? __ldg(src + e) : 0.0f;
-      }
+      for (int e = 0; e < 8; ++e) r[e] = (m < m_valid && kb + e < k_valid) ? __ldg(base + (int64_t)(kb + e) * ld + m) : 0.0f;
     }
   }
   SHP_DEV void store(double* s, const Regs& r) const {
@@ -100,36 +97,43 @@ struct F32Panel {
         int id = t + kThreads * q, row = id >> 2, c4 = id & 3;
         double2 lo = make_double2((double)r[4 * q + 0], (double)r[4 * q + 1]);
         double2 hi = make_double2((double)r[4 * q + 2], (double)r[4 * q + 3]);
-        *reinterpret_cast<double2*>(s + row * kTileK + (((2 * c4) ^ (row & 7)) << 1)) = lo;
-        *reinterpret_cast<double2*>(s + row * kTileK + (((2 * c4 + 1) ^ (row & 7)) << 1)) = hi;
+        // odd rows store their odd chunk first: the two rows of a quarter-warp then
+        // cover disjoint chunk positions in each store instruction
+        const int c0 = 2 * c4 + (row & 1), c1 = 2 * c4 + 1 - (row & 1);
+        *reinterpret_cast<double2*>(s + swc(row, c0)) = (row & 1) ? hi : lo;
+        *reinterpret_cast<double2*>(s + swc(row, c1)) = (row & 1) ? lo : hi;
       }
     } else {
+      const int row = t & 127, cb = 4 * (t >> 7);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        int id = t + kThreads * q, kk = id >> 5, c = id & 31;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) s[swz(4 * c + e, kk)] = (double)r[4 * q + e];
-      }
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<double2*>(s + swc(row, cb + j)) = make_double2((double)r[2 * j], (double)r[2 * j + 1]);
     }
   }
 };
 
 // ------------------------------------------------------------------ compute
+SHP_DEV void load_frags(double (&a)[8], double (&b)[4], const double* sA, const double* sB, int ra, int rb, int k) {
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) a[mt] = sA[swz(ra + mt * 8, k)];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) b[nt] = sB[swz(rb + nt * 8, k)];
+}
+
+// One 16-deep k tile: 4 k-groups x 32 DMMA per warp; the fragments of group
+// g+1 are loaded while the DMMAs of group g issue (register double buffer).
 SHP_DEV void mma_ktile(Acc& acc, const double* sA, const double* sB, int warp, int lane) {
   const int ra = (warp & 1) * 64 + (lane >> 2);
   const int rb = (warp >> 1) * 32 + (lane >> 2);
+  double a[2][8], b[2][4];
+  load_frags(a[0], b[0], sA, sB, ra, rb, lane & 3);
 #pragma unroll
   for (int g = 0; g < kTileK / 4; ++g) {
-    const int k = 4 * g + (lane & 3);
-    double a[8], b[4];
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) a[mt] = sA[swz(ra + mt * 8, k)];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) b[nt] = sB[swz(rb + nt * 8, k)];
+    if (g + 1 < kTileK / 4) load_frags(a[(g + 1) & 1], b[(g + 1) & 1], sA, sB, ra, rb, 4 * (g + 1) + (lane & 3));
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma884(acc.c[mt][nt][0], acc.c[mt][nt][1], a[mt], b[nt]);
+      for (int nt = 0; nt < 4; ++nt) dmma884(acc.c[mt][nt][0], acc.c[mt][nt][1], a[g & 1][mt], b[g & 1][nt]);
   }
 }
 
@@ -138,15 +142,15 @@ SHP_DEV void mma_ktile(Acc& acc, const double* sA, const double* sB, int warp, i
 template <class LA, class LB>
 SHP_DEV void gemm_tile(Acc& acc, const LA& la, const LB& lb, int k_tiles, double* smem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* sA[2] = {smem, smem + 2 * kTileElems};
-  double* sB[2] = {smem + kTileElems, smem + 3 * kTileElems};
+  // stage s: A at smem + s*2*kTileElems, B right after it (offsets, not a pointer
+  // array, so that the compiler keeps the shared address space: LDS, not LD)
   typename LA::Regs ra;
   typename LB::Regs rb;
   acc_zero(acc);
   la.load(0, ra);
   lb.load(0, rb);
-  la.store(sA[0], ra);
-  lb.store(sB[0], rb);
+  la.store(smem, ra);
+  lb.store(smem + kTileElems, rb);
   __syncthreads();
   for (int kt = 0; kt < k_tiles; ++kt) {
     const int s = kt & 1;
@@ -155,13 +159,68 @@ SHP_DEV void gemm_tile(Acc& acc, const LA& la, const LB& lb, int k_tiles, double
       la.load(kt + 1, ra);
       lb.load(kt + 1, rb);
     }
-    mma_ktile(acc, sA[s], sB[s], warp, lane);
+    const double* cur = smem + s * (2 * kTileElems);
+    mma_ktile(acc, cur, cur + kTileElems, warp, lane);
     if (more) {
-      la.store(sA[s ^ 1], ra);
-      lb.store(sB[s ^ 1], rb);
+      double* nxt = smem + (s ^ 1) * (2 * kTileElems);
+      la.store(nxt, ra);
+      lb.store(nxt + kTileElems, rb);
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------- cp.async fp64 pipeline
+// For fp64 row panels (the Newton products): LDGSTS 16-byte copies straight
+// into the swizzled tile, kStages-deep ring, no register staging.
+constexpr int kStages = 3;
+constexpr int kAsyncSmemDoubles = kStages * 2 * kTileElems;
+
+SHP_DEV void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+}
+SHP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+SHP_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+SHP_DEV void f64_issue(double* s, const double* base, int64_t ld, int kt) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int id = t + kThreads * q, row = id >> 3, c = id & 7;
+    cp_async16(s + swc(row, c), base + (int64_t)row * ld + kt * kTileK + 2 * c);
+  }
+}
+
+// C = A_panel . B_panel^T over K = 16 * k_tiles, both fp64 row panels.
+// `smem` holds kAsyncSmemDoubles doubles.  Ends with __syncthreads.
+SHP_DEV void gemm_tile_f64(Acc& acc, const double* A, const double* B, int64_t ld, int k_tiles, double* smem) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  acc_zero(acc);
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (st < k_tiles) {
+      f64_issue(smem + st * 2 * kTileElems, A, ld, st);
+      f64_issue(smem + st * 2 * kTileElems + kTileElems, B, ld, st);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < k_tiles; ++kt) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // stage kt visible to all; stage kt-1 fully consumed
+    const int nk = kt + kStages - 1;
+    if (nk < k_tiles) {
+      double* s = smem + (nk % kStages) * 2 * kTileElems;
+      f64_issue(s, A, ld, nk);
+      f64_issue(s + kTileElems, B, ld, nk);
+    }
+    cp_async_commit();
+    const double* cur = smem + (kt % kStages) * 2 * kTileElems;
+    mma_ktile(acc, cur, cur + kTileElems, warp, lane);
+  }
+  cp_async_wait<0>();
+  __syncthreads();
 }
 
 // Upper-triangular tile index t -> (ti, tj), ti <= tj, row-major over the

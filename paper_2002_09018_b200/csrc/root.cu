@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
   grid.sync();
 
   // ---- iterations
-  int* act = reinterpret_cast<int*>(smem + kGemmSmemDoubles);
+  int* act = reinterpret_cast<int*>(smem + kAsyncSmemDoubles);
   int* cnt = act + kMaxBatchPerLaunch;  // 257 ints scratch
   __shared__ int s_nact;
   // initial active list: lam ok and decide(k=0) == continue
@@ -325,9 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         upper_tile(t, T, ti, tj);
         const double* Aop = (job == 0) ? buf(a, mat, BX0 + xs) : buf(a, mat, tb);
         const double* Bop = buf(a, mat, tb);
-        F64Rows la{Aop + (int64_t)ti * kTileM * np, np};
-        F64Rows lb{Bop + (int64_t)tj * kTileM * np, np};
-        gemm_tile(acc, la, lb, np / kTileK, smem);
+        gemm_tile_f64(acc, Aop + (int64_t)ti * kTileM * np, Bop + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
         double* dst = (job == 0) ? buf(a, mat, BX0 + (xs ^ 1)) : buf(a, mat, BS0);
         epilogue<EPI_STORE>(a, acc, mat, ti, tj, dst, nullptr, nullptr);
       }
@@ -343,9 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         int ti, tj;
         upper_tile(t, T, ti, tj);
         const double* S = buf(a, mat, src);
-        F64Rows la{S + (int64_t)ti * kTileM * np, np};
-        F64Rows lb{S + (int64_t)tj * kTileM * np, np};
-        gemm_tile(acc, la, lb, np / kTileK, smem);
+        gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
         epilogue<EPI_STORE>(a, acc, mat, ti, tj, buf(a, mat, dstb), nullptr, nullptr);
       }
       grid.sync();
@@ -359,9 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         const int mat = act[pos];
         int ti, tj;
         upper_tile(t, T, ti, tj);
-        F64Rows la{buf(a, mat, tp) + (int64_t)ti * kTileM * np, np};
-        F64Rows lb{buf(a, mat, BM0 + xs) + (int64_t)tj * kTileM * np, np};
-        gemm_tile(acc, la, lb, np / kTileK, smem);
+        gemm_tile_f64(acc, buf(a, mat, tp) + (int64_t)ti * kTileM * np,
+                      buf(a, mat, BM0 + xs) + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
         epilogue<EPI_MUPDATE>(a, acc, mat, ti, tj, buf(a, mat, BM0 + (xs ^ 1)), buf(a, mat, tb_next),
                               a.errh + (int64_t)mat * (a.max_iter + 1) + (k + 1));
       }
@@ -431,7 +426,7 @@ size_t root_workspace_bytes(int batch, int n, int max_iter) {
 }
 
 size_t root_smem_bytes(int n) {
-  size_t gemm = (size_t)kGemmSmemDoubles * sizeof(double) + (kMaxBatchPerLaunch + kThreads + 1) * sizeof(int);
+  size_t gemm = (size_t)kAsyncSmemDoubles * sizeof(double) + (kMaxBatchPerLaunch + kThreads + 1) * sizeof(int);
   size_t pi = (2 * (size_t)n + 8) * sizeof(double);
   return gemm > pi ? gemm : pi;
 }
@@ -523,8 +518,8 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
     const bool valid = i < n && j < n;
     double x = 0.0, ah = 0.0;
     if (valid) {
-      x = (double)a.X[(int64_t)mat * a.stride_x + (int64_t)i * a.ldx + j];
-      const int r = i < j ? i : j, q = i < j ? j : i;
+      const int r = i < j ? i : j, q = i < j ? j : i;  // upper triangles (symmetric by contract)
+      x = (double)a.X[(int64_t)mat * a.stride_x + (int64_t)r * a.ldx + q];
       ah = (double)a.A[(int64_t)mat * a.stride_a + (int64_t)r * a.lda + q];
       if (i == j) ah = __dadd_rn(ah, __dmul_rn(a.eps_rel, a.info[mat].lambda_max));
     }
@@ -541,9 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
       int ti, tj;
       upper_tile(t, T, ti, tj);
       const double* S = rbuf(a, mat, src);
-      F64Rows la{S + (int64_t)ti * kTileM * np, np};
-      F64Rows lb{S + (int64_t)tj * kTileM * np, np};
-      gemm_tile(acc, la, lb, np / kTileK, smem);
+      gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       double* D = rbuf(a, mat, dst);
 #pragma unroll
@@ -567,9 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
   for (int it = blockIdx.x; it < a.batch * T * T; it += gridDim.x) {
     const int mat = it / (T * T), t = it - mat * T * T;
     const int ti = t / T, tj = t - ti * T;
-    F64Rows la{rbuf(a, mat, src) + (int64_t)ti * kTileM * np, np};
-    F64Rows lb{rbuf(a, mat, 3) + (int64_t)tj * kTileM * np, np};
-    gemm_tile(acc, la, lb, np / kTileK, smem);
+    gemm_tile_f64(acc, rbuf(a, mat, src) + (int64_t)ti * kTileM * np, rbuf(a, mat, 3) + (int64_t)tj * kTileM * np,
+                  np, np / kTileK, smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double s = 0.0;
 #pragma unroll
@@ -612,7 +604,7 @@ size_t residual_workspace_bytes(int batch, int n) {
 int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* X, int64_t ldx, int64_t stride_x,
                     int batch, int n, int p, double eps_rel, const shampoo_root_info_t* info, double* residual,
                     void* ws, cudaStream_t stream, int64_t* launches) {
-  const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
+  const size_t smem = (size_t)kAsyncSmemDoubles * sizeof(double);
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
