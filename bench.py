@@ -38,6 +38,9 @@ BLOCK = 1024
 MAX_PRECOND = 8192
 KAPPA_REFRESH = 500  # root refresh interval of the paper's Transformer runs
 FP64_DMMA_PEAK_TFLOPS = 37.1  # measured: tools/microbench/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)
+# dram__bytes_read.sum + dram__bytes_write.sum of root_kernel per 1024^2 p=4 matrix (20 iterations), from the
+# ncu --set full capture in profiles/r01_ncu_root_kernel.txt (148-matrix launch: 323.6 GB)
+ROOT_TRAFFIC_BYTES_PER_MATRIX = 323.626e9 / 148
 
 
 def parse():
@@ -273,7 +276,8 @@ def main():
         flops = float(inf["iters"].sum()) * 4 * n * n * (n + 1) + cnt * 100 * 2.0 * n * n
         achieved = flops / (kms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": ROOT_TRAFFIC_BYTES_PER_MATRIX * cnt,
+                "traffic_note": "bytes per launch, ncu capture of the same kernel (148 matrices) scaled per matrix",
                 "kernel": f"root_kernel (FP64 DMMA coupled Newton, batch {cnt} x 1024^2, p=4)",
                 "kernel_ms": kms, "flops_per_launch": flops,
                 "peak_source": "FP64 DMMA.8x8x4 peak measured on this pool's B200 by tools/microbench/fp64_pipes.cu "

@@ -1,0 +1,67 @@
+"""Multi-GPU check of row e (run under torchrun, NCCL): owner-sharded statistics +
+roots + all-gather must give roots bit-identical to a single-GPU computation.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29511 tools/check_multi_gpu.py
+"""
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2002_09018_b200 as shp  # noqa: E402
+import synth  # noqa: E402
+from paper_2002_09018_b200 import dist as sdist  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    shapes = [s for _, s in synth.transformer_big_shapes()][3:40]  # attention + FFN blocks (no vocab)
+    Gs = [synth.lowrank_gradient_device(m, n, synth.BASE_SEED + 3 + i, dev) for i, (m, n) in enumerate(shapes)]
+    table = shp.TensorTable(Gs, [torch.zeros_like(G) for G in Gs])
+    # sharded
+    plan = shp.make_plan(shapes, 1024, 8192, world)
+    stats = torch.zeros(plan.stats_elems, device=dev)
+    roots = torch.zeros_like(stats)
+    for _ in range(2):
+        shp.stats_update(table, plan, stats, 1.0, 1.0, rank)
+    sdist.refresh_roots(plan, stats, roots, rank, world)
+    torch.cuda.synchronize()
+    # single-GPU reference on every rank (same kernels, whole plan)
+    plan1 = shp.make_plan(shapes, 1024, 8192, 1)
+    table1 = shp.TensorTable(Gs, [torch.zeros_like(G) for G in Gs])
+    stats1 = torch.zeros(plan1.stats_elems, device=dev)
+    roots1 = torch.zeros_like(stats1)
+    for _ in range(2):
+        shp.stats_update(table1, plan1, stats1, 1.0, 1.0, -1)
+    shp.refresh_group_roots(plan1, stats1, roots1, 0)
+    torch.cuda.synchronize()
+    bad = 0
+    for b, b1 in zip(plan.blocks, plan1.blocks):
+        for side in ("left", "right"):
+            if b[f"p_{side}"]:
+                n = int(b["rows"] if side == "left" else b["cols"])
+                ld = int(b[f"{side}_ld"])
+                o, o1 = int(b[f"{side}_off"]), int(b1[f"{side}_off"])
+                if not torch.equal(roots[o:o + n * ld], roots1[o1:o1 + n * ld]):
+                    bad += 1
+    t = torch.tensor([bad], device=dev)
+    dist.all_reduce(t)
+    if rank == 0:
+        n_roots = int((plan.blocks["p_left"] > 0).sum() + (plan.blocks["p_right"] > 0).sum())
+        print(f"world {world}: {n_roots} roots, mismatching (summed over ranks) = {int(t.item())}", flush=True)
+    dist.destroy_process_group()
+    if int(t.item()) != 0:
+        raise SystemExit(1)
+
+
+if __name__ == "__main__":
+    main()
