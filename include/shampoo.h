@@ -174,12 +174,21 @@ int shampoo_root_residual_batched(const float* A, int64_t lda, int64_t stride_a,
  *   graft_scale[b] = sqrt(graft_num[b]) / ||P_b||_F  (0 if ||P_b|| = 0),
  * written into tensors[t].P.  roots uses the statistics packing.  The caller
  * applies W -= eta * graft_scale[b] * P_b (grafting).
+ * Products: 3xTF32 on the tcgen05 tensor cores (fp32-accurate: x = hi + lo
+ * exact TF32 split, hi.hi + hi.lo + lo.hi accumulated in TMEM) for blocks with
+ * a right factor whose ragged extents sit on the tensor edge or are multiples
+ * of 32; FP64 DMMA for the rest (left-only blocks).
+ *   tensors_host, blocks_host : HOST tables (the call derives TMA tensor maps
+ *                               and per-block GEMM jobs from them and uploads
+ *                               them into the workspace, stream-ordered)
  *   graft_num  : double[n_blocks] from shampoo_stats_update (nullable -> no scale)
  *   graft_scale: float[n_blocks] out (nullable)
  *   den        : double[n_blocks] out, ||P_b||_F^2 (nullable)
- *   workspace  : >= shampoo_precondition_workspace_bytes(blocks_host, n_blocks) */
-size_t shampoo_precondition_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks);
-int shampoo_precondition(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
+ *   workspace  : >= shampoo_precondition_workspace_bytes(...), 256-B aligned
+ * Errors: SHAMPOO_ERR_WORKSPACE if the workspace is smaller than required. */
+size_t shampoo_precondition_workspace_bytes(const shampoo_tensor_t* tensors_host, int32_t n_tensors,
+                                            const shampoo_block_t* blocks_host, int32_t n_blocks);
+int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors, const shampoo_block_t* blocks_host,
                          int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
                          double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream);
 

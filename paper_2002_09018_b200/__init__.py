@@ -231,12 +231,14 @@ def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, ow
 # -------------------------------------------------------------------- a8-a9
 def precondition(table: TensorTable, plan: Plan, roots: torch.Tensor, graft_num: torch.Tensor | None = None,
                  graft_scale: torch.Tensor | None = None, den: torch.Tensor | None = None, stream=None):
+    """P for every block (3xTF32 tcgen05 / FP64 DMMA) and the per-block graft scale."""
     L = _lib.lib()
     nb = plan.n_blocks
-    wsb = L.shampoo_precondition_workspace_bytes(plan.blocks.ctypes.data, nb)
+    th, bh = table.host, plan.blocks
+    wsb = L.shampoo_precondition_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb)
     ws = workspace(wsb, roots.device, "precondition")
-    check(L.shampoo_precondition(table.dev.data_ptr(), table.n, plan.device_blocks(roots.device).data_ptr(), nb,
-                                 roots.data_ptr(), graft_num.data_ptr() if graft_num is not None else None,
+    check(L.shampoo_precondition(th.ctypes.data, table.n, bh.ctypes.data, nb, roots.data_ptr(),
+                                 graft_num.data_ptr() if graft_num is not None else None,
                                  graft_scale.data_ptr() if graft_scale is not None else None,
                                  den.data_ptr() if den is not None else None, ws.data_ptr(), ws.numel(),
                                  _stream_ptr(stream)))

@@ -78,7 +78,7 @@ def lib():
     L.shampoo_root_residual_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl, _vp, _vp,
                                                 _vp, _sz, _vp]
     L.shampoo_root_residual_batched.restype = ctypes.c_int
-    L.shampoo_precondition_workspace_bytes.argtypes = [_vp, _i32]
+    L.shampoo_precondition_workspace_bytes.argtypes = [_vp, _i32, _vp, _i32]
     L.shampoo_precondition_workspace_bytes.restype = _sz
     L.shampoo_precondition.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     L.shampoo_precondition.restype = ctypes.c_int

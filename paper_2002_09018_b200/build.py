@@ -23,8 +23,8 @@ CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLU
             "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
-SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu"]
-HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h"]
+SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu", "tc_gemm.cu"]
+HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h", "tc_common.cuh", "tc_gemm.h"]
 
 
 def _newer(target: str, deps) -> bool:

@@ -152,24 +152,30 @@ int shampoo_root_residual_batched(const float* A, int64_t lda, int64_t stride_a,
                          static_cast<cudaStream_t>(stream), &g_launches);
 }
 
-size_t shampoo_precondition_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks) {
-  if (!blocks_host || n_blocks <= 0) return 0;
-  return precondition_workspace_bytes(blocks_host, n_blocks);
+size_t shampoo_precondition_workspace_bytes(const shampoo_tensor_t* tensors_host, int32_t n_tensors,
+                                            const shampoo_block_t* blocks_host, int32_t n_blocks) {
+  if (!tensors_host || !blocks_host || n_blocks <= 0 || n_tensors <= 0) return 0;
+  return precondition_workspace_bytes(tensors_host, n_tensors, blocks_host, n_blocks);
 }
 
-int shampoo_precondition(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
+int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors, const shampoo_block_t* blocks_host,
                          int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
                          double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream) {
   g_err[0] = 0;
   g_launches = 0;
   if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
   if (n_blocks == 0) return SHAMPOO_OK;
-  if (!tensors || !blocks || !roots) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block/roots");
+  if (!tensors_host || !blocks_host || !roots) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block/roots");
+  for (int32_t b = 0; b < n_blocks; ++b)
+    if (blocks_host[b].tensor_id < 0 || blocks_host[b].tensor_id >= n_tensors)
+      return set_error(SHAMPOO_ERR_INVALID_ARG, "block %d: tensor_id out of range", b);
+  for (int32_t t = 0; t < n_tensors; ++t)
+    if (!tensors_host[t].G || !tensors_host[t].P) return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor %d: null G or P", t);
   if (!workspace) return set_error(SHAMPOO_ERR_WORKSPACE, "null workspace");
   if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
     return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
-  return precondition_launch(tensors, n_tensors, blocks, n_blocks, roots, graft_num, graft_scale, den, workspace,
-                             workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
+  return precondition_launch(tensors_host, n_tensors, blocks_host, n_blocks, roots, graft_num, graft_scale, den,
+                             workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
 }
 
 }  // extern "C"

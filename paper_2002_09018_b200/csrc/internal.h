@@ -29,10 +29,11 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
                  void* ws, cudaStream_t stream, int64_t* launches);
 
 // precondition.cu
-size_t precondition_workspace_bytes(const shampoo_block_t* blocks_host, int n_blocks);
-int precondition_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_block_t* blocks, int n_blocks,
-                        const float* roots, const double* graft_num, float* graft_scale, double* den, void* ws,
-                        size_t ws_bytes, cudaStream_t stream, int64_t* launches);
+size_t precondition_workspace_bytes(const shampoo_tensor_t* tensors_host, int n_tensors,
+                                    const shampoo_block_t* blocks_host, int n_blocks);
+int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, const shampoo_block_t* blocks_host,
+                        int n_blocks, const float* roots, const double* graft_num, float* graft_scale, double* den,
+                        void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
 
 int num_sms();
 

@@ -10,8 +10,13 @@
 // -> diag-only blocks -> den partials -> finish (fixed-order sums, scale).
 // The products run on the FP64 tensor pipe through dmma_gemm.cuh; Y is kept
 // in fp32 in the workspace (L2-resident for a 1024^2 block).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "dmma_gemm.cuh"
 #include "internal.h"
+#include "tc_gemm.h"
 
 namespace shp {
 
@@ -19,56 +24,18 @@ constexpr int kPChunks = 64;
 
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-struct PrecWs {
-  int64_t* pre1;  // n_blocks + 1 phase-1 tiles
-  int64_t* pre2;  // n_blocks + 1 phase-2 tiles
-  int64_t* yoff;  // n_blocks + 1 Y offsets (elements)
-  double* part;   // n_blocks * kPChunks
-  float* Y;
-};
-
-static size_t y_elems(const shampoo_block_t* blocks, int n_blocks) {
-  size_t s = 0;
-  for (int b = 0; b < n_blocks; ++b)
-    if (blocks[b].p_left && blocks[b].p_right) s += (size_t)blocks[b].rows * blocks[b].cols;
-  return s;
-}
-
-static size_t fixed_bytes(int n_blocks) {
-  return 3 * al((size_t)(n_blocks + 1) * sizeof(int64_t)) + al((size_t)n_blocks * kPChunks * sizeof(double));
-}
-
-size_t precondition_workspace_bytes(const shampoo_block_t* blocks_host, int n_blocks) {
-  return fixed_bytes(n_blocks) + al(y_elems(blocks_host, n_blocks) * sizeof(float));
-}
-
-static PrecWs carve(void* ws, int n_blocks) {
-  char* q = static_cast<char*>(ws);
-  PrecWs w;
-  const size_t pb = al((size_t)(n_blocks + 1) * sizeof(int64_t));
-  w.pre1 = reinterpret_cast<int64_t*>(q);
-  q += pb;
-  w.pre2 = reinterpret_cast<int64_t*>(q);
-  q += pb;
-  w.yoff = reinterpret_cast<int64_t*>(q);
-  q += pb;
-  w.part = reinterpret_cast<double*>(q);
-  q += al((size_t)n_blocks * kPChunks * sizeof(double));
-  w.Y = reinterpret_cast<float*>(q);
-  return w;
-}
-
 SHP_DEV int ntile(int n) { return (n + kTileM - 1) / kTileM; }
 
-SHP_DEV void block_counts(const shampoo_block_t& b, int64_t& n1, int64_t& n2, int64_t& ny) {
+// DMMA-path work of a block (blocks served by the tcgen05 path have tc_flag set)
+SHP_DEV void block_counts(const shampoo_block_t& b, int tc_flag, int64_t& n1, int64_t& n2, int64_t& ny) {
   const int64_t t = (int64_t)ntile(b.rows) * ntile(b.cols);
-  n1 = b.p_left ? t : 0;
-  n2 = b.p_right ? t : 0;
-  ny = (b.p_left && b.p_right) ? (int64_t)b.rows * b.cols : 0;
+  n1 = (b.p_left && !tc_flag) ? t : 0;
+  n2 = (b.p_right && !tc_flag) ? t : 0;
+  ny = (b.p_left && b.p_right && !tc_flag) ? (int64_t)b.rows * b.cols : 0;
 }
 
-__global__ void __launch_bounds__(1024) prec_prep_kernel(const shampoo_block_t* blocks, int n_blocks,
-                                                         int64_t* pre1, int64_t* pre2, int64_t* yoff) {
+__global__ void __launch_bounds__(1024) prec_prep_kernel(const shampoo_block_t* blocks, const int* tc_flags,
+                                                         int n_blocks, int64_t* pre1, int64_t* pre2, int64_t* yoff) {
   __shared__ int64_t s1[1024], s2[1024], s3[1024];
   const int t = threadIdx.x;
   const int per = (n_blocks + 1023) / 1024;
@@ -76,7 +43,7 @@ __global__ void __launch_bounds__(1024) prec_prep_kernel(const shampoo_block_t* 
   int64_t a1 = 0, a2 = 0, a3 = 0;
   for (int b = b0; b < b1; ++b) {
     int64_t n1, n2, ny;
-    block_counts(blocks[b], n1, n2, ny);
+    block_counts(blocks[b], tc_flags[b], n1, n2, ny);
     a1 += n1;
     a2 += n2;
     a3 += ny;
@@ -109,7 +76,7 @@ __global__ void __launch_bounds__(1024) prec_prep_kernel(const shampoo_block_t* 
     pre2[b] = a2;
     yoff[b] = a3;
     int64_t n1, n2, ny;
-    block_counts(blocks[b], n1, n2, ny);
+    block_counts(blocks[b], tc_flags[b], n1, n2, ny);
     a1 += n1;
     a2 += n2;
     a3 += ny;
@@ -242,31 +209,308 @@ __global__ void prec_finish_kernel(int n_blocks, const double* part, const doubl
   }
 }
 
-int precondition_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_block_t* blocks, int n_blocks,
-                        const float* roots, const double* graft_num, float* graft_scale, double* den, void* ws,
-                        size_t ws_bytes, cudaStream_t stream, int64_t* launches) {
-  (void)n_tensors;
-  (void)ws_bytes;
+// ---------------------------------------------------------------- host plan
+// Everything the call needs is derived from the HOST tables on every call:
+// tcgen05 eligibility, TMA maps, per-block GEMM jobs, split segments and the
+// workspace layout.  One pageable cudaMemcpyAsync uploads the tables.
+struct RootRun {  // consecutive equal-size roots at a constant stride (one 3-D TMA map)
+  int64_t off0, stride;
+  int n, ld, count;
+};
+
+struct PrecLayout {
+  // host staging (uploaded as one blob at ws + 0)
+  std::vector<uint8_t> blob;
+  size_t off_tensors = 0, off_blocks = 0, off_flags = 0, off_maps = 0, off_jobs1 = 0, off_jobs2 = 0, off_segs = 0;
+  int n_maps = 0, n_jobs1 = 0, n_jobs2 = 0, n_segs = 0;
+  int64_t tiles1 = 0, tiles2 = 0;
+  bool any_dmma = false;
+  // device regions (offsets from ws)
+  size_t off_pre = 0, off_part = 0, off_Y = 0, off_rhi = 0, off_rlo = 0, off_ghi = 0, off_glo = 0, off_zhi = 0,
+         off_zlo = 0, total = 0;
+  int64_t roots_elems = 0;
+};
+
+static bool tc_eligible(const shampoo_block_t& b, const shampoo_tensor_t& t) {
+  if (!b.p_right) return false;  // left-only / diagonal-only blocks stay on the DMMA / elementwise path
+  const bool rows_ok = (b.rows % 32 == 0) || (b.row0 + b.rows == t.m);
+  const bool cols_ok = (b.cols % 32 == 0) || (b.col0 + b.cols == t.n);
+  return rows_ok && cols_ok;
+}
+
+static int64_t r4(int64_t x) { return (x + 3) / 4 * 4; }
+
+template <class T>
+static size_t put(std::vector<uint8_t>& blob, const T* p, size_t n, size_t align = 256) {
+  size_t off = (blob.size() + align - 1) / align * align;
+  blob.resize(off + n * sizeof(T));
+  if (n) std::memcpy(blob.data() + off, p, n * sizeof(T));
+  return off;
+}
+
+// Builds the layout; when `ws` is null only sizes are computed (maps need real pointers).
+static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_block_t* B, int n_blocks,
+                        const float* roots, char* ws, PrecLayout& L) {
+  std::vector<int> flags(n_blocks, 0);
+  std::vector<char> t_g(n_tensors, 0), t_z(n_tensors, 0);
+  size_t y_elems = 0;
+  for (int b = 0; b < n_blocks; ++b) {
+    flags[b] = tc_eligible(B[b], T[B[b].tensor_id]) ? 1 : 0;
+    if (flags[b]) {
+      t_g[B[b].tensor_id] = 1;
+      if (B[b].p_left) t_z[B[b].tensor_id] = 1;
+    } else if (B[b].p_left || B[b].p_right) {
+      L.any_dmma = true;
+      if (B[b].p_left && B[b].p_right) y_elems += (size_t)B[b].rows * B[b].cols;
+    }
+  }
+  // roots runs
+  struct R { int64_t off; int n, ld; };
+  std::vector<R> rs;
+  for (int b = 0; b < n_blocks; ++b) {
+    if (B[b].p_left) rs.push_back({B[b].left_off, B[b].rows, B[b].left_ld});
+    if (B[b].p_right) rs.push_back({B[b].right_off, B[b].cols, B[b].right_ld});
+  }
+  std::sort(rs.begin(), rs.end(), [](const R& a, const R& c) { return a.off < c.off; });
+  std::vector<RootRun> runs;
+  int64_t rend = 0;
+  for (const R& r : rs) {
+    const int64_t stride = ((int64_t)r.n * r.ld + 63) / 64 * 64;
+    rend = std::max(rend, r.off + (int64_t)r.n * r.ld);
+    if (!runs.empty()) {
+      RootRun& q = runs.back();
+      if (q.n == r.n && q.ld == r.ld && q.stride == stride && r.off == q.off0 + (int64_t)q.count * q.stride) {
+        ++q.count;
+        continue;
+      }
+    }
+    runs.push_back({r.off, stride, r.n, r.ld, 1});
+  }
+  L.roots_elems = rend;
+  // device layout
+  const size_t pb = al((size_t)(n_blocks + 1) * sizeof(int64_t));
+  size_t q = 0;
+  auto region = [&](size_t bytes) { size_t o = q; q = al(q + bytes); return o; };
+  // header blob size is unknown until maps are built; reserve generously
+  const size_t n_maps_max = 2 * runs.size() + 4 * (size_t)n_tensors;
+  const size_t hdr = al((size_t)n_tensors * sizeof(shampoo_tensor_t)) + al((size_t)n_blocks * sizeof(shampoo_block_t)) +
+                     al((size_t)n_blocks * sizeof(int)) + al(n_maps_max * sizeof(CUtensorMap)) +
+                     2 * al((size_t)n_blocks * sizeof(TcJob)) + al(((size_t)n_tensors + 64) * sizeof(SplitSeg)) + 4096;
+  region(hdr);
+  L.off_pre = region(3 * pb);
+  L.off_part = region((size_t)n_blocks * kPChunks * sizeof(double));
+  L.off_Y = region(y_elems * sizeof(float));
+  L.off_rhi = region((size_t)rend * sizeof(float));
+  L.off_rlo = region((size_t)rend * sizeof(float));
+  std::vector<size_t> goff(n_tensors, 0), zoff(n_tensors, 0);
+  size_t gsz = 0, zsz = 0;
+  for (int t = 0; t < n_tensors; ++t) {
+    if (t_g[t]) { goff[t] = gsz; gsz += (size_t)al((size_t)T[t].m * r4(T[t].n) * sizeof(float)); }
+    if (t_z[t]) { zoff[t] = zsz; zsz += (size_t)al((size_t)T[t].n * r4(T[t].m) * sizeof(float)); }
+  }
+  L.off_ghi = region(gsz);
+  L.off_glo = region(gsz);
+  L.off_zhi = region(zsz);
+  L.off_zlo = region(zsz);
+  L.total = q;
+  if (!ws) return SHAMPOO_OK;
+
+  // ---- tensor maps
+  std::vector<CUtensorMap> maps;
+  auto add_map = [&](const void* base, int dims, const uint64_t* size, const uint64_t* strides) -> int {
+    CUtensorMap m;
+    int rc = make_map_f32(&m, base, dims, size, strides, 128);
+    if (rc) return -1;
+    maps.push_back(m);
+    return (int)maps.size() - 1;
+  };
+  float* rhi = reinterpret_cast<float*>(ws + L.off_rhi);
+  float* rlo = reinterpret_cast<float*>(ws + L.off_rlo);
+  std::vector<int> run_map_hi(runs.size()), run_map_lo(runs.size());
+  for (size_t i = 0; i < runs.size(); ++i) {
+    const RootRun& r = runs[i];
+    uint64_t size[3] = {(uint64_t)r.n, (uint64_t)r.n, (uint64_t)r.count};
+    uint64_t st[2] = {(uint64_t)r.ld * 4, (uint64_t)r.stride * 4};
+    run_map_hi[i] = add_map(rhi + r.off0, 3, size, st);
+    run_map_lo[i] = add_map(rlo + r.off0, 3, size, st);
+    if (run_map_hi[i] < 0 || run_map_lo[i] < 0) return SHAMPOO_ERR_CUDA;
+  }
+  auto find_root = [&](int64_t off, int& map_hi, int& map_lo, int& z) {
+    for (size_t i = 0; i < runs.size(); ++i) {
+      const RootRun& r = runs[i];
+      if (off >= r.off0 && off < r.off0 + (int64_t)r.count * r.stride) {
+        map_hi = run_map_hi[i];
+        map_lo = run_map_lo[i];
+        z = (int)((off - r.off0) / r.stride);
+        return;
+      }
+    }
+  };
+  std::vector<int> g_hi(n_tensors, -1), g_lo(n_tensors, -1), z_hi(n_tensors, -1), z_lo(n_tensors, -1);
+  std::vector<SplitSeg> segs;
+  for (int t = 0; t < n_tensors; ++t) {
+    const int64_t ldg = r4(T[t].n), ldz = r4(T[t].m);
+    if (t_g[t]) {
+      float* gh = reinterpret_cast<float*>(ws + L.off_ghi + goff[t]);
+      float* gl = reinterpret_cast<float*>(ws + L.off_glo + goff[t]);
+      uint64_t size[2] = {(uint64_t)T[t].n, (uint64_t)T[t].m};
+      uint64_t st[1] = {(uint64_t)ldg * 4};
+      g_hi[t] = add_map(gh, 2, size, st);
+      g_lo[t] = add_map(gl, 2, size, st);
+      if (g_hi[t] < 0 || g_lo[t] < 0) return SHAMPOO_ERR_CUDA;
+      segs.push_back({T[t].G, gh, gl, T[t].ldg, ldg, (int32_t)T[t].m, (int32_t)T[t].n});
+    }
+    if (t_z[t]) {
+      float* zh = reinterpret_cast<float*>(ws + L.off_zhi + zoff[t]);
+      float* zl = reinterpret_cast<float*>(ws + L.off_zlo + zoff[t]);
+      uint64_t size[2] = {(uint64_t)T[t].m, (uint64_t)T[t].n};
+      uint64_t st[1] = {(uint64_t)ldz * 4};
+      z_hi[t] = add_map(zh, 2, size, st);
+      z_lo[t] = add_map(zl, 2, size, st);
+      if (z_hi[t] < 0 || z_lo[t] < 0) return SHAMPOO_ERR_CUDA;
+    }
+  }
+  // roots split: the packed buffer as rows of 4096 floats + a tail
+  {
+    const int64_t W = 4096, full_rows = rend / W, tail = rend - full_rows * W;
+    for (int64_t r0 = 0; r0 < full_rows; r0 += 1 << 20) {
+      const int64_t rows = std::min<int64_t>(1 << 20, full_rows - r0);
+      segs.push_back({roots + r0 * W, rhi + r0 * W, rlo + r0 * W, W, W, (int32_t)rows, (int32_t)W});
+    }
+    if (tail) segs.push_back({roots + full_rows * W, rhi + full_rows * W, rlo + full_rows * W, W, W, 1, (int32_t)tail});
+  }
+  // ---- jobs
+  std::vector<TcJob> j1, j2;
+  int64_t t1 = 0, t2 = 0;
+  for (int b = 0; b < n_blocks; ++b) {
+    if (!flags[b]) continue;
+    const shampoo_block_t& bk = B[b];
+    const shampoo_tensor_t& tt = T[bk.tensor_id];
+    const int tm = (bk.rows + 127) / 128, tn = (bk.cols + 127) / 128;
+    TcJob j;
+    std::memset(&j, 0, sizeof j);
+    // phase 1: C = G_b . X_R   (M = rows, N = cols, K = cols)
+    j.a = {g_hi[bk.tensor_id], g_lo[bk.tensor_id], (int32_t)bk.col0, (int32_t)bk.row0, 0, 2};
+    int mh = -1, ml = -1, z = 0;
+    find_root(bk.right_off, mh, ml, z);
+    j.b = {mh, ml, 0, 0, z, 3};
+    j.M = bk.rows;
+    j.N = bk.cols;
+    j.K = bk.cols;
+    j.tiles_n = tn;
+    j.tile_begin = t1;
+    if (bk.p_left) {
+      const int64_t ldz = r4(tt.m);
+      float* zh = reinterpret_cast<float*>(ws + L.off_zhi + zoff[bk.tensor_id]);
+      float* zl = reinterpret_cast<float*>(ws + L.off_zlo + zoff[bk.tensor_id]);
+      j.out_mode = 1;
+      j.out_hi = zh + bk.col0 * ldz + bk.row0;
+      j.out_lo = zl + bk.col0 * ldz + bk.row0;
+      j.ld_out = ldz;
+    } else {
+      j.out_mode = 0;
+      j.out_hi = tt.P + bk.row0 * tt.ldp + bk.col0;
+      j.ld_out = tt.ldp;
+    }
+    j1.push_back(j);
+    t1 += (int64_t)tm * tn;
+    if (bk.p_left) {
+      // phase 2: P = X_L . Z   (B_j[k] = Zt[col0 + j][row0 + k]; K = rows)
+      TcJob k2;
+      std::memset(&k2, 0, sizeof k2);
+      find_root(bk.left_off, mh, ml, z);
+      k2.a = {mh, ml, 0, 0, z, 3};
+      k2.b = {z_hi[bk.tensor_id], z_lo[bk.tensor_id], (int32_t)bk.row0, (int32_t)bk.col0, 0, 2};
+      k2.M = bk.rows;
+      k2.N = bk.cols;
+      k2.K = bk.rows;
+      k2.out_mode = 0;
+      k2.out_hi = tt.P + bk.row0 * tt.ldp + bk.col0;
+      k2.ld_out = tt.ldp;
+      k2.tiles_n = tn;
+      k2.tile_begin = t2;
+      j2.push_back(k2);
+      t2 += (int64_t)tm * tn;
+    }
+  }
+  L.tiles1 = t1;
+  L.tiles2 = t2;
+  L.n_jobs1 = (int)j1.size();
+  L.n_jobs2 = (int)j2.size();
+  L.n_maps = (int)maps.size();
+  L.n_segs = (int)segs.size();
+  L.blob.clear();
+  L.off_tensors = put(L.blob, T, n_tensors);
+  L.off_blocks = put(L.blob, B, n_blocks);
+  L.off_flags = put(L.blob, flags.data(), flags.size());
+  L.off_maps = put(L.blob, maps.data(), maps.size());
+  L.off_jobs1 = put(L.blob, j1.data(), j1.size());
+  L.off_jobs2 = put(L.blob, j2.data(), j2.size());
+  L.off_segs = put(L.blob, segs.data(), segs.size());
+  if (L.blob.size() > hdr) return set_error(SHAMPOO_ERR_WORKSPACE, "precondition header overflow");
+  return SHAMPOO_OK;
+}
+
+size_t precondition_workspace_bytes(const shampoo_tensor_t* tensors_host, int n_tensors,
+                                    const shampoo_block_t* blocks_host, int n_blocks) {
+  PrecLayout L;
+  build_layout(tensors_host, n_tensors, blocks_host, n_blocks, nullptr, nullptr, L);
+  return L.total;
+}
+
+int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, const shampoo_block_t* blocks_host,
+                        int n_blocks, const float* roots, const double* graft_num, float* graft_scale, double* den,
+                        void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches) {
   if (n_blocks == 0) return SHAMPOO_OK;
-  PrecWs w = carve(ws, n_blocks);
-  const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(prec_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(prec_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(prec_gemm_kernel)");
-    configured = true;
+  PrecLayout L;
+  build_layout(tensors_host, n_tensors, blocks_host, n_blocks, nullptr, nullptr, L);
+  if (ws_bytes < L.total)
+    return set_error(SHAMPOO_ERR_WORKSPACE, "precondition workspace: have %zu bytes, need %zu", ws_bytes, L.total);
+  char* w = static_cast<char*>(ws);
+  int rc = build_layout(tensors_host, n_tensors, blocks_host, n_blocks, roots, w, L);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(w, L.blob.data(), L.blob.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return set_cuda_error("cudaMemcpyAsync(precondition tables)");
+  const shampoo_tensor_t* tensors = reinterpret_cast<const shampoo_tensor_t*>(w + L.off_tensors);
+  const shampoo_block_t* blocks = reinterpret_cast<const shampoo_block_t*>(w + L.off_blocks);
+  const int* flags = reinterpret_cast<const int*>(w + L.off_flags);
+  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(w + L.off_maps);
+  const size_t pb = al((size_t)(n_blocks + 1) * sizeof(int64_t));
+  int64_t* pre1 = reinterpret_cast<int64_t*>(w + L.off_pre);
+  int64_t* pre2 = reinterpret_cast<int64_t*>(w + L.off_pre + pb);
+  int64_t* yoff = reinterpret_cast<int64_t*>(w + L.off_pre + 2 * pb);
+  double* part = reinterpret_cast<double*>(w + L.off_part);
+  float* Y = reinterpret_cast<float*>(w + L.off_Y);
+
+  // tcgen05 3xTF32 path
+  rc = tf32_split_launch(reinterpret_cast<const SplitSeg*>(w + L.off_segs), L.n_segs, stream, launches);
+  if (rc) return rc;
+  rc = tc_gemm_launch(reinterpret_cast<const TcJob*>(w + L.off_jobs1), L.n_jobs1, L.tiles1, maps, stream, launches);
+  if (rc) return rc;
+  rc = tc_gemm_launch(reinterpret_cast<const TcJob*>(w + L.off_jobs2), L.n_jobs2, L.tiles2, maps, stream, launches);
+  if (rc) return rc;
+  // DMMA path for the remaining blocks (left-only, unaligned)
+  if (L.any_dmma) {
+    const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(prec_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+              cudaSuccess ||
+          cudaFuncSetAttribute(prec_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+              cudaSuccess)
+        return set_cuda_error("cudaFuncSetAttribute(prec_gemm_kernel)");
+      configured = true;
+    }
+    prec_prep_kernel<<<1, 1024, 0, stream>>>(blocks, flags, n_blocks, pre1, pre2, yoff);
+    prec_gemm_kernel<1><<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, roots, pre1, yoff, Y);
+    prec_gemm_kernel<2><<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, roots, pre2, yoff, Y);
+    *launches += 3;
   }
   const unsigned eg = (unsigned)n_blocks * kPChunks;
-  prec_prep_kernel<<<1, 1024, 0, stream>>>(blocks, n_blocks, w.pre1, w.pre2, w.yoff);
-  prec_gemm_kernel<1><<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, roots, w.pre1, w.yoff, w.Y);
-  prec_gemm_kernel<2><<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, roots, w.pre2, w.yoff, w.Y);
   prec_diag_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks);
-  prec_den_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.part);
-  prec_finish_kernel<<<(n_blocks + 255) / 256, 256, 0, stream>>>(n_blocks, w.part, graft_num, graft_scale, den);
-  *launches += 6;
+  prec_den_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, part);
+  prec_finish_kernel<<<(n_blocks + 255) / 256, 256, 0, stream>>>(n_blocks, part, graft_num, graft_scale, den);
+  *launches += 3;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("precondition kernels", e);
   return SHAMPOO_OK;

@@ -3,7 +3,8 @@ identical seeded inputs.  Bars (BASELINE.json north star):
   * plan, statistics L/R and D: bit-exact;
   * roots: relative Frobenius error <= 1e-3 (north star); the FP64-DMMA path
     is additionally held to 2e-6 (fp32 output rounding + fp64 iteration);
-  * preconditioned gradient: relative Frobenius error <= 1e-3 (held to 1e-5);
+  * preconditioned gradient: relative Frobenius error <= 1e-3 (held to 2e-5:
+    3xTF32 tcgen05 products, ~1e-6 measured);
   * graft numerator / scale: relative 1e-9 / 1e-5.
 """
 
@@ -309,7 +310,7 @@ def test_precondition_with_oracle_roots(shp):
         Pg = P.cpu().numpy()
         for b in (bb for bb in pl_o.blocks if bb.tensor_id == t):
             sl = (slice(b.row0, b.row0 + b.rows), slice(b.col0, b.col0 + b.cols))
-            assert rel(Pg[sl], Po[sl]) < 1e-6, (t, b.block_index)
+            assert rel(Pg[sl], Po[sl]) < 2e-5, (t, b.block_index)  # 3xTF32 tcgen05 / fp64 DMMA
     np.testing.assert_allclose(den.cpu().numpy(), den_o, rtol=1e-5)
     np.testing.assert_allclose(sc.cpu().numpy(), sc_o, rtol=1e-5)
 
@@ -347,5 +348,55 @@ def test_full_step_config1_chain(shp):
     shp.precondition(table, pl, roots, gn, sc)
     torch.cuda.synchronize()
     assert np.array_equal(bits(stats.cpu().numpy()), bits(stats_o))
-    assert rel(Pd.cpu().numpy(), Ps_o[0]) < 1e-5
+    assert rel(Pd.cpu().numpy(), Ps_o[0]) < 2e-5
     assert abs(sc.cpu().numpy()[0] - sc_o[0]) <= 1e-5 * sc_o[0]
+
+
+def test_precondition_tcgen05_large_blocks(shp):
+    """1024-blocks (the bench's geometry: 32 k-tiles, 8x8 output tiles per block,
+    two-sided + right-only) through the tcgen05 3xTF32 path.  The roots are
+    arbitrary symmetric matrices with random signs (P = X_L G X_R is a plain
+    definition); their sums cancel ~sqrt(K)-fold per product, so the fp32 TMEM
+    accumulation shows up at ~1e-5 here (bar 1e-3; the PSD-root cases above
+    land near 1e-6)."""
+    shapes = [(1024, 2048), (2048, 1024), (3000, 512)]
+    pl_o = oplan.plan(shapes, 1024, 2048, 1)
+    pl = shp.make_plan(shapes, 1024, 2048, 1)
+
+    def rf(b, side, n):
+        S = synth.gaussian((n, n), 5000 + 2 * b.block_index + side).astype(np.float64) / np.sqrt(n)
+        return ((S + S.T) * 0.5).astype(np.float32)
+
+    roots = _pack_roots(pl_o, rf)
+    Gs = [synth.lowrank_gradient(m, n, 80 + i) for i, (m, n) in enumerate(shapes)]
+    Ds = [np.ones(s, np.float32) for s in shapes]
+    num = np.ones(len(pl_o.blocks))
+    Ps_o, sc_o, den_o = opre.precondition_plan(Gs, Ds, pl_o, roots.astype(np.float64), num)
+    Gd = [torch.from_numpy(G).to(DEV) for G in Gs]
+    Pd = [torch.full(s, np.nan, dtype=torch.float32, device=DEV) for s in shapes]
+    table = shp.TensorTable(Gd, [torch.from_numpy(D).to(DEV) for D in Ds], Pd)
+    den = torch.zeros(pl.n_blocks, dtype=torch.float64, device=DEV)
+    shp.precondition(table, pl, torch.from_numpy(roots).to(DEV), None, None, den)
+    torch.cuda.synchronize()
+    worst = 0.0
+    for t, (P, Po) in enumerate(zip(Pd, Ps_o)):
+        Pg = P.cpu().numpy()
+        for b in (bb for bb in pl_o.blocks if bb.tensor_id == t):
+            sl = (slice(b.row0, b.row0 + b.rows), slice(b.col0, b.col0 + b.cols))
+            e = rel(Pg[sl], Po[sl])
+            worst = max(worst, e)
+            assert e < 1e-4, (t, b.block_index, e)
+    print("worst block rel err", worst)
+    np.testing.assert_allclose(den.cpu().numpy(), den_o, rtol=1e-4)
+
+
+def test_precondition_determinism(shp):
+    shapes = [(1024, 1024)]
+    pl = shp.make_plan(shapes, 1024, 8192, 1)
+    G = torch.from_numpy(synth.lowrank_gradient(1024, 1024, 3)).to(DEV)
+    roots = torch.randn(pl.stats_elems, device=DEV)
+    P1, P2 = torch.zeros_like(G), torch.zeros_like(G)
+    shp.precondition(shp.TensorTable([G], [torch.ones_like(G)], [P1]), pl, roots)
+    shp.precondition(shp.TensorTable([G], [torch.ones_like(G)], [P2]), pl, roots)
+    torch.cuda.synchronize()
+    assert torch.equal(P1, P2)
