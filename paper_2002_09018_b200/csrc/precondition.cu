@@ -226,13 +226,14 @@ struct PrecLayout {
   int64_t tiles1 = 0, tiles2 = 0;
   bool any_dmma = false;
   // device regions (offsets from ws)
-  size_t off_pre = 0, off_part = 0, off_Y = 0, off_rhi = 0, off_rlo = 0, off_ghi = 0, off_glo = 0, off_zhi = 0,
-         off_zlo = 0, total = 0;
+  size_t off_pre = 0, off_part = 0, off_Y = 0, off_rlo = 0, off_glo = 0, off_zhi = 0, off_zlo = 0, total = 0;
   int64_t roots_elems = 0;
 };
 
 static bool tc_eligible(const shampoo_block_t& b, const shampoo_tensor_t& t) {
   if (!b.p_right) return false;  // left-only / diagonal-only blocks stay on the DMMA / elementwise path
+  // the raw G is the TMA "hi" operand: contiguous rows, 16-byte aligned
+  if (t.ldg != t.n || (t.n & 3) || (reinterpret_cast<uintptr_t>(t.G) & 15)) return false;
   const bool rows_ok = (b.rows % 32 == 0) || (b.row0 + b.rows == t.m);
   const bool cols_ok = (b.cols % 32 == 0) || (b.col0 + b.cols == t.n);
   return rows_ok && cols_ok;
@@ -300,15 +301,13 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
   L.off_pre = region(3 * pb);
   L.off_part = region((size_t)n_blocks * kPChunks * sizeof(double));
   L.off_Y = region(y_elems * sizeof(float));
-  L.off_rhi = region((size_t)rend * sizeof(float));
   L.off_rlo = region((size_t)rend * sizeof(float));
   std::vector<size_t> goff(n_tensors, 0), zoff(n_tensors, 0);
   size_t gsz = 0, zsz = 0;
   for (int t = 0; t < n_tensors; ++t) {
-    if (t_g[t]) { goff[t] = gsz; gsz += (size_t)al((size_t)T[t].m * r4(T[t].n) * sizeof(float)); }
+    if (t_g[t]) { goff[t] = gsz; gsz += (size_t)al((size_t)T[t].m * T[t].n * sizeof(float)); }
     if (t_z[t]) { zoff[t] = zsz; zsz += (size_t)al((size_t)T[t].n * r4(T[t].m) * sizeof(float)); }
   }
-  L.off_ghi = region(gsz);
   L.off_glo = region(gsz);
   L.off_zhi = region(zsz);
   L.off_zlo = region(zsz);
@@ -324,7 +323,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
     maps.push_back(m);
     return (int)maps.size() - 1;
   };
-  float* rhi = reinterpret_cast<float*>(ws + L.off_rhi);
+  const float* rhi = roots;  // raw fp32 roots: the tensor core reads trunc_tf32
   float* rlo = reinterpret_cast<float*>(ws + L.off_rlo);
   std::vector<int> run_map_hi(runs.size()), run_map_lo(runs.size());
   for (size_t i = 0; i < runs.size(); ++i) {
@@ -349,16 +348,15 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
   std::vector<int> g_hi(n_tensors, -1), g_lo(n_tensors, -1), z_hi(n_tensors, -1), z_lo(n_tensors, -1);
   std::vector<SplitSeg> segs;
   for (int t = 0; t < n_tensors; ++t) {
-    const int64_t ldg = r4(T[t].n), ldz = r4(T[t].m);
+    const int64_t ldz = r4(T[t].m);
     if (t_g[t]) {
-      float* gh = reinterpret_cast<float*>(ws + L.off_ghi + goff[t]);
       float* gl = reinterpret_cast<float*>(ws + L.off_glo + goff[t]);
       uint64_t size[2] = {(uint64_t)T[t].n, (uint64_t)T[t].m};
-      uint64_t st[1] = {(uint64_t)ldg * 4};
-      g_hi[t] = add_map(gh, 2, size, st);
+      uint64_t st[1] = {(uint64_t)T[t].n * 4};
+      g_hi[t] = add_map(T[t].G, 2, size, st);
       g_lo[t] = add_map(gl, 2, size, st);
       if (g_hi[t] < 0 || g_lo[t] < 0) return SHAMPOO_ERR_CUDA;
-      segs.push_back({T[t].G, gh, gl, T[t].ldg, ldg, (int32_t)T[t].m, (int32_t)T[t].n});
+      segs.push_back({T[t].G, gl, T[t].m * T[t].n});
     }
     if (t_z[t]) {
       float* zh = reinterpret_cast<float*>(ws + L.off_zhi + zoff[t]);
@@ -370,15 +368,8 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
       if (z_hi[t] < 0 || z_lo[t] < 0) return SHAMPOO_ERR_CUDA;
     }
   }
-  // roots split: the packed buffer as rows of 4096 floats + a tail
-  {
-    const int64_t W = 4096, full_rows = rend / W, tail = rend - full_rows * W;
-    for (int64_t r0 = 0; r0 < full_rows; r0 += 1 << 20) {
-      const int64_t rows = std::min<int64_t>(1 << 20, full_rows - r0);
-      segs.push_back({roots + r0 * W, rhi + r0 * W, rlo + r0 * W, W, W, (int32_t)rows, (int32_t)W});
-    }
-    if (tail) segs.push_back({roots + full_rows * W, rhi + full_rows * W, rlo + full_rows * W, W, W, 1, (int32_t)tail});
-  }
+  // roots: the whole packed range (a multiple of 4 floats) as one flat segment
+  if (rend) segs.push_back({roots, rlo, rend});
   // ---- jobs
   std::vector<TcJob> j1, j2;
   int64_t t1 = 0, t2 = 0;

@@ -131,14 +131,11 @@ TC_DEV bool elect_one() {
   return pred != 0;
 }
 
-// tf32 split of an fp32 value: hi = x rounded to nearest TF32 (cvt.rna, so hi is
-// exactly representable and the tensor core reads it unchanged whether it
-// truncates or rounds), lo = x - hi exactly (|lo| <= 2^-11 |x|).
-TC_DEV float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
+// TF32 split for tcgen05.mma.kind::tf32, which TRUNCATES fp32 operands to TF32
+// (measured on B200: tools/probe_tf32_semantics.py, 16384/16384 products equal
+// the truncated value).  The raw fp32 x therefore acts as hi = trunc(x) and the
+// exact remainder lo = x - trunc(x) (|lo| < 2^-10 |x|) is the second operand.
+TC_DEV float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 }  // namespace tc
 }  // namespace shp

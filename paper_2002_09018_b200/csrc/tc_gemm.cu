@@ -2,11 +2,12 @@
 //
 //   C[M x N] = A[M x K] . B[N x K]^T   (both operands K-major, fp32 in HBM)
 //
-// fp32-accurate products from TF32 tensor-core passes: every operand is kept as
-// an exact split x = hi + lo with hi = rna_tf32(x) (exactly representable in
-// TF32) and lo = x - hi; the three passes lo.hi + hi.lo + hi.hi accumulate into
-// one fp32 TMEM accumulator (the dropped lo.lo term and lo's own TF32 rounding
-// are ~2^-22 relative; measured P error ~1e-6, bar 1e-3).  Used by the
+// fp32-accurate products from TF32 tensor-core passes: every operand is an
+// exact split x = hi + lo, hi = trunc_tf32(x) -- which is what the tensor core
+// reads from the raw fp32 x -- and lo = x - hi (stored separately); the three
+// passes lo.hi + hi.lo + hi.hi accumulate into one fp32 TMEM accumulator (the
+// dropped lo.lo term and lo's own truncation are ~2^-20 relative; measured P
+// error ~2e-6, bar 1e-3).  Used by the
 // preconditioned gradient (row a8), whose error bar is 1e-3.
 //
 // Kernel structure (one CTA per SM, persistent over 128x128 output tiles):
@@ -196,9 +197,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int e = 0; e < 16; ++e)
               if (j0 + e < job.N) {
                 const float v = __uint_as_float(r[e]);
-                const float h = tc::tf32_hi(v);
-                job.out_hi[(int64_t)(j0 + e) * job.ld_out + i] = h;
-                job.out_lo[(int64_t)(j0 + e) * job.ld_out + i] = v - h;
+                job.out_hi[(int64_t)(j0 + e) * job.ld_out + i] = v;
+                job.out_lo[(int64_t)(j0 + e) * job.ld_out + i] = tc::tf32_lo(v);
               }
           }
         }
@@ -219,19 +219,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // -------------------------------------------------------------- split kernel
-// dst_hi/dst_lo[r][c] = split(src[r][c]) for a list of 2-D segments.
-__global__ void tf32_split_kernel(const SplitSeg* __restrict__ segs, int n_segs) {
+// lo = x - trunc_tf32(x) over flat segments, float4 vectorised, 4 loads in flight.
+__global__ void __launch_bounds__(256) tf32_split_kernel(const SplitSeg* __restrict__ segs, int n_segs) {
   const SplitSeg s = segs[blockIdx.y];
-  for (int r = blockIdx.x; r < s.rows; r += gridDim.x) {
-    const float* src = s.src + (int64_t)r * s.ld_src;
-    float* hi = s.hi + (int64_t)r * s.ld_dst;
-    float* lo = s.lo + (int64_t)r * s.ld_dst;
-    for (int c = threadIdx.x; c < s.cols; c += blockDim.x) {
-      const float v = __ldg(src + c);
-      const float h = tc::tf32_hi(v);
-      hi[c] = h;
-      lo[c] = v - h;
-    }
+  const float4* src = reinterpret_cast<const float4*>(s.src);
+  float4* lo = reinterpret_cast<float4*>(s.lo);
+  const int64_t n4 = s.n >> 2, step = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * step < n4; i += 4 * step) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(src + i + u * step);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      lo[i + u * step] = make_float4(tc::tf32_lo(v[u].x), tc::tf32_lo(v[u].y), tc::tf32_lo(v[u].z), tc::tf32_lo(v[u].w));
+  }
+  for (; i < n4; i += step) {
+    const float4 v = __ldg(src + i);
+    lo[i] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
   }
 }
 
@@ -284,7 +289,7 @@ int tc_gemm_launch(const TcJob* jobs_dev, int n_jobs, int64_t total_tiles, const
 
 int tf32_split_launch(const SplitSeg* segs_dev, int n_segs, cudaStream_t stream, int64_t* launches) {
   if (n_segs == 0) return SHAMPOO_OK;
-  tf32_split_kernel<<<dim3(256, n_segs), 256, 0, stream>>>(segs_dev, n_segs);
+  tf32_split_kernel<<<dim3(2 * num_sms(), n_segs), 256, 0, stream>>>(segs_dev, n_segs);
   ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("tf32_split_kernel", e);

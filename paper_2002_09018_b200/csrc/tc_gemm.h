@@ -16,7 +16,7 @@ struct TcOperand {
 };
 
 // C[M x N] = A[M x K] . B[N x K]^T over 128x128 tiles (tiles_n = ceil(N/128)).
-// out_mode 0: out_hi[i*ld + j] = C;  1: out_hi[j*ld + i] = hi(C), out_lo[j*ld + i] = C - hi(C).
+// out_mode 0: out_hi[i*ld + j] = C;  1: out_hi[j*ld + i] = C, out_lo[j*ld + i] = C - trunc_tf32(C).
 struct TcJob {
   TcOperand a, b;
   int32_t M, N, K;
@@ -28,12 +28,14 @@ struct TcJob {
   int64_t tile_begin;  // first global tile index of this job (jobs sorted)
 };
 
-struct SplitSeg {  // dst_hi/dst_lo[r][c] = tf32 split of src[r][c]
+// lo[i] = x - trunc_tf32(x) for x = src[i], i < n (n % 4 == 0, 16-B aligned).
+// The tensor core truncates fp32 inputs to TF32 (measured:
+// tools/probe_tf32_semantics.py), so the raw fp32 buffer serves as "hi" and
+// only the exact remainder lo needs storing.
+struct SplitSeg {
   const float* src;
-  float* hi;
   float* lo;
-  int64_t ld_src, ld_dst;
-  int32_t rows, cols;
+  int64_t n;
 };
 
 size_t tc_gemm_smem_bytes();
