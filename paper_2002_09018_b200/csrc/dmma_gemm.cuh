@@ -172,9 +172,15 @@ SHP_DEV void gemm_tile(Acc& acc, const LA& la, const LB& lb, int k_tiles, double
 
 // ---------------------------------------------------- cp.async fp64 pipeline
 // For fp64 row panels (the Newton products): LDGSTS 16-byte copies straight
-// into the swizzled tile, kStages-deep ring, no register staging.
+// into the swizzled tile, kStages-deep ring of 32-deep k tiles (64 KB per
+// stage), no register staging.  Same swizzle X(r) on the low 3 chunk bits
+// (rows are 256 B, a multiple of the 128-B bank window).
 constexpr int kStages = 3;
-constexpr int kAsyncSmemDoubles = kStages * 2 * kTileElems;
+constexpr int kAsyncK = 32;
+constexpr int kAsyncTile = kTileM * kAsyncK;               // doubles per operand tile
+constexpr int kAsyncSmemDoubles = kStages * 2 * kAsyncTile;
+
+SHP_DEV int swz32(int r, int k) { return r * kAsyncK + ((((k >> 1) ^ swx(r)) << 1) | (k & 1)); }
 
 SHP_DEV void cp_async16(void* smem_dst, const void* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -187,13 +193,35 @@ SHP_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)
 SHP_DEV void f64_issue(double* s, const double* base, int64_t ld, int kt) {
   const int t = threadIdx.x;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int id = t + kThreads * q, row = id >> 3, c = id & 7;
-    cp_async16(s + swc(row, c), base + (int64_t)row * ld + kt * kTileK + 2 * c);
+  for (int q = 0; q < 8; ++q) {
+    const int id = t + kThreads * q, row = id >> 4, c = id & 15;
+    cp_async16(s + row * kAsyncK + ((c ^ swx(row)) << 1), base + (int64_t)row * ld + kt * kAsyncK + 2 * c);
   }
 }
 
-// C = A_panel . B_panel^T over K = 16 * k_tiles, both fp64 row panels.
+SHP_DEV void load_frags32(double (&a)[8], double (&b)[4], const double* sA, const double* sB, int ra, int rb, int k) {
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) a[mt] = sA[swz32(ra + mt * 8, k)];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) b[nt] = sB[swz32(rb + nt * 8, k)];
+}
+
+SHP_DEV void mma_ktile32(Acc& acc, const double* sA, const double* sB, int warp, int lane) {
+  const int ra = (warp & 1) * 64 + (lane >> 2);
+  const int rb = (warp >> 1) * 32 + (lane >> 2);
+  double a[2][8], b[2][4];
+  load_frags32(a[0], b[0], sA, sB, ra, rb, lane & 3);
+#pragma unroll
+  for (int g = 0; g < kAsyncK / 4; ++g) {
+    if (g + 1 < kAsyncK / 4) load_frags32(a[(g + 1) & 1], b[(g + 1) & 1], sA, sB, ra, rb, 4 * (g + 1) + (lane & 3));
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma884(acc.c[mt][nt][0], acc.c[mt][nt][1], a[g & 1][mt], b[g & 1][nt]);
+  }
+}
+
+// C = A_panel . B_panel^T over K = 32 * k_tiles, both fp64 row panels.
 // `smem` holds kAsyncSmemDoubles doubles.  Ends with __syncthreads.
 SHP_DEV void gemm_tile_f64(Acc& acc, const double* A, const double* B, int64_t ld, int k_tiles, double* smem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -201,8 +229,8 @@ SHP_DEV void gemm_tile_f64(Acc& acc, const double* A, const double* B, int64_t l
 #pragma unroll
   for (int st = 0; st < kStages - 1; ++st) {
     if (st < k_tiles) {
-      f64_issue(smem + st * 2 * kTileElems, A, ld, st);
-      f64_issue(smem + st * 2 * kTileElems + kTileElems, B, ld, st);
+      f64_issue(smem + st * 2 * kAsyncTile, A, ld, st);
+      f64_issue(smem + st * 2 * kAsyncTile + kAsyncTile, B, ld, st);
     }
     cp_async_commit();
   }
@@ -211,13 +239,13 @@ SHP_DEV void gemm_tile_f64(Acc& acc, const double* A, const double* B, int64_t l
     __syncthreads();  // stage kt visible to all; stage kt-1 fully consumed
     const int nk = kt + kStages - 1;
     if (nk < k_tiles) {
-      double* s = smem + (nk % kStages) * 2 * kTileElems;
+      double* s = smem + (nk % kStages) * 2 * kAsyncTile;
       f64_issue(s, A, ld, nk);
-      f64_issue(s + kTileElems, B, ld, nk);
+      f64_issue(s + kAsyncTile, B, ld, nk);
     }
     cp_async_commit();
-    const double* cur = smem + (kt % kStages) * 2 * kTileElems;
-    mma_ktile(acc, cur, cur + kTileElems, warp, lane);
+    const double* cur = smem + (kt % kStages) * 2 * kAsyncTile;
+    mma_ktile32(acc, cur, cur + kAsyncTile, warp, lane);
   }
   cp_async_wait<0>();
   __syncthreads();

@@ -111,24 +111,60 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
   double lam = 0.0;
   const bool vec4 = ((a.lda & 3) == 0) && ((n & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   for (int it = 0; it < a.power_iters; ++it) {
-    for (int r = warp; r < n; r += kThreads / 32) {
-      const float* row = A + (int64_t)r * a.lda;
-      double acc = 0.0;
-      if (vec4) {
-#pragma unroll 4
-        for (int c = 4 * lane; c < n; c += 128) {
-          float4 q = __ldg(reinterpret_cast<const float4*>(row + c));
-          acc = fma((double)q.x, v[c], acc);
-          acc = fma((double)q.y, v[c + 1], acc);
-          acc = fma((double)q.z, v[c + 2], acc);
-          acc = fma((double)q.w, v[c + 3], acc);
+    if (vec4) {
+      // 4 rows per warp pass x 4 column chunks (128 floats each) per row: 16 float4
+      // loads in flight per lane.  Each lane accumulates its columns in ascending
+      // order, so the reduction order is fixed (deterministic).
+      for (int r0 = warp * 4; r0 < n; r0 += 4 * (kThreads / 32)) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const float* rows[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rows[q] = A + (int64_t)min(r0 + q, n - 1) * a.lda;
+        int c = 4 * lane;
+        for (; c + 3 * 128 < n; c += 4 * 128) {
+          float4 f[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) f[q][u] = __ldg(reinterpret_cast<const float4*>(rows[q] + c + u * 128));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cc = c + u * 128;
+            const double v0 = v[cc], v1 = v[cc + 1], v2 = v[cc + 2], v3 = v[cc + 3];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[q] = fma((double)f[q][u].x, v0, acc[q]);
+              acc[q] = fma((double)f[q][u].y, v1, acc[q]);
+              acc[q] = fma((double)f[q][u].z, v2, acc[q]);
+              acc[q] = fma((double)f[q][u].w, v3, acc[q]);
+            }
+          }
         }
-      } else {
+        for (; c < n; c += 128) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(rows[q] + c));
+            acc[q] = fma((double)f.x, v[c], acc[q]);
+            acc[q] = fma((double)f.y, v[c + 1], acc[q]);
+            acc[q] = fma((double)f.z, v[c + 2], acc[q]);
+            acc[q] = fma((double)f.w, v[c + 3], acc[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double s = warp_sum_fixed(acc[q]);
+          if (lane == 0 && r0 + q < n) w[r0 + q] = s;
+        }
+      }
+    } else {
+      for (int r = warp; r < n; r += kThreads / 32) {
+        const float* row = A + (int64_t)r * a.lda;
+        double acc = 0.0;
 #pragma unroll 4
         for (int c = lane; c < n; c += 32) acc = fma((double)__ldg(row + c), v[c], acc);
+        acc = warp_sum_fixed(acc);
+        if (lane == 0) w[r] = acc;
       }
-      acc = warp_sum_fixed(acc);
-      if (lane == 0) w[r] = acc;
     }
     __syncthreads();
     double pl = 0.0, pw = 0.0;
@@ -253,48 +289,39 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
   }
   grid.sync();
 
-  // ---- phase 1: setup M_0, T_0, X_0 and err_0
+  // ---- phase 1: setup M_0, T_0, X_0 and err_0 (one warp per padded row)
   {
-    const int64_t total = (int64_t)a.batch * np2;
-    const int lane = threadIdx.x & 31;
-    for (int64_t base = (int64_t)blockIdx.x * kThreads; base < total; base += (int64_t)gridDim.x * kThreads) {
-      const int64_t idx = base + threadIdx.x;
+    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (kThreads / 32);
+    const int64_t rows = (int64_t)a.batch * np;
+    for (int64_t rid = gw; rid < rows; rid += nw) {
+      const int mat = (int)(rid / np), i = (int)(rid - (int64_t)mat * np);
+      const double lam = a.lam[mat];
+      if (!lam_ok(lam)) continue;  // warp-uniform
+      const double c = lam * (1.0 + a.eps_rel);
+      const double xd = c_pow_neg_inv_p(c, a.p), inv_p = 1.0 / (double)a.p;
+      const float* arow = a.A + (int64_t)mat * a.stride_a + (int64_t)i * a.lda;
+      double* mrow = buf(a, mat, BM0) + (int64_t)i * np;
+      double* trow = buf(a, mat, BT) + (int64_t)i * np;
+      double* xrow = buf(a, mat, BX0) + (int64_t)i * np;
       double e = 0.0;
-      int mat = -1;
-      if (idx < total) {
-        mat = (int)(idx / np2);
-        const int64_t rem = idx - (int64_t)mat * np2;
-        const int i = (int)(rem / np), j = (int)(rem - (int64_t)i * np);
-        const double lam = a.lam[mat];
-        if (lam_ok(lam)) {
-          const double c = lam * (1.0 + a.eps_rel);
-          const bool valid = i < a.n && j < a.n;
-          double m = 0.0, t = 0.0, x = 0.0;
-          if (valid) {
-            // upper triangle (statistics are symmetric by construction)
-            const int r = i < j ? i : j, q = i < j ? j : i;
-            double av = (double)a.A[(int64_t)mat * a.stride_a + (int64_t)r * a.lda + q];
-            if (i == j) av = __dadd_rn(av, __dmul_rn(a.eps_rel, lam));  // (eps*lam) rounded, then added
-            m = av / c;
-            const double d = (i == j) ? 1.0 : 0.0;
-            t = ((double)(a.p + 1) * d - m) * (1.0 / (double)a.p);
-            x = (i == j) ? c_pow_neg_inv_p(c, a.p) : 0.0;
-            e = fabs(m - d);
-          }
-          buf(a, mat, BM0)[rem] = m;
-          buf(a, mat, BT)[rem] = t;
-          buf(a, mat, BX0)[rem] = x;
+      for (int j = lane; j < np; j += 32) {
+        double m = 0.0, t = 0.0, x = 0.0;
+        if (i < a.n && j < a.n) {
+          double av = (double)arow[j];
+          if (i == j) av = __dadd_rn(av, __dmul_rn(a.eps_rel, lam));  // (eps*lam) rounded, then added
+          m = av / c;
+          const double d = (i == j) ? 1.0 : 0.0;
+          t = ((double)(a.p + 1) * d - m) * inv_p;
+          x = (i == j) ? xd : 0.0;
+          e = fmax_nan(e, fabs(m - d));
         }
+        mrow[j] = m;
+        trow[j] = t;
+        xrow[j] = x;
       }
-      // warp-level max over the (possibly two) matrices touched by this warp
-      const int mat0 = __shfl_sync(0xffffffffu, mat, 0);
-      const bool same = __all_sync(0xffffffffu, mat == mat0 || mat < 0);
-      if (same) {
-        double w = warp_max(e);
-        if (lane == 0 && mat0 >= 0 && lam_ok(a.lam[mat0])) atomic_max_nonneg(a.errh + (int64_t)mat0 * (a.max_iter + 1), w);
-      } else if (mat >= 0 && lam_ok(a.lam[mat])) {
-        atomic_max_nonneg(a.errh + (int64_t)mat * (a.max_iter + 1), e);
-      }
+      e = warp_max(e);
+      if (lane == 0) atomic_max_nonneg(a.errh + (int64_t)mat * (a.max_iter + 1), e);
     }
   }
   grid.sync();
@@ -325,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         upper_tile(t, T, ti, tj);
         const double* Aop = (job == 0) ? buf(a, mat, BX0 + xs) : buf(a, mat, tb);
         const double* Bop = buf(a, mat, tb);
-        gemm_tile_f64(acc, Aop + (int64_t)ti * kTileM * np, Bop + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
+        gemm_tile_f64(acc, Aop + (int64_t)ti * kTileM * np, Bop + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
         double* dst = (job == 0) ? buf(a, mat, BX0 + (xs ^ 1)) : buf(a, mat, BS0);
         epilogue<EPI_STORE>(a, acc, mat, ti, tj, dst, nullptr, nullptr);
       }
@@ -341,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         int ti, tj;
         upper_tile(t, T, ti, tj);
         const double* S = buf(a, mat, src);
-        gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
+        gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
         epilogue<EPI_STORE>(a, acc, mat, ti, tj, buf(a, mat, dstb), nullptr, nullptr);
       }
       grid.sync();
@@ -356,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         int ti, tj;
         upper_tile(t, T, ti, tj);
         gemm_tile_f64(acc, buf(a, mat, tp) + (int64_t)ti * kTileM * np,
-                      buf(a, mat, BM0 + xs) + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
+                      buf(a, mat, BM0 + xs) + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
         epilogue<EPI_MUPDATE>(a, acc, mat, ti, tj, buf(a, mat, BM0 + (xs ^ 1)), buf(a, mat, tb_next),
                               a.errh + (int64_t)mat * (a.max_iter + 1) + (k + 1));
       }
@@ -400,16 +427,19 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
   }
   grid.sync();
   {
-    const int n = a.n;
-    const int64_t nn = (int64_t)n * n, total = (int64_t)a.batch * nn;
-    for (int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kThreads) {
-      const int mat = (int)(idx / nn);
-      const int64_t rem = idx - (int64_t)mat * nn;
-      const int i = (int)(rem / n), j = (int)(rem - (int64_t)i * n);
+    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (kThreads / 32);
+    const int64_t rows = (int64_t)a.batch * a.n;
+    for (int64_t rid = gw; rid < rows; rid += nw) {
+      const int mat = (int)(rid / a.n), i = (int)(rid - (int64_t)mat * a.n);
       const int4 r = a.res[mat];
-      float* out = a.X + (int64_t)mat * a.stride_x + (int64_t)i * a.ldx + j;
-      if (r.z == 3) *out = (i == j) ? 1.0f : 0.0f;
-      else if (r.x >= 0) *out = (float)buf(a, mat, r.x)[(int64_t)i * np + j];
+      float* out = a.X + (int64_t)mat * a.stride_x + (int64_t)i * a.ldx;
+      if (r.z == 3) {
+        for (int j = lane; j < a.n; j += 32) out[j] = (i == j) ? 1.0f : 0.0f;
+      } else if (r.x >= 0) {
+        const double* src = buf(a, mat, r.x) + (int64_t)i * np;
+        for (int j = lane; j < a.n; j += 32) out[j] = (float)src[j];
+      }
     }
   }
 }
@@ -536,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
       int ti, tj;
       upper_tile(t, T, ti, tj);
       const double* S = rbuf(a, mat, src);
-      gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kTileK, smem);
+      gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       double* D = rbuf(a, mat, dst);
 #pragma unroll
@@ -561,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
     const int mat = it / (T * T), t = it - mat * T * T;
     const int ti = t / T, tj = t - ti * T;
     gemm_tile_f64(acc, rbuf(a, mat, src) + (int64_t)ti * kTileM * np, rbuf(a, mat, 3) + (int64_t)tj * kTileM * np,
-                  np, np / kTileK, smem);
+                  np, np / kAsyncK, smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double s = 0.0;
 #pragma unroll

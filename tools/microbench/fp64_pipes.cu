@@ -80,6 +80,39 @@ __global__ void dmma_16816_peak(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Mixed: even warps run DMMA chains, odd warps run DFMA chains -- do the two
+// FP64 datapaths (tensor DMMA subpipe vs FP64 ALU pipe) add up?
+__global__ void mixed_peak(double* out, int iters) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if (warp & 1) {
+    double a[8];
+    double b = 1.0000001 + threadIdx.x * 1e-9, c = 0.999999;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = i * 0.1 + blockIdx.x * 1e-7;
+    for (int it = 0; it < iters * 16; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += a[i];
+  } else {
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { acc[i][0] = 0; acc[i][1] = 0; }
+    double a = 1.0 + threadIdx.x * 1e-9, b = 0.5 + blockIdx.x * 1e-9;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[i][0]), "+d"(acc[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 // Rounding semantics: one m8n8k4 per trial. A row-major 8x4, B col-major (4x8), C 8x8.
 __global__ void dmma_semantics(const double* A, const double* B, const double* C, double* D, int trials) {
   int lane = threadIdx.x;
@@ -120,6 +153,8 @@ int main() {
     timeit("dmma_m16n8k4", dmma_1684_peak, sms * occ, 256, 20000, 8 * 2.0 * 512 / 32, dout);
     timeit("dmma_m16n8k16", dmma_16816_peak, sms * occ, 256, 10000, 4 * 2.0 * 2048 / 32, dout);
   }
+  // mixed: per warp pair, DMMA warp does iters*8*256 FMA, DFMA warp iters*16*8*32 = same count
+  for (int occ : {1, 2}) timeit("mixed dmma+dfma", mixed_peak, sms * occ, 256, 10000, 8 * 2.0 * 256 / 32, dout);
   // semantics
   const int T = 4096;
   double *hA = (double*)malloc(T * 32 * 8), *hB = (double*)malloc(T * 32 * 8), *hC = (double*)malloc(T * 64 * 8), *hD = (double*)malloc(T * 64 * 8);

@@ -20,6 +20,8 @@ ap.add_argument("--batch", type=int, default=148)
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--p", type=int, default=4)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--max-iter", type=int, default=100)
+ap.add_argument("--power-iters", type=int, default=100)
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -28,7 +30,7 @@ X = torch.empty_like(A)
 for r in range(args.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    X, info = shp.inverse_pth_root_batched(A, args.p, X=X)
+    X, info = shp.inverse_pth_root_batched(A, args.p, X=X, max_iter=args.max_iter, power_iters=args.power_iters)
     e1.record()
     torch.cuda.synchronize()
 inf = shp.info_to_numpy(info)
