@@ -171,14 +171,33 @@ SHP_DEV void gemm_tile(Acc& acc, const LA& la, const LB& lb, int k_tiles, double
 }
 
 // ---------------------------------------------------- cp.async fp64 pipeline
-// For fp64 row panels (the Newton products): LDGSTS 16-byte copies straight
-// into the swizzled tile, kStages-deep ring of 32-deep k tiles (64 KB per
-// stage), no register staging.  Same swizzle X(r) on the low 3 chunk bits
-// (rows are 256 B, a multiple of the 128-B bank window).
+// For fp64 row panels (the Newton products).  A compact CTA: 64x64 output tile,
+// 4 warps (2x2), warp tile 32x32 = 4x4 DMMA 8x8 tiles (64 accumulator
+// registers), so that TWO CTAs fit on an SM (registers and 2 x 96 KB of shared
+// memory) and one CTA's epilogue / pipeline fill / barrier overlaps the other
+// CTA's DMMA stream.  Operands arrive by LDGSTS 16-byte copies straight into the
+// swizzled tiles, a kStages-deep ring of 32-deep k tiles.  Rows are 256 B (a
+// multiple of the 128-B bank window), so the same X(r) swizzle on the low 3
+// chunk bits keeps fragment reads and copies conflict-free.
 constexpr int kStages = 3;
 constexpr int kAsyncK = 32;
-constexpr int kAsyncTile = kTileM * kAsyncK;               // doubles per operand tile
-constexpr int kAsyncSmemDoubles = kStages * 2 * kAsyncTile;
+constexpr int kNT = 64;                                     // Newton tile (square)
+constexpr int kNThreads = 128;
+constexpr int kAsyncTile = kNT * kAsyncK;                   // doubles per operand tile
+constexpr int kAsyncSmemDoubles = kStages * 2 * kAsyncTile;  // 96 KB
+
+struct AccN {
+  double c[4][4][2];
+};
+
+SHP_DEV void accn_zero(AccN& a) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a.c[i][j][0] = a.c[i][j][1] = 0.0;
+}
+SHP_DEV int accn_row(int warp, int lane, int mt) { return (warp & 1) * 32 + mt * 8 + (lane >> 2); }
+SHP_DEV int accn_col(int warp, int lane, int nt, int e) { return (warp >> 1) * 32 + nt * 8 + 2 * (lane & 3) + e; }
 
 SHP_DEV int swz32(int r, int k) { return r * kAsyncK + ((((k >> 1) ^ swx(r)) << 1) | (k & 1)); }
 
@@ -193,39 +212,40 @@ SHP_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)
 SHP_DEV void f64_issue(double* s, const double* base, int64_t ld, int kt) {
   const int t = threadIdx.x;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int id = t + kThreads * q, row = id >> 4, c = id & 15;
+  for (int q = 0; q < kAsyncTile / 2 / kNThreads; ++q) {
+    const int id = t + kNThreads * q, row = id >> 4, c = id & 15;
     cp_async16(s + row * kAsyncK + ((c ^ swx(row)) << 1), base + (int64_t)row * ld + kt * kAsyncK + 2 * c);
   }
 }
 
-SHP_DEV void load_frags32(double (&a)[8], double (&b)[4], const double* sA, const double* sB, int ra, int rb, int k) {
+SHP_DEV void load_fragsn(double (&a)[4], double (&b)[4], const double* sA, const double* sB, int ra, int rb, int k) {
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) a[mt] = sA[swz32(ra + mt * 8, k)];
+  for (int mt = 0; mt < 4; ++mt) a[mt] = sA[swz32(ra + mt * 8, k)];
 #pragma unroll
   for (int nt = 0; nt < 4; ++nt) b[nt] = sB[swz32(rb + nt * 8, k)];
 }
 
-SHP_DEV void mma_ktile32(Acc& acc, const double* sA, const double* sB, int warp, int lane) {
-  const int ra = (warp & 1) * 64 + (lane >> 2);
+SHP_DEV void mma_ktilen(AccN& acc, const double* sA, const double* sB, int warp, int lane) {
+  const int ra = (warp & 1) * 32 + (lane >> 2);
   const int rb = (warp >> 1) * 32 + (lane >> 2);
-  double a[2][8], b[2][4];
-  load_frags32(a[0], b[0], sA, sB, ra, rb, lane & 3);
+  double a[2][4], b[2][4];
+  load_fragsn(a[0], b[0], sA, sB, ra, rb, lane & 3);
 #pragma unroll
   for (int g = 0; g < kAsyncK / 4; ++g) {
-    if (g + 1 < kAsyncK / 4) load_frags32(a[(g + 1) & 1], b[(g + 1) & 1], sA, sB, ra, rb, 4 * (g + 1) + (lane & 3));
+    if (g + 1 < kAsyncK / 4) load_fragsn(a[(g + 1) & 1], b[(g + 1) & 1], sA, sB, ra, rb, 4 * (g + 1) + (lane & 3));
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) dmma884(acc.c[mt][nt][0], acc.c[mt][nt][1], a[g & 1][mt], b[g & 1][nt]);
   }
 }
 
-// C = A_panel . B_panel^T over K = 32 * k_tiles, both fp64 row panels.
-// `smem` holds kAsyncSmemDoubles doubles.  Ends with __syncthreads.
-SHP_DEV void gemm_tile_f64(Acc& acc, const double* A, const double* B, int64_t ld, int k_tiles, double* smem) {
+// C = A_panel . B_panel^T over K = 32 * k_tiles for a 64x64 tile; both operands
+// fp64 row panels (64 rows from A and B).  `smem` holds kAsyncSmemDoubles doubles.
+// All kNThreads threads call it; ends with __syncthreads.
+SHP_DEV void gemm_tile_f64(AccN& acc, const double* A, const double* B, int64_t ld, int k_tiles, double* smem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  acc_zero(acc);
+  accn_zero(acc);
 #pragma unroll
   for (int st = 0; st < kStages - 1; ++st) {
     if (st < k_tiles) {
@@ -245,7 +265,7 @@ SHP_DEV void gemm_tile_f64(Acc& acc, const double* A, const double* B, int64_t l
     }
     cp_async_commit();
     const double* cur = smem + (kt % kStages) * 2 * kAsyncTile;
-    mma_ktile32(acc, cur, cur + kAsyncTile, warp, lane);
+    mma_ktilen(acc, cur, cur + kAsyncTile, warp, lane);
   }
   cp_async_wait<0>();
   __syncthreads();

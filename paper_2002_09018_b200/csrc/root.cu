@@ -32,6 +32,7 @@ namespace cg = cooperative_groups;
 namespace shp {
 
 constexpr int kBufs = 7;  // X0, X1, M0, M1, T, S0, S1
+constexpr int kRT = kNThreads;  // threads per root-kernel CTA (2 CTAs per SM)
 enum { BX0 = 0, BX1 = 1, BM0 = 2, BM1 = 3, BT = 4, BS0 = 5, BS1 = 6 };
 constexpr double kStagnationGate = 1e-2;
 constexpr int kMaxBatchPerLaunch = 2048;
@@ -87,7 +88,7 @@ SHP_DEV double block_sum(double v, double* red) {
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < kThreads / 32; ++w) s = __dadd_rn(s, red[w]);
+  for (int w = 0; w < kRT / 32; ++w) s = __dadd_rn(s, red[w]);
   return s;
 }
 
@@ -100,31 +101,35 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
   const float* A = a.A + (int64_t)mat * a.stride_a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double part = 0.0;
-  for (int i = threadIdx.x; i < n; i += kThreads) {
+  for (int i = threadIdx.x; i < n; i += kRT) {
     double x = (double)(splitmix64((uint64_t)i) >> 11) * 0x1.0p-53 * 2.0 - 1.0;
     v[i] = x;
     part = fma(x, x, part);
   }
   double nv = sqrt(block_sum(part, red));
-  for (int i = threadIdx.x; i < n; i += kThreads) v[i] = v[i] / nv;
+  for (int i = threadIdx.x; i < n; i += kRT) v[i] = v[i] / nv;
   __syncthreads();
   double lam = 0.0;
   const bool vec4 = ((a.lda & 3) == 0) && ((n & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   for (int it = 0; it < a.power_iters; ++it) {
     if (vec4) {
-      // 4 rows per warp pass x 4 column chunks (128 floats each) per row: 16 float4
-      // loads in flight per lane.  Each lane accumulates its columns in ascending
-      // order, so the reduction order is fixed (deterministic).
-      for (int r0 = warp * 4; r0 < n; r0 += 4 * (kThreads / 32)) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const float* rows[4];
+      // kPR rows per warp pass x 4 column chunks (128 floats each) per row:
+      // 4*kPR float4 loads in flight per lane.  Each lane accumulates its columns in
+      // ascending order, so the reduction order is fixed (deterministic).
+      constexpr int kPR = 8;
+      for (int r0 = warp * kPR; r0 < n; r0 += kPR * (kRT / 32)) {
+        double acc[kPR];
+        const float* rows[kPR];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) rows[q] = A + (int64_t)min(r0 + q, n - 1) * a.lda;
+        for (int q = 0; q < kPR; ++q) {
+          acc[q] = 0.0;
+          rows[q] = A + (int64_t)min(r0 + q, n - 1) * a.lda;
+        }
         int c = 4 * lane;
         for (; c + 3 * 128 < n; c += 4 * 128) {
-          float4 f[4][4];
+          float4 f[kPR][4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < kPR; ++q)
 #pragma unroll
             for (int u = 0; u < 4; ++u) f[q][u] = __ldg(reinterpret_cast<const float4*>(rows[q] + c + u * 128));
 #pragma unroll
@@ -132,7 +137,7 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
             const int cc = c + u * 128;
             const double v0 = v[cc], v1 = v[cc + 1], v2 = v[cc + 2], v3 = v[cc + 3];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < kPR; ++q) {
               acc[q] = fma((double)f[q][u].x, v0, acc[q]);
               acc[q] = fma((double)f[q][u].y, v1, acc[q]);
               acc[q] = fma((double)f[q][u].z, v2, acc[q]);
@@ -142,7 +147,7 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
         }
         for (; c < n; c += 128) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < kPR; ++q) {
             const float4 f = __ldg(reinterpret_cast<const float4*>(rows[q] + c));
             acc[q] = fma((double)f.x, v[c], acc[q]);
             acc[q] = fma((double)f.y, v[c + 1], acc[q]);
@@ -151,13 +156,13 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kPR; ++q) {
           const double s = warp_sum_fixed(acc[q]);
           if (lane == 0 && r0 + q < n) w[r0 + q] = s;
         }
       }
     } else {
-      for (int r = warp; r < n; r += kThreads / 32) {
+      for (int r = warp; r < n; r += kRT / 32) {
         const float* row = A + (int64_t)r * a.lda;
         double acc = 0.0;
 #pragma unroll 4
@@ -168,14 +173,14 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
     }
     __syncthreads();
     double pl = 0.0, pw = 0.0;
-    for (int i = threadIdx.x; i < n; i += kThreads) {
+    for (int i = threadIdx.x; i < n; i += kRT) {
       pl = fma(v[i], w[i], pl);
       pw = fma(w[i], w[i], pw);
     }
     lam = block_sum(pl, red);
     double nw = sqrt(block_sum(pw, red));
     if (!(nw != 0.0)) break;  // also stops on NaN (lam is then NaN)
-    for (int i = threadIdx.x; i < n; i += kThreads) v[i] = w[i] / nw;
+    for (int i = threadIdx.x; i < n; i += kRT) v[i] = w[i] / nw;
     __syncthreads();
   }
   __syncthreads();
@@ -197,7 +202,7 @@ SHP_DEV bool lam_ok(double lam) { return isfinite(lam) && lam > 0.0; }
 enum { EPI_STORE = 0, EPI_MUPDATE = 1 };
 
 template <int MODE>
-SHP_DEV void epilogue(const RootArgs& a, const Acc& acc, int mat, int ti, int tj, double* dst, double* tdst,
+SHP_DEV void epilogue(const RootArgs& a, const AccN& acc, int mat, int ti, int tj, double* dst, double* tdst,
                       double* err_slot) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = a.np, n = a.n;
@@ -206,11 +211,11 @@ SHP_DEV void epilogue(const RootArgs& a, const Acc& acc, int mat, int ti, int tj
   const double pp1 = (double)(a.p + 1);
   double emax = 0.0;
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const int i = ti * kTileM + acc_row(warp, lane, mt);
+  for (int mt = 0; mt < 4; ++mt) {
+    const int i = ti * kNT + accn_row(warp, lane, mt);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
-      const int j = tj * kTileM + acc_col(warp, lane, nt, 0);
+      const int j = tj * kNT + accn_col(warp, lane, nt, 0);
       const double c0 = acc.c[mt][nt][0], c1 = acc.c[mt][nt][1];
       *reinterpret_cast<double2*>(dst + (int64_t)i * np + j) = make_double2(c0, c1);
       if (mirror) {
@@ -242,9 +247,9 @@ SHP_DEV void epilogue(const RootArgs& a, const Acc& acc, int mat, int ti, int tj
 // Ordered compaction of the active list: keep act[pos] iff the matrix may
 // continue at check k.  Every CTA computes the same result from global state.
 SHP_DEV int compact(const RootArgs& a, int* act, int nact, int k, int* cnt, bool first) {
-  const int per = (nact + kThreads - 1) / kThreads;
+  const int per = (nact + kRT - 1) / kRT;
   const int b0 = threadIdx.x * per;
-  int mine[kMaxBatchPerLaunch / kThreads];
+  int mine[kMaxBatchPerLaunch / kRT];
   int nm = 0;
   for (int q = 0; q < per; ++q) {
     const int pos = b0 + q;
@@ -258,32 +263,32 @@ SHP_DEV int compact(const RootArgs& a, int* act, int nact, int k, int* cnt, bool
   __syncthreads();
   if (threadIdx.x == 0) {
     int s = 0;
-    for (int i = 0; i < kThreads; ++i) {
+    for (int i = 0; i < kRT; ++i) {
       const int c = cnt[i];
       cnt[i] = s;
       s += c;
     }
-    cnt[kThreads] = s;
+    cnt[kRT] = s;
   }
   __syncthreads();
   const int out = cnt[threadIdx.x];
   for (int q = 0; q < nm; ++q) act[out + q] = mine[q];
-  const int total = cnt[kThreads];
+  const int total = cnt[kRT];
   __syncthreads();
   return total;
 }
 
 // ---------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
+__global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
   extern __shared__ __align__(16) double smem[];
   cg::grid_group grid = cg::this_grid();
-  const int np = a.np, T = np / kTileM, tiles = T * (T + 1) / 2;
+  const int np = a.np, T = np / kNT, tiles = T * (T + 1) / 2;
   const int64_t np2 = (int64_t)np * np;
 
   // ---- phase 0: power iteration (one CTA per matrix) + err history reset
   for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
     double* e = a.errh + (int64_t)mat * (a.max_iter + 1);
-    for (int k = threadIdx.x; k <= a.max_iter; k += kThreads) e[k] = 0.0;
+    for (int k = threadIdx.x; k <= a.max_iter; k += kRT) e[k] = 0.0;
     double lam = power_iteration(a, mat, smem);
     if (threadIdx.x == 0) a.lam[mat] = lam;
   }
@@ -291,8 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
 
   // ---- phase 1: setup M_0, T_0, X_0 and err_0 (one warp per padded row)
   {
-    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-    const int nw = gridDim.x * (kThreads / 32);
+    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kRT / 32) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (kRT / 32);
     const int64_t rows = (int64_t)a.batch * np;
     for (int64_t rid = gw; rid < rows; rid += nw) {
       const int mat = (int)(rid / np), i = (int)(rid - (int64_t)mat * np);
@@ -331,11 +336,11 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
   int* cnt = act + kMaxBatchPerLaunch;  // 257 ints scratch
   __shared__ int s_nact;
   // initial active list: lam ok and decide(k=0) == continue
-  for (int i = threadIdx.x; i < a.batch; i += kThreads) act[i] = i;
+  for (int i = threadIdx.x; i < a.batch; i += kRT) act[i] = i;
   __syncthreads();
   s_nact = compact(a, act, a.batch, 0, cnt, /*first=*/true);
   int nact = s_nact;
-  Acc acc;
+  AccN acc;
   for (int k = 0; nact > 0; ++k) {
     const int xs = k & 1;  // X_k in BX0 + xs, M_k in BM0 + xs
     const int tb = (a.p == 1) ? ((k & 1) ? BS0 : BT) : BT;
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         upper_tile(t, T, ti, tj);
         const double* Aop = (job == 0) ? buf(a, mat, BX0 + xs) : buf(a, mat, tb);
         const double* Bop = buf(a, mat, tb);
-        gemm_tile_f64(acc, Aop + (int64_t)ti * kTileM * np, Bop + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
+        gemm_tile_f64(acc, Aop + (int64_t)ti * kNT * np, Bop + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
         double* dst = (job == 0) ? buf(a, mat, BX0 + (xs ^ 1)) : buf(a, mat, BS0);
         epilogue<EPI_STORE>(a, acc, mat, ti, tj, dst, nullptr, nullptr);
       }
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         int ti, tj;
         upper_tile(t, T, ti, tj);
         const double* S = buf(a, mat, src);
-        gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
+        gemm_tile_f64(acc, S + (int64_t)ti * kNT * np, S + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
         epilogue<EPI_STORE>(a, acc, mat, ti, tj, buf(a, mat, dstb), nullptr, nullptr);
       }
       grid.sync();
@@ -382,8 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
         const int mat = act[pos];
         int ti, tj;
         upper_tile(t, T, ti, tj);
-        gemm_tile_f64(acc, buf(a, mat, tp) + (int64_t)ti * kTileM * np,
-                      buf(a, mat, BM0 + xs) + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
+        gemm_tile_f64(acc, buf(a, mat, tp) + (int64_t)ti * kNT * np,
+                      buf(a, mat, BM0 + xs) + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
         epilogue<EPI_MUPDATE>(a, acc, mat, ti, tj, buf(a, mat, BM0 + (xs ^ 1)), buf(a, mat, tb_next),
                               a.errh + (int64_t)mat * (a.max_iter + 1) + (k + 1));
       }
@@ -427,8 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
   }
   grid.sync();
   {
-    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-    const int nw = gridDim.x * (kThreads / 32);
+    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kRT / 32) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (kRT / 32);
     const int64_t rows = (int64_t)a.batch * a.n;
     for (int64_t rid = gw; rid < rows; rid += nw) {
       const int mat = (int)(rid / a.n), i = (int)(rid - (int64_t)mat * a.n);
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) root_kernel(RootArgs a) {
 // ---------------------------------------------------------------- host side
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static int padded(int n) { return (n + kTileM - 1) / kTileM * kTileM; }
+static int padded(int n) { return (n + kNT - 1) / kNT * kNT; }
 
 size_t root_workspace_bytes(int batch, int n, int max_iter) {
   const size_t np = (size_t)padded(n);
@@ -456,7 +461,7 @@ size_t root_workspace_bytes(int batch, int n, int max_iter) {
 }
 
 size_t root_smem_bytes(int n) {
-  size_t gemm = (size_t)kAsyncSmemDoubles * sizeof(double) + (kMaxBatchPerLaunch + kThreads + 1) * sizeof(int);
+  size_t gemm = (size_t)kAsyncSmemDoubles * sizeof(double) + (kMaxBatchPerLaunch + kRT + 1) * sizeof(int);
   size_t pi = (2 * (size_t)n + 8) * sizeof(double);
   return gemm > pi ? gemm : pi;
 }
@@ -472,7 +477,7 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     configured_smem = smem;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, root_kernel, kThreads, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, root_kernel, kRT, smem) != cudaSuccess || per_sm < 1)
     return set_error(SHAMPOO_ERR_UNSUPPORTED, "root_kernel cannot be resident (smem %zu)", smem);
   const int np = padded(n);
   char* w = static_cast<char*>(ws);
@@ -506,7 +511,7 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     a.res = reinterpret_cast<int4*>(q);
     void* args[] = {&a};
     const int grid = num_sms() * per_sm;
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kThreads), args, smem, stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);
     if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_kernel)", e);
     ++*launches;
   }
@@ -536,12 +541,12 @@ SHP_DEV double* rbuf(const ResArgs& a, int mat, int b) {
   return a.bufs + ((int64_t)mat * kResBufs + b) * (int64_t)a.np * a.np;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
+__global__ void __launch_bounds__(kRT, 2) residual_kernel(ResArgs a) {
   extern __shared__ __align__(16) double smem[];
   cg::grid_group grid = cg::this_grid();
-  const int np = a.np, n = a.n, T = np / kTileM, tiles = T * (T + 1) / 2;
+  const int np = a.np, n = a.n, T = np / kNT, tiles = T * (T + 1) / 2;
   const int64_t np2 = (int64_t)np * np, total = (int64_t)a.batch * np2;
-  for (int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kThreads) {
+  for (int64_t idx = (int64_t)blockIdx.x * kRT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kRT) {
     const int mat = (int)(idx / np2);
     const int64_t rem = idx - (int64_t)mat * np2;
     const int i = (int)(rem / np), j = (int)(rem - (int64_t)i * np);
@@ -558,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
   }
   grid.sync();
   int src = 0;
-  Acc acc;
+  AccN acc;
   for (int q = a.p; q > 1; q >>= 1) {
     const int dst = (src == 1) ? 2 : 1;
     for (int it = blockIdx.x; it < a.batch * tiles; it += gridDim.x) {
@@ -566,15 +571,15 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
       int ti, tj;
       upper_tile(t, T, ti, tj);
       const double* S = rbuf(a, mat, src);
-      gemm_tile_f64(acc, S + (int64_t)ti * kTileM * np, S + (int64_t)tj * kTileM * np, np, np / kAsyncK, smem);
+      gemm_tile_f64(acc, S + (int64_t)ti * kNT * np, S + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       double* D = rbuf(a, mat, dst);
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        const int i = ti * kTileM + acc_row(warp, lane, mt);
+      for (int mt = 0; mt < 4; ++mt) {
+        const int i = ti * kNT + accn_row(warp, lane, mt);
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-          const int j = tj * kTileM + acc_col(warp, lane, nt, 0);
+          const int j = tj * kNT + accn_col(warp, lane, nt, 0);
           *reinterpret_cast<double2*>(D + (int64_t)i * np + j) = make_double2(acc.c[mt][nt][0], acc.c[mt][nt][1]);
           if (ti != tj) {
             D[(int64_t)j * np + i] = acc.c[mt][nt][0];
@@ -586,22 +591,22 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
     grid.sync();
     src = dst;
   }
-  __shared__ double red[kThreads / 32];
+  __shared__ double red[kRT / 32];
   for (int it = blockIdx.x; it < a.batch * T * T; it += gridDim.x) {
     const int mat = it / (T * T), t = it - mat * T * T;
     const int ti = t / T, tj = t - ti * T;
-    gemm_tile_f64(acc, rbuf(a, mat, src) + (int64_t)ti * kTileM * np, rbuf(a, mat, 3) + (int64_t)tj * kTileM * np,
+    gemm_tile_f64(acc, rbuf(a, mat, src) + (int64_t)ti * kNT * np, rbuf(a, mat, 3) + (int64_t)tj * kNT * np,
                   np, np / kAsyncK, smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double s = 0.0;
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int i = ti * kTileM + acc_row(warp, lane, mt);
+    for (int mt = 0; mt < 4; ++mt) {
+      const int i = ti * kNT + accn_row(warp, lane, mt);
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int j = tj * kTileM + acc_col(warp, lane, nt, e);
+          const int j = tj * kNT + accn_col(warp, lane, nt, e);
           if (i < n && j < n) {
             const double d = acc.c[mt][nt][e] - ((i == j) ? 1.0 : 0.0);
             s = fma(d, d, s);
@@ -613,13 +618,13 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       double t2 = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) t2 = __dadd_rn(t2, red[w]);
+      for (int w = 0; w < kRT / 32; ++w) t2 = __dadd_rn(t2, red[w]);
       a.part[(int64_t)mat * T * T + t] = t2;
     }
     __syncthreads();
   }
   grid.sync();
-  for (int mat = blockIdx.x * kThreads + threadIdx.x; mat < a.batch; mat += gridDim.x * kThreads) {
+  for (int mat = blockIdx.x * kRT + threadIdx.x; mat < a.batch; mat += gridDim.x * kRT) {
     double s = 0.0;
     for (int t = 0; t < T * T; ++t) s = __dadd_rn(s, a.part[(int64_t)mat * T * T + t]);
     a.out[mat] = sqrt(s);
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) residual_kernel(ResArgs a) {
 }
 
 size_t residual_workspace_bytes(int batch, int n) {
-  const size_t np = (size_t)padded(n), T = np / kTileM;
+  const size_t np = (size_t)padded(n), T = np / kNT;
   return align256((size_t)batch * kResBufs * np * np * sizeof(double)) + align256((size_t)batch * T * T * sizeof(double));
 }
 
@@ -642,7 +647,7 @@ int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* 
     configured = true;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, residual_kernel, kThreads, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, residual_kernel, kRT, smem) != cudaSuccess || per_sm < 1)
     return set_error(SHAMPOO_ERR_UNSUPPORTED, "residual_kernel cannot be resident");
   ResArgs a;
   a.A = A;
@@ -664,7 +669,7 @@ int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* 
   q += align256((size_t)batch * kResBufs * np * np * sizeof(double));
   a.part = reinterpret_cast<double*>(q);
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)residual_kernel, dim3(num_sms() * per_sm), dim3(kThreads),
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)residual_kernel, dim3(num_sms() * per_sm), dim3(kRT),
                                               args, smem, stream);
   if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(residual_kernel)", e);
   ++*launches;
