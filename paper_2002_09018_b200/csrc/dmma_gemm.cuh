@@ -271,6 +271,71 @@ SHP_DEV void gemm_tile_f64(AccN& acc, const double* A, const double* B, int64_t 
   __syncthreads();
 }
 
+// fp32 panel for the compact (64-row, 32-deep) tiles, register-staged and
+// widened to fp64 on the way into shared memory; bounds-masked (zero fill).
+// kmaj == 0: A_m[k] = src[m][k] (row panel); kmaj == 1: A_m[k] = src[k][m].
+struct F32PanelN {
+  const float* base;
+  int64_t ld;
+  int kmaj;
+  int m0, m_valid, k_valid;
+  using Regs = float[16];
+  SHP_DEV void load(int kt, Regs& r) const {
+    const int t = threadIdx.x;
+    if (!kmaj) {
+      // thread -> (row = t >> 1, 16 consecutive k at 16*(t & 1)): a warp reads 16 rows x 64 B
+      const int m = m0 + (t >> 1), kb = kt * kAsyncK + 16 * (t & 1);
+      const float* src = base + (int64_t)m * ld + kb;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) r[e] = (m < m_valid && kb + e < k_valid) ? __ldg(src + e) : 0.0f;
+    } else {
+      // thread -> (m = t & 63, 16 consecutive k at 16*(t >> 6)): per k, 64 consecutive m
+      const int m = m0 + (t & 63), kb = kt * kAsyncK + 16 * (t >> 6);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) r[e] = (m < m_valid && kb + e < k_valid) ? __ldg(base + (int64_t)(kb + e) * ld + m) : 0.0f;
+    }
+  }
+  SHP_DEV void store(double* s, const Regs& r) const {
+    const int t = threadIdx.x;
+    const int row = kmaj ? (t & 63) : (t >> 1);
+    const int cb = kmaj ? 8 * (t >> 6) : 8 * (t & 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<double2*>(s + row * kAsyncK + (((cb + j) ^ swx(row)) << 1)) =
+          make_double2((double)r[2 * j], (double)r[2 * j + 1]);
+  }
+};
+
+// 64x64 tile over K = 32 * k_tiles from two fp32 panels (2-stage register-staged
+// double buffer: global loads of k tile t+1 are in flight during the DMMAs of t).
+// `smem` holds 2 * 2 * kAsyncTile doubles (64 KB).  Ends with __syncthreads.
+SHP_DEV void gemm_tile_f32n(AccN& acc, const F32PanelN& la, const F32PanelN& lb, int k_tiles, double* smem) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  F32PanelN::Regs ra, rb;
+  accn_zero(acc);
+  la.load(0, ra);
+  lb.load(0, rb);
+  la.store(smem, ra);
+  lb.store(smem + kAsyncTile, rb);
+  __syncthreads();
+  for (int kt = 0; kt < k_tiles; ++kt) {
+    const int s = kt & 1;
+    const bool more = kt + 1 < k_tiles;
+    if (more) {
+      la.load(kt + 1, ra);
+      lb.load(kt + 1, rb);
+    }
+    const double* cur = smem + s * (2 * kAsyncTile);
+    mma_ktilen(acc, cur, cur + kAsyncTile, warp, lane);
+    if (more) {
+      double* nxt = smem + (s ^ 1) * (2 * kAsyncTile);
+      la.store(nxt, ra);
+      lb.store(nxt + kAsyncTile, rb);
+    }
+    __syncthreads();
+  }
+}
+
 // Upper-triangular tile index t -> (ti, tj), ti <= tj, row-major over the
 // upper triangle of a T x T tile grid.
 SHP_DEV void upper_tile(int t, int T, int& ti, int& tj) {

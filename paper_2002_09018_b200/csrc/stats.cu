@@ -11,12 +11,16 @@
 //   memset(flags) -> check (non-finite G per block) -> prep (tile prefix sums)
 //   -> stats (persistent DMMA tiles, L and R, owned blocks only)
 //   -> diag (D update + per-chunk graft partials) -> finish (fixed-order sums)
+#include <algorithm>
+
 #include "dmma_gemm.cuh"
 #include "internal.h"
 
 namespace shp {
 
 constexpr int kChunks = 64;  // row chunks per block for the elementwise passes
+constexpr int kPrefixSmem = 4096;  // prefix entries cached in shared memory (32 KB)
+constexpr int kStatsGemmBytes = 4 * kAsyncTile * 8;  // 2 stages x (A, B) fp64 tiles, 64 KB
 
 struct StatsWs {
   int* flag;         // n_blocks (non-finite marker)
@@ -42,7 +46,7 @@ static StatsWs carve(void* ws, int n_blocks) {
   return w;
 }
 
-SHP_DEV int tiles_of(int n) { return (n + kTileM - 1) / kTileM; }
+SHP_DEV int tiles_of(int n) { return (n + kNT - 1) / kNT; }  // 64x64 output tiles
 SHP_DEV int64_t upper_count(int n) {
   const int64_t T = tiles_of(n);
   return T * (T + 1) / 2;
@@ -112,18 +116,27 @@ SHP_DEV int find_block(const int64_t* prefix, int n_blocks, int64_t item) {
 }
 
 // ------------------------------------------------------------ statistics
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kNThreads, 2)
     stats_kernel(const shampoo_tensor_t* tensors, const shampoo_block_t* blocks, int n_blocks, int only_owner,
                  float* stats, double decay, double weight, const int* flag, const int64_t* prefix) {
   extern __shared__ __align__(16) double smem[];
   const int64_t total = prefix[n_blocks];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Acc acc;
+  // tile -> block lookups binary-search the prefix array; keep it in shared
+  // memory (after the GEMM buffers) when it fits, instead of 9 dependent
+  // global loads at every tile start
+  int64_t* spre = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(smem) + kStatsGemmBytes);
+  const bool pre_in_smem = n_blocks + 1 <= kPrefixSmem;
+  if (pre_in_smem)
+    for (int i = threadIdx.x; i <= n_blocks; i += kNThreads) spre[i] = prefix[i];
+  __syncthreads();
+  const int64_t* pre = pre_in_smem ? spre : prefix;
+  AccN acc;
   for (int64_t item = blockIdx.x; item < total; item += gridDim.x) {
-    const int b = find_block(prefix, n_blocks, item);
+    const int b = find_block(pre, n_blocks, item);
     const shampoo_block_t blk = blocks[b];
     if (flag[b]) continue;  // uniform across the CTA
-    int64_t local = item - prefix[b];
+    int64_t local = item - pre[b];
     const bool has_l = blk.p_left && (only_owner < 0 || blk.owner_left == only_owner);
     int side = 1;
     if (has_l) {
@@ -137,22 +150,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     upper_tile((int)local, tiles_of(nvalid), ti, tj);
     const shampoo_tensor_t ten = tensors[blk.tensor_id];
     const float* gb = ten.G + blk.row0 * ten.ldg + blk.col0;
-    F32Panel la{gb, ten.ldg, side, ti * kTileM, nvalid, K};
-    F32Panel lb{gb, ten.ldg, side, tj * kTileM, nvalid, K};
-    gemm_tile(acc, la, lb, (K + kTileK - 1) / kTileK, smem);
-    // epilogue: EMA with the fixed rounding sequence, upper triangle + mirror
+    F32PanelN la{gb, ten.ldg, side, ti * kNT, nvalid, K};
+    F32PanelN lb{gb, ten.ldg, side, tj * kNT, nvalid, K};
+    // the old statistic values of this thread's outputs, loaded before the k loop
+    // so their latency hides behind the DMMAs
     float* S = stats + (side == 0 ? blk.left_off : blk.right_off);
     const int64_t ld = side == 0 ? blk.left_ld : blk.right_ld;
+    float oldv[4][4][2];
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int i = ti * kTileM + acc_row(warp, lane, mt);
+    for (int mt = 0; mt < 4; ++mt) {
+      const int i = ti * kNT + accn_row(warp, lane, mt);
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int j = tj * kTileM + acc_col(warp, lane, nt, e);
+          const int j = tj * kNT + accn_col(warp, lane, nt, e);
+          oldv[mt][nt][e] = (i < nvalid && j < nvalid && i <= j) ? S[(int64_t)i * ld + j] : 0.0f;
+        }
+    }
+    gemm_tile_f32n(acc, la, lb, (K + kAsyncK - 1) / kAsyncK, smem);
+    // epilogue: EMA with the fixed rounding sequence, upper triangle + mirror
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int i = ti * kNT + accn_row(warp, lane, mt);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = tj * kNT + accn_col(warp, lane, nt, e);
           if (i < nvalid && j < nvalid && i <= j) {
-            const double old = (double)S[(int64_t)i * ld + j];
+            const double old = (double)oldv[mt][nt][e];
             const double t1 = __dmul_rn(weight, acc.c[mt][nt][e]);
             const double t2 = __dmul_rn(decay, old);
             const float r = __double2float_rn(__dadd_rn(t1, t2));
@@ -217,9 +244,10 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
   if (n_blocks == 0) return SHAMPOO_OK;
   StatsWs w = carve(ws, n_blocks);
   static bool configured = false;
-  const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
+  const size_t smem_max = (size_t)kStatsGemmBytes + (size_t)kPrefixSmem * sizeof(int64_t);
+  const size_t smem = (size_t)kStatsGemmBytes + (size_t)std::min(n_blocks + 1, kPrefixSmem) * sizeof(int64_t);
   if (!configured) {
-    if (cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max) != cudaSuccess)
       return set_cuda_error("cudaFuncSetAttribute(stats_kernel)");
     configured = true;
   }
@@ -228,7 +256,7 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
   const unsigned eg = (unsigned)n_blocks * kChunks;
   check_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.flag);
   prep_kernel<<<1, 1024, 0, stream>>>(blocks, n_blocks, only_owner, w.prefix);
-  stats_kernel<<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, only_owner, stats, decay, weight,
+  stats_kernel<<<2 * num_sms(), kNThreads, smem, stream>>>(tensors, blocks, n_blocks, only_owner, stats, decay, weight,
                                                       w.flag, w.prefix);
   diag_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.flag, w.part);
   finish_kernel<<<(n_blocks + 255) / 256, 256, 0, stream>>>(n_blocks, w.flag, w.part, graft_num, block_status);
