@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tol", type=float, default=1e-7)
+    ap.add_argument("--block-size", type=int, default=BLOCK,
+                    help="config 5 sweep (128..4096); the metric is quoted at 1024")
+    ap.add_argument("--max-precond-dim", type=int, default=MAX_PRECOND)
     return ap.parse_args()
 
 
@@ -174,7 +177,8 @@ def main():
 
     names_shapes = synth.transformer_big_shapes()
     shapes = [s for _, s in names_shapes]
-    plan = shp.make_plan(shapes, BLOCK, MAX_PRECOND, world)
+    B = args.block_size
+    plan = shp.make_plan(shapes, B, args.max_precond_dim, world)
     n_p4 = int(sum((plan.blocks["p_left"] == 4).sum() + (plan.blocks["p_right"] == 4).sum() for _ in [0]))
     # gradients (device), vocab tensors row-sparse (Zipf ids), others low-rank + noise
     Gs = []
@@ -253,7 +257,7 @@ def main():
     ms_per_step = total_ms / args.steps
 
     # dominant kernel: the p=4 root launch (one cooperative kernel per call), timed alone on the stream
-    g4 = [g for g in plan.groups_of(rank) if int(g["p"]) == 4 and int(g["n"]) == BLOCK]
+    g4 = sorted([g for g in plan.groups_of(rank) if int(g["p"]) == 4], key=lambda g: -int(g["count"]) * int(g["n"]) ** 3)
     roof = None
     iters_mean = None
     if g4:
@@ -263,22 +267,25 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        shp.inverse_pth_root_ptr(stats.data_ptr() + 4 * off, BLOCK, stride, roots.data_ptr() + 4 * off, BLOCK, stride,
-                                 cnt, BLOCK, 4, info, tol=args.tol, device=dev)
+        gn_ = int(g["n"])
+        gld = (gn_ + 3) // 4 * 4
+        shp.inverse_pth_root_ptr(stats.data_ptr() + 4 * off, gld, stride, roots.data_ptr() + 4 * off, gld, stride,
+                                 cnt, gn_, 4, info, tol=args.tol, device=dev)
         e1.record(stream)
         torch.cuda.synchronize()
         kms = e0.elapsed_time(e1)
         inf = shp.info_to_numpy(info)
         iters_mean = float(inf["iters"].mean())
-        n = BLOCK
+        n = gn_
         # algorithmic flops: 4 symmetric products per iteration, n^2 (n+1) flops each (upper triangle
         # incl. diagonal x 2n), + the power iteration (100 x 2 n^2)
         flops = float(inf["iters"].sum()) * 4 * n * n * (n + 1) + cnt * 100 * 2.0 * n * n
         achieved = flops / (kms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": ROOT_TRAFFIC_BYTES_PER_MATRIX * cnt,
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+                "traffic": ROOT_TRAFFIC_BYTES_PER_MATRIX * cnt if n == 1024 else None,
                 "traffic_note": "bytes per launch, ncu capture of the same kernel (148 matrices) scaled per matrix",
-                "kernel": f"root_kernel (FP64 DMMA coupled Newton, batch {cnt} x 1024^2, p=4)",
+                "kernel": f"root_kernel (FP64 DMMA coupled Newton, batch {cnt} x {n}^2, p=4)",
                 "kernel_ms": kms, "flops_per_launch": flops,
                 "peak_source": "FP64 DMMA.8x8x4 peak measured on this pool's B200 by tools/microbench/fp64_pipes.cu "
                                "(MEASURED_PEAKS.json has no FP64 entry)"}
@@ -327,8 +334,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "transformer_big_b1024_full_step", "model": "Transformer-Big (P:494) shapes",
-                       "block_size": BLOCK, "max_precond_dim": MAX_PRECOND, "blocks": nb,
+            "config": {"workload": f"transformer_big_b{B}_full_step", "model": "Transformer-Big (P:494) shapes",
+                       "block_size": B, "max_precond_dim": args.max_precond_dim, "blocks": nb,
                        "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
                        "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
                        "parallelism": f"root-shard{world}", "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
