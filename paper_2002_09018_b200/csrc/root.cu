@@ -49,6 +49,7 @@ struct RootArgs {
   double* lam;   // batch
   double* errh;  // batch * (max_iter + 1)
   int4* res;     // batch: {result buffer, iters, status, -}
+  double* wpi;   // 2 * batch * n: power-iteration w vectors (split mode, ping-pong)
 };
 
 SHP_DEV double* buf(const RootArgs& a, int mat, int b) {
@@ -92,6 +93,104 @@ SHP_DEV double block_sum(double v, double* red) {
   return s;
 }
 
+// ---- power-iteration pieces.  Every w[r] is one warp's fixed-lane-order dot
+// product and every scalar reduction runs the same 128-thread block_sum over
+// the full vectors, so lambda_hat is bit-identical whether one CTA or several
+// CTAs compute a matrix's rows (batch-size independent results).
+SHP_DEV void pi_init(double* v, int n, double* red) {
+  double part = 0.0;
+  for (int i = threadIdx.x; i < n; i += kRT) {
+    const double x = (double)(splitmix64((uint64_t)i) >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    v[i] = x;
+    part = fma(x, x, part);
+  }
+  const double nv = sqrt(block_sum(part, red));
+  for (int i = threadIdx.x; i < n; i += kRT) v[i] = v[i] / nv;
+  __syncthreads();
+}
+
+// w[r] = sum_c A[r][c] v[c] for r in [r0, r1)
+SHP_DEV void pi_rows(const RootArgs& a, const float* A, const double* v, double* w, int r0, int r1) {
+  const int n = a.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool vec4 = ((a.lda & 3) == 0) && ((n & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  if (vec4) {
+    // kPR rows per warp pass x 4 column chunks (128 floats each) per row: 4*kPR
+    // float4 loads in flight per lane; each lane accumulates its columns in
+    // ascending order.
+    constexpr int kPR = 8;
+    for (int rb = r0 + warp * kPR; rb < r1; rb += kPR * (kRT / 32)) {
+      double acc[kPR];
+      const float* rows[kPR];
+#pragma unroll
+      for (int q = 0; q < kPR; ++q) {
+        acc[q] = 0.0;
+        rows[q] = A + (int64_t)min(rb + q, r1 - 1) * a.lda;
+      }
+      int c = 4 * lane;
+      for (; c + 3 * 128 < n; c += 4 * 128) {
+        float4 f[kPR][4];
+#pragma unroll
+        for (int q = 0; q < kPR; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) f[q][u] = __ldg(reinterpret_cast<const float4*>(rows[q] + c + u * 128));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = c + u * 128;
+          const double v0 = v[cc], v1 = v[cc + 1], v2 = v[cc + 2], v3 = v[cc + 3];
+#pragma unroll
+          for (int q = 0; q < kPR; ++q) {
+            acc[q] = fma((double)f[q][u].x, v0, acc[q]);
+            acc[q] = fma((double)f[q][u].y, v1, acc[q]);
+            acc[q] = fma((double)f[q][u].z, v2, acc[q]);
+            acc[q] = fma((double)f[q][u].w, v3, acc[q]);
+          }
+        }
+      }
+      for (; c < n; c += 128) {
+#pragma unroll
+        for (int q = 0; q < kPR; ++q) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(rows[q] + c));
+          acc[q] = fma((double)f.x, v[c], acc[q]);
+          acc[q] = fma((double)f.y, v[c + 1], acc[q]);
+          acc[q] = fma((double)f.z, v[c + 2], acc[q]);
+          acc[q] = fma((double)f.w, v[c + 3], acc[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kPR; ++q) {
+        const double sum = warp_sum_fixed(acc[q]);
+        if (lane == 0 && rb + q < r1) w[rb + q] = sum;
+      }
+    }
+  } else {
+    for (int r = r0 + warp; r < r1; r += kRT / 32) {
+      const float* row = A + (int64_t)r * a.lda;
+      double acc = 0.0;
+#pragma unroll 4
+      for (int c = lane; c < n; c += 32) acc = fma((double)__ldg(row + c), v[c], acc);
+      acc = warp_sum_fixed(acc);
+      if (lane == 0) w[r] = acc;
+    }
+  }
+}
+
+// lam = v.w, nw = |w|; v <- w/nw unless nw == 0 (or NaN-free zero).  Returns false
+// when the iteration must stop (|w| == 0), as the oracle's `break`.
+SHP_DEV bool pi_update(double* v, const double* w, int n, double* red, double& lam) {
+  double pl = 0.0, pw = 0.0;
+  for (int i = threadIdx.x; i < n; i += kRT) {
+    pl = fma(v[i], w[i], pl);
+    pw = fma(w[i], w[i], pw);
+  }
+  lam = block_sum(pl, red);
+  const double nw = sqrt(block_sum(pw, red));
+  if (!(nw != 0.0)) return false;  // also stops on NaN (lam is then NaN)
+  for (int i = threadIdx.x; i < n; i += kRT) v[i] = w[i] / nw;
+  __syncthreads();
+  return true;
+}
+
 // One CTA: lambda_hat of matrix `mat` (smem: v[n], w[n], red[8]).
 SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
   const int n = a.n;
@@ -99,92 +198,44 @@ SHP_DEV double power_iteration(const RootArgs& a, int mat, double* smem) {
   double* w = smem + n;
   double* red = smem + 2 * n;
   const float* A = a.A + (int64_t)mat * a.stride_a;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double part = 0.0;
-  for (int i = threadIdx.x; i < n; i += kRT) {
-    double x = (double)(splitmix64((uint64_t)i) >> 11) * 0x1.0p-53 * 2.0 - 1.0;
-    v[i] = x;
-    part = fma(x, x, part);
-  }
-  double nv = sqrt(block_sum(part, red));
-  for (int i = threadIdx.x; i < n; i += kRT) v[i] = v[i] / nv;
-  __syncthreads();
+  pi_init(v, n, red);
   double lam = 0.0;
-  const bool vec4 = ((a.lda & 3) == 0) && ((n & 3) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   for (int it = 0; it < a.power_iters; ++it) {
-    if (vec4) {
-      // kPR rows per warp pass x 4 column chunks (128 floats each) per row:
-      // 4*kPR float4 loads in flight per lane.  Each lane accumulates its columns in
-      // ascending order, so the reduction order is fixed (deterministic).
-      constexpr int kPR = 8;
-      for (int r0 = warp * kPR; r0 < n; r0 += kPR * (kRT / 32)) {
-        double acc[kPR];
-        const float* rows[kPR];
-#pragma unroll
-        for (int q = 0; q < kPR; ++q) {
-          acc[q] = 0.0;
-          rows[q] = A + (int64_t)min(r0 + q, n - 1) * a.lda;
-        }
-        int c = 4 * lane;
-        for (; c + 3 * 128 < n; c += 4 * 128) {
-          float4 f[kPR][4];
-#pragma unroll
-          for (int q = 0; q < kPR; ++q)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) f[q][u] = __ldg(reinterpret_cast<const float4*>(rows[q] + c + u * 128));
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int cc = c + u * 128;
-            const double v0 = v[cc], v1 = v[cc + 1], v2 = v[cc + 2], v3 = v[cc + 3];
-#pragma unroll
-            for (int q = 0; q < kPR; ++q) {
-              acc[q] = fma((double)f[q][u].x, v0, acc[q]);
-              acc[q] = fma((double)f[q][u].y, v1, acc[q]);
-              acc[q] = fma((double)f[q][u].z, v2, acc[q]);
-              acc[q] = fma((double)f[q][u].w, v3, acc[q]);
-            }
-          }
-        }
-        for (; c < n; c += 128) {
-#pragma unroll
-          for (int q = 0; q < kPR; ++q) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(rows[q] + c));
-            acc[q] = fma((double)f.x, v[c], acc[q]);
-            acc[q] = fma((double)f.y, v[c + 1], acc[q]);
-            acc[q] = fma((double)f.z, v[c + 2], acc[q]);
-            acc[q] = fma((double)f.w, v[c + 3], acc[q]);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < kPR; ++q) {
-          const double s = warp_sum_fixed(acc[q]);
-          if (lane == 0 && r0 + q < n) w[r0 + q] = s;
-        }
-      }
-    } else {
-      for (int r = warp; r < n; r += kRT / 32) {
-        const float* row = A + (int64_t)r * a.lda;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int c = lane; c < n; c += 32) acc = fma((double)__ldg(row + c), v[c], acc);
-        acc = warp_sum_fixed(acc);
-        if (lane == 0) w[r] = acc;
-      }
-    }
+    pi_rows(a, A, v, w, 0, n);
     __syncthreads();
-    double pl = 0.0, pw = 0.0;
-    for (int i = threadIdx.x; i < n; i += kRT) {
-      pl = fma(v[i], w[i], pl);
-      pw = fma(w[i], w[i], pw);
-    }
-    lam = block_sum(pl, red);
-    double nw = sqrt(block_sum(pw, red));
-    if (!(nw != 0.0)) break;  // also stops on NaN (lam is then NaN)
-    for (int i = threadIdx.x; i < n; i += kRT) v[i] = w[i] / nw;
-    __syncthreads();
+    if (!pi_update(v, w, n, red, lam)) break;
   }
   __syncthreads();
   return lam;
+}
+
+// Split mode (batch < grid): `k` CTAs share each matrix's rows; w goes through
+// global memory (ping-pong) with one grid.sync per power step; every CTA of a
+// matrix then runs the same pi_update on the full vectors.
+SHP_DEV void power_iteration_split(const RootArgs& a, double* smem, cg::grid_group& grid) {
+  const int n = a.n, k = gridDim.x / a.batch;
+  const int mat = blockIdx.x / k, part = blockIdx.x % k;
+  const bool active = mat < a.batch;
+  double* v = smem;
+  double* w = smem + n;
+  double* red = smem + 2 * n;
+  const int rows_per = ((n + k - 1) / k + 7) / 8 * 8;
+  const int r0 = min(n, part * rows_per), r1 = min(n, r0 + rows_per);
+  const float* A = active ? a.A + (int64_t)mat * a.stride_a : nullptr;
+  if (active) pi_init(v, n, red);
+  double lam = 0.0;
+  bool running = true;
+  for (int it = 0; it < a.power_iters; ++it) {
+    double* wg = a.wpi + ((int64_t)(it & 1) * a.batch + (active ? mat : 0)) * n;
+    if (active && running) pi_rows(a, A, v, wg, r0, r1);
+    grid.sync();
+    if (active && running) {
+      for (int i = threadIdx.x; i < n; i += kRT) w[i] = wg[i];
+      __syncthreads();
+      running = pi_update(v, w, n, red, lam);
+    }
+  }
+  if (active && part == 0 && threadIdx.x == 0) a.lam[mat] = lam;
 }
 
 SHP_DEV double c_pow_neg_inv_p(double c, int p) {
@@ -285,12 +336,18 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
   const int np = a.np, T = np / kNT, tiles = T * (T + 1) / 2;
   const int64_t np2 = (int64_t)np * np;
 
-  // ---- phase 0: power iteration (one CTA per matrix) + err history reset
+  // ---- phase 0: power iteration + err history reset
   for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
     double* e = a.errh + (int64_t)mat * (a.max_iter + 1);
     for (int k = threadIdx.x; k <= a.max_iter; k += kRT) e[k] = 0.0;
-    double lam = power_iteration(a, mat, smem);
-    if (threadIdx.x == 0) a.lam[mat] = lam;
+  }
+  if (2 * a.batch <= (int)gridDim.x) {
+    power_iteration_split(a, smem, grid);  // small batch: several CTAs per matrix
+  } else {
+    for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
+      const double lam = power_iteration(a, mat, smem);
+      if (threadIdx.x == 0) a.lam[mat] = lam;
+    }
   }
   grid.sync();
 
@@ -457,7 +514,8 @@ static int padded(int n) { return (n + kNT - 1) / kNT * kNT; }
 size_t root_workspace_bytes(int batch, int n, int max_iter) {
   const size_t np = (size_t)padded(n);
   return align256((size_t)batch * kBufs * np * np * sizeof(double)) + align256((size_t)batch * sizeof(double)) +
-         align256((size_t)batch * (max_iter + 1) * sizeof(double)) + align256((size_t)batch * sizeof(int4));
+         align256((size_t)batch * (max_iter + 1) * sizeof(double)) + align256((size_t)batch * sizeof(int4)) +
+         align256((size_t)2 * batch * n * sizeof(double));
 }
 
 size_t root_smem_bytes(int n) {
@@ -509,6 +567,8 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     a.errh = reinterpret_cast<double*>(q);
     q += align256((size_t)bc * (max_iter + 1) * sizeof(double));
     a.res = reinterpret_cast<int4*>(q);
+    q += align256((size_t)bc * sizeof(int4));
+    a.wpi = reinterpret_cast<double*>(q);
     void* args[] = {&a};
     const int grid = num_sms() * per_sm;
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);

@@ -400,3 +400,14 @@ def test_precondition_determinism(shp):
     shp.precondition(shp.TensorTable([G], [torch.ones_like(G)], [P2]), pl, roots)
     torch.cuda.synchronize()
     assert torch.equal(P1, P2)
+
+
+def test_root_results_independent_of_batch_size(shp):
+    """A root must not depend on which other matrices share its launch: small
+    batches split each matrix's power iteration over several CTAs, large ones
+    use one CTA per matrix; both reduce in the same fixed order."""
+    As = synth.psd_batch(64, 200, 31, "mixed")
+    Xs, _ = shp.inverse_pth_root_batched(torch.from_numpy(As[:3]).to(DEV), 4)
+    Xl, _ = shp.inverse_pth_root_batched(torch.from_numpy(As).to(DEV), 4)
+    torch.cuda.synchronize()
+    assert torch.equal(Xs, Xl[:3])
