@@ -82,6 +82,15 @@ typedef struct {
   int64_t m, n;
 } shampoo_tensor_t;
 
+/* Optimizer state of one parameter tensor for the Alg. 1 tail (f2); an array of
+ * these, parallel to the shampoo_tensor_t array, lives in DEVICE memory. */
+typedef struct {
+  float* W;  /* parameters, updated in place                                 */
+  float* M;  /* momentum of the grafted diagonal direction D^{-1/2} o G       */
+  float* Pm; /* momentum of the preconditioned gradient                      */
+  int64_t ldw, ldm, ldpm;
+} shampoo_state_t;
+
 /* Per-matrix result of the root solver (device array). */
 typedef struct {
   int32_t iters;     /* coupled-Newton iterations performed                        */
@@ -191,6 +200,23 @@ size_t shampoo_precondition_workspace_bytes(const shampoo_tensor_t* tensors_host
 int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors, const shampoo_block_t* blocks_host,
                          int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
                          double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream);
+
+/* ----------------------------------------- f2: momentum, step size, update
+ * The tail of Algorithm 1, per block b (readings #9, #11):
+ *   M_t = beta1 M_{t-1} + (1-beta1) D_t^{-1/2} o G_t               (line 12)
+ *   shampoo_branch (t > tau):
+ *     Pm_t = beta1 Pm_{t-1} + (1-beta1) P_t   (P_t = shampoo_precondition's P)
+ *     eta_b = eta0 ||M_t||_F / ||Pm_t||_F (0 if ||Pm_t|| = 0);  W -= eta_b Pm_t
+ *   else:  eta_b = eta0;  W -= eta0 M_t                               (lines 22-23)
+ * Norms are fixed-order fp64 sums over the stored fp32 values (deterministic).
+ *   tensors, states, blocks : DEVICE tables (parallel tensor / state arrays)
+ *   eta_out : double[n_blocks] out (nullable)
+ *   workspace: >= shampoo_momentum_workspace_bytes(n_blocks), 256-B aligned */
+size_t shampoo_momentum_workspace_bytes(int32_t n_blocks);
+int shampoo_momentum_step(const shampoo_tensor_t* tensors, const shampoo_state_t* states, int32_t n_tensors,
+                          const shampoo_block_t* blocks, int32_t n_blocks, double beta1, double eta0,
+                          int32_t shampoo_branch, double* eta_out, void* workspace, size_t workspace_bytes,
+                          shampoo_stream_t stream);
 
 /* Number of kernel launches the last compute call on this host thread
  * enqueued (bench accounting, "gpu_launches"). */

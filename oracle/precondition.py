@@ -70,3 +70,28 @@ def precondition_plan(Gs, Ds, pl, roots: np.ndarray, graft_num=None, blocks=None
         if graft_num is not None:
             scales[bi] = graft_scale(float(graft_num[bi]), dens[bi])
     return Ps, scales, dens
+
+
+def momentum_step_block(W, M, Pm, G, D, P, beta1: float, eta0: float, shampoo_branch: bool):
+    """f2: the tail of Alg. 1 for one block (reading #9), in
+    place on fp32 state arrays W, M, Pm (views of the block); arithmetic in fp64,
+    every stored value rounded to fp32; norms over the stored fp32 values.
+        M  <- beta1 M + (1-beta1) D^{-1/2} o G                 (line 12)
+        t > tau: Pm <- beta1 Pm + (1-beta1) P                  (line 18)
+                 eta = eta0 ||M||_F / ||Pm||_F  (0 if ||Pm|| = 0)  (line 19)
+                 W <- W - eta Pm                               (line 20)
+        else:    eta = eta0;  W <- W - eta0 M                  (lines 22-23)
+    Returns eta."""
+    g = np.asarray(G, np.float64)
+    d = np.maximum(np.asarray(D, np.float64), 1e-30)
+    M[...] = (beta1 * M.astype(np.float64) + (1.0 - beta1) * (g / np.sqrt(d))).astype(np.float32)
+    if shampoo_branch:
+        Pm[...] = (beta1 * Pm.astype(np.float64) + (1.0 - beta1) * np.asarray(P, np.float64)).astype(np.float32)
+        nm = float(np.sum(M.astype(np.float64) ** 2))
+        npm = float(np.sum(Pm.astype(np.float64) ** 2))
+        eta = eta0 * np.sqrt(nm) / np.sqrt(npm) if npm > 0 else 0.0
+        W[...] = (W.astype(np.float64) - eta * Pm.astype(np.float64)).astype(np.float32)
+    else:
+        eta = eta0
+        W[...] = (W.astype(np.float64) - eta0 * M.astype(np.float64)).astype(np.float32)
+    return float(eta)

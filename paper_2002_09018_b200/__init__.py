@@ -24,7 +24,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BLOCK_DTYPE, GROUP_DTYPE, ROOT_INFO_DTYPE, TENSOR_DTYPE, ShampooError, check, last_launch_count
+from ._lib import (BLOCK_DTYPE, GROUP_DTYPE, ROOT_INFO_DTYPE, STATE_DTYPE, TENSOR_DTYPE, ShampooError, check,
+                   last_launch_count)
 
 _lib.lib()  # fail loudly at import if the CUDA library is missing
 
@@ -242,3 +243,33 @@ def precondition(table: TensorTable, plan: Plan, roots: torch.Tensor, graft_num:
                                  graft_scale.data_ptr() if graft_scale is not None else None,
                                  den.data_ptr() if den is not None else None, ws.data_ptr(), ws.numel(),
                                  _stream_ptr(stream)))
+
+
+# ----------------------------------------------------------------------- f2
+class StateTable:
+    """Device table of shampoo_state_t (W, M, Pm per tensor), parallel to a TensorTable."""
+
+    def __init__(self, Ws, Ms, Pms):
+        host = np.zeros(len(Ws), STATE_DTYPE)
+        for i, (W, M, Pm) in enumerate(zip(Ws, Ms, Pms)):
+            for T in (W, M, Pm):
+                if T.dtype != torch.float32 or T.dim() != 2 or T.stride(1) != 1:
+                    raise ValueError(f"state {i}: need row-major 2-D float32 tensors")
+            host[i] = (W.data_ptr(), M.data_ptr(), Pm.data_ptr(), W.stride(0), M.stride(0), Pm.stride(0))
+        self.host = host
+        self.n = len(Ws)
+        self.dev = torch.from_numpy(host.view(np.uint8).copy()).to(Ws[0].device)
+        self._keep = (list(Ws), list(Ms), list(Pms))
+
+
+def momentum_step(table: TensorTable, states: StateTable, plan: Plan, beta1: float, eta0: float,
+                  shampoo_branch: bool, eta_out: torch.Tensor | None = None, stream=None):
+    """Alg. 1 lines 12, 17-23 per block: momentum of both directions, grafted step
+    size and the parameter update (f2)."""
+    L = _lib.lib()
+    nb = plan.n_blocks
+    ws = workspace(L.shampoo_momentum_workspace_bytes(nb), table.device, "momentum")
+    check(L.shampoo_momentum_step(table.dev.data_ptr(), states.dev.data_ptr(), table.n,
+                                  plan.device_blocks(table.device).data_ptr(), nb, float(beta1), float(eta0),
+                                  1 if shampoo_branch else 0, eta_out.data_ptr() if eta_out is not None else None,
+                                  ws.data_ptr(), ws.numel(), _stream_ptr(stream)))

@@ -22,6 +22,7 @@ GROUP_DTYPE = np.dtype([("owner", "<i4"), ("n", "<i4"), ("p", "<i4"), ("count", 
                         ("offset", "<i8"), ("stride", "<i8")])
 TENSOR_DTYPE = np.dtype([("G", "<u8"), ("D", "<u8"), ("P", "<u8"), ("ldg", "<i8"), ("ldd", "<i8"),
                          ("ldp", "<i8"), ("m", "<i8"), ("n", "<i8")])
+STATE_DTYPE = np.dtype([("W", "<u8"), ("M", "<u8"), ("Pm", "<u8"), ("ldw", "<i8"), ("ldm", "<i8"), ("ldpm", "<i8")])
 ROOT_INFO_DTYPE = np.dtype([("iters", "<i4"), ("status", "<i4"), ("lambda_max", "<f8"), ("err", "<f8")])
 assert BLOCK_DTYPE.itemsize == 72 and GROUP_DTYPE.itemsize == 32
 assert TENSOR_DTYPE.itemsize == 64 and ROOT_INFO_DTYPE.itemsize == 24
@@ -34,6 +35,7 @@ EXPORTED = [
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition",
+    "shampoo_momentum_workspace_bytes", "shampoo_momentum_step",
 ]
 
 
@@ -56,7 +58,7 @@ def lib():
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2002_09018_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2002_09018_b200/build.py` "
                           "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     L.shampoo_abi_version.restype = ctypes.c_int
@@ -82,6 +84,10 @@ def lib():
     L.shampoo_precondition_workspace_bytes.restype = _sz
     L.shampoo_precondition.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     L.shampoo_precondition.restype = ctypes.c_int
+    L.shampoo_momentum_workspace_bytes.argtypes = [_i32]
+    L.shampoo_momentum_workspace_bytes.restype = _sz
+    L.shampoo_momentum_step.argtypes = [_vp, _vp, _i32, _vp, _i32, _dbl, _dbl, _i32, _vp, _vp, _sz, _vp]
+    L.shampoo_momentum_step.restype = ctypes.c_int
     if L.shampoo_abi_version() != 1:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L

@@ -1,7 +1,7 @@
 """Build libshampoo.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2002_09018_b200.build            # incremental
-    python -m paper_2002_09018_b200.build --force    # rebuild everything
+    python paper_2002_09018_b200/build.py            # incremental
+    python paper_2002_09018_b200/build.py --force    # rebuild everything
 """
 
 from __future__ import annotations
@@ -23,7 +23,7 @@ CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLU
             "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
-SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu", "tc_gemm.cu"]
+SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu", "tc_gemm.cu", "momentum.cu"]
 HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h", "tc_common.cuh", "tc_gemm.h"]
 
 

@@ -178,4 +178,23 @@ int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors
                              workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
 }
 
+size_t shampoo_momentum_workspace_bytes(int32_t n_blocks) { return n_blocks > 0 ? momentum_workspace_bytes(n_blocks) : 0; }
+
+int shampoo_momentum_step(const shampoo_tensor_t* tensors, const shampoo_state_t* states, int32_t n_tensors,
+                          const shampoo_block_t* blocks, int32_t n_blocks, double beta1, double eta0,
+                          int32_t shampoo_branch, double* eta_out, void* workspace, size_t workspace_bytes,
+                          shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
+  if (n_blocks == 0) return SHAMPOO_OK;
+  if (!tensors || !states || !blocks) return set_error(SHAMPOO_ERR_INVALID_ARG, "null table");
+  if (!std::isfinite(beta1) || beta1 < 0.0 || beta1 >= 1.0 || !std::isfinite(eta0))
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "beta1 must be in [0, 1) and eta0 finite");
+  int rc = check_ws(workspace, workspace_bytes, momentum_workspace_bytes(n_blocks));
+  if (rc) return rc;
+  return momentum_launch(tensors, states, blocks, n_blocks, beta1, eta0, shampoo_branch ? 1 : 0, eta_out, workspace,
+                         static_cast<cudaStream_t>(stream), &g_launches);
+}
+
 }  // extern "C"

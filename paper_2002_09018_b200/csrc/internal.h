@@ -35,6 +35,12 @@ int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, con
                         int n_blocks, const float* roots, const double* graft_num, float* graft_scale, double* den,
                         void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
 
+// momentum.cu
+size_t momentum_workspace_bytes(int n_blocks);
+int momentum_launch(const shampoo_tensor_t* tensors, const shampoo_state_t* states, const shampoo_block_t* blocks,
+                    int n_blocks, double beta1, double eta0, int shampoo_branch, double* eta_out, void* ws,
+                    cudaStream_t stream, int64_t* launches);
+
 int num_sms();
 
 }  // namespace shp

@@ -18,8 +18,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def shp():
-    from paper_2002_09018_b200 import build
-    build.build()
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_shampoo_build", os.path.join(ROOT, "paper_2002_09018_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
     import paper_2002_09018_b200 as shp
     return shp
 
@@ -27,7 +30,7 @@ def shp():
 def test_library_exports_every_declared_symbol(shp):
     from paper_2002_09018_b200 import _lib
     header = open(os.path.join(ROOT, "include", "shampoo.h")).read()
-    declared = sorted(set(re.findall(r"\b(shampoo_[a-z_0-9]+)\s*\(", header)))
+    declared = sorted(set(re.findall(r"^(?:int|int64_t|size_t|const char\*)\s+(shampoo_[a-z_0-9]+)\(", header, re.M)))
     assert len(declared) >= 12
     L = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared:

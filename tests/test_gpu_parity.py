@@ -411,3 +411,39 @@ def test_root_results_independent_of_batch_size(shp):
     Xl, _ = shp.inverse_pth_root_batched(torch.from_numpy(As).to(DEV), 4)
     torch.cuda.synchronize()
     assert torch.equal(Xs, Xl[:3])
+
+
+@pytest.mark.parametrize("branch,beta1", [(True, 0.0), (True, 0.9), (False, 0.9)])
+def test_momentum_step_vs_oracle(shp, branch, beta1):
+    """f2: Alg. 1 tail (momentum, grafted step size, update) per block vs the oracle, two steps."""
+    shapes = [(200, 240), (300, 100), (1, 50)]
+    pl_o = oplan.plan(shapes, 128, 256, 1)
+    pl = shp.make_plan(shapes, 128, 256, 1)
+    W_o = [synth.gaussian(s, 300 + i) for i, s in enumerate(shapes)]
+    M_o = [np.zeros(s, np.float32) for s in shapes]
+    Pm_o = [np.zeros(s, np.float32) for s in shapes]
+    Wd = [torch.from_numpy(w.copy()).to(DEV) for w in W_o]
+    Md = [torch.zeros(s, dtype=torch.float32, device=DEV) for s in shapes]
+    Pmd = [torch.zeros(s, dtype=torch.float32, device=DEV) for s in shapes]
+    states = shp.StateTable(Wd, Md, Pmd)
+    for step in range(2):
+        Gs = [synth.gaussian(s, 400 + 10 * step + i) for i, s in enumerate(shapes)]
+        Ds = [np.abs(synth.gaussian(s, 500 + 10 * step + i)) + 0.1 for i, s in enumerate(shapes)]
+        Ps = [synth.gaussian(s, 600 + 10 * step + i) for i, s in enumerate(shapes)]
+        table = shp.TensorTable([torch.from_numpy(g).to(DEV) for g in Gs], [torch.from_numpy(d).to(DEV) for d in Ds],
+                                [torch.from_numpy(p).to(DEV) for p in Ps])
+        eta = torch.zeros(pl.n_blocks, dtype=torch.float64, device=DEV)
+        shp.momentum_step(table, states, pl, beta1, 0.05, branch, eta)
+        eta_o = []
+        for b in pl_o.blocks:
+            sl = (slice(b.row0, b.row0 + b.rows), slice(b.col0, b.col0 + b.cols))
+            t = b.tensor_id
+            eta_o.append(opre.momentum_step_block(W_o[t][sl], M_o[t][sl], Pm_o[t][sl], Gs[t][sl], Ds[t][sl],
+                                                  Ps[t][sl], beta1, 0.05, branch))
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(eta.cpu().numpy(), eta_o, rtol=1e-6)
+        for t in range(len(shapes)):
+            np.testing.assert_allclose(Md[t].cpu().numpy(), M_o[t], rtol=1e-6, atol=1e-7)
+            np.testing.assert_allclose(Wd[t].cpu().numpy(), W_o[t], rtol=1e-6, atol=1e-7)
+            if branch:
+                np.testing.assert_allclose(Pmd[t].cpu().numpy(), Pm_o[t], rtol=1e-6, atol=1e-7)

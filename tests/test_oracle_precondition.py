@@ -103,3 +103,59 @@ def test_precondition_plan_assembles_blocks():
     # (40000, 3): left skipped (> 8192), right p = 2 with identity root -> P = G
     np.testing.assert_array_equal(Ps[1], Gs[1].astype(np.float64))
     assert np.all(scales > 0)
+
+
+# ------------------------------------------------------------------ f2 tail
+
+def _blk(shape, seed):
+    return gaussian(shape, seed)
+
+
+def test_momentum_beta0_graft_identity():
+    # with beta1 = 0 the update has norm eta0 * ||D^{-1/2} o G||_F
+    G, P = _blk((5, 7), 1), _blk((5, 7), 2)
+    D = np.abs(_blk((5, 7), 3)) + 0.5
+    W = _blk((5, 7), 4)
+    W0 = W.copy()
+    M = np.zeros_like(W)
+    Pm = np.zeros_like(W)
+    eta = opre.momentum_step_block(W, M, Pm, G, D, P, 0.0, 0.1, True)
+    step = np.linalg.norm((W - W0).astype(np.float64))
+    want = 0.1 * np.linalg.norm(G.astype(np.float64) / np.sqrt(D.astype(np.float64)))
+    assert abs(step - want) < 1e-5 * want
+    assert eta > 0
+
+
+def test_momentum_warm_start_branch_is_adagrad():
+    # lines 22-23: t <= tau -> W -= eta0 M (diagonal AdaGrad with momentum), P ignored
+    G = _blk((4, 4), 5)
+    D = np.abs(_blk((4, 4), 6)) + 1.0
+    W = np.zeros((4, 4), np.float32)
+    M = np.zeros_like(W)
+    Pm = np.full_like(W, 3.0)
+    opre.momentum_step_block(W, M, Pm, G, D, None, 0.0, 0.5, False)
+    np.testing.assert_allclose(W, -0.5 * G / np.sqrt(D), rtol=1e-6)
+    assert np.all(Pm == 3.0)
+
+
+def test_momentum_two_step_unrolled():
+    b1 = 0.9
+    Gs = [_blk((3, 6), 10 + s) for s in range(2)]
+    Ds = [np.abs(_blk((3, 6), 20 + s)) + 0.25 for s in range(2)]
+    Ps = [_blk((3, 6), 30 + s) for s in range(2)]
+    W = np.zeros((3, 6), np.float32)
+    M = np.zeros_like(W)
+    Pm = np.zeros_like(W)
+    for s in range(2):
+        opre.momentum_step_block(W, M, Pm, Gs[s], Ds[s], Ps[s], b1, 1.0, True)
+    a = [G.astype(np.float64) / np.sqrt(D.astype(np.float64)) for G, D in zip(Gs, Ds)]
+    np.testing.assert_allclose(M, b1 * (1 - b1) * a[0] + (1 - b1) * a[1], rtol=1e-5)
+    np.testing.assert_allclose(Pm, b1 * (1 - b1) * Ps[0] + (1 - b1) * Ps[1], rtol=1e-5, atol=1e-7)
+
+
+def test_momentum_zero_preconditioned_gradient():
+    W = _blk((2, 3), 40)
+    W0 = W.copy()
+    eta = opre.momentum_step_block(W, np.zeros_like(W), np.zeros_like(W), _blk((2, 3), 41), np.ones((2, 3)),
+                                   np.zeros((2, 3)), 0.0, 1.0, True)
+    assert eta == 0.0 and np.array_equal(W, W0)
