@@ -130,16 +130,18 @@ int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, i
  * t1 = weight*acc, t2 = decay*old, (float)(t1+t2)); they are BIT-EXACT with the
  * oracle.  (decay, weight) = (beta2, 1-beta2) or (1, 1) (reading #6).
  *   tensors, blocks : device tables (n_tensors / n_blocks entries)
+ *   blocks_host     : the same block table in HOST memory (sizes the workspace)
  *   stats           : packed fp32 statistics (offsets from the plan), in/out
  *   graft_num       : double[n_blocks] out (nullable)
  *   block_status    : int32[n_blocks] out (nullable)
- *   workspace       : >= shampoo_stats_workspace_bytes(n_blocks), 256-B aligned
+ *   workspace       : >= shampoo_stats_workspace_bytes(blocks_host, n_blocks, only_owner), 256-B
+ *                     aligned (holds the owned blocks widened to zero-padded fp64 panels)
  * G, D, P need only fp32 alignment; any ld >= n works. */
-size_t shampoo_stats_workspace_bytes(int32_t n_blocks);
+size_t shampoo_stats_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks, int32_t only_owner);
 int shampoo_stats_update(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
-                         int32_t n_blocks, int32_t only_owner, float* stats, double decay, double weight,
-                         double* graft_num, int32_t* block_status, void* workspace, size_t workspace_bytes,
-                         shampoo_stream_t stream);
+                         const shampoo_block_t* blocks_host, int32_t n_blocks, int32_t only_owner, float* stats,
+                         double decay, double weight, double* graft_num, int32_t* block_status, void* workspace,
+                         size_t workspace_bytes, shampoo_stream_t stream);
 
 /* --------------------------------------- a3-a6: batched inverse p-th roots
  * X_i ~ (A_i + eps_rel*lambda_hat_i*I)^{-1/p} for a strided batch of n x n

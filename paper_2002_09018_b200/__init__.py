@@ -143,10 +143,10 @@ def stats_update(table: TensorTable, plan: Plan, stats: torch.Tensor, decay: flo
     assert stats.dtype == torch.float32 and stats.is_contiguous() and stats.numel() >= plan.stats_elems
     L = _lib.lib()
     nb = plan.n_blocks
-    wsb = L.shampoo_stats_workspace_bytes(nb)
+    wsb = L.shampoo_stats_workspace_bytes(plan.blocks.ctypes.data, nb, only_owner)
     ws = workspace(wsb, stats.device, "stats")
-    check(L.shampoo_stats_update(table.dev.data_ptr(), table.n, plan.device_blocks(stats.device).data_ptr(), nb,
-                                 only_owner, stats.data_ptr(), float(decay), float(weight),
+    check(L.shampoo_stats_update(table.dev.data_ptr(), table.n, plan.device_blocks(stats.device).data_ptr(),
+                                 plan.blocks.ctypes.data, nb, only_owner, stats.data_ptr(), float(decay), float(weight),
                                  graft_num.data_ptr() if graft_num is not None else None,
                                  block_status.data_ptr() if block_status is not None else None,
                                  ws.data_ptr(), ws.numel(), _stream_ptr(stream)))

@@ -66,9 +66,9 @@ def lib():
     L.shampoo_last_launch_count.restype = _i64
     L.shampoo_plan.argtypes = [_vp, _i32, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp]
     L.shampoo_plan.restype = ctypes.c_int
-    L.shampoo_stats_workspace_bytes.argtypes = [_i32]
+    L.shampoo_stats_workspace_bytes.argtypes = [_vp, _i32, _i32]
     L.shampoo_stats_workspace_bytes.restype = _sz
-    L.shampoo_stats_update.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp, _dbl, _dbl, _vp, _vp, _vp, _sz, _vp]
+    L.shampoo_stats_update.argtypes = [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _dbl, _dbl, _vp, _vp, _vp, _sz, _vp]
     L.shampoo_stats_update.restype = ctypes.c_int
     L.shampoo_root_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
     L.shampoo_root_workspace_bytes.restype = _sz

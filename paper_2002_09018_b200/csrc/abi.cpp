@@ -75,22 +75,24 @@ int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, i
                    group_capacity, n_groups, stats_elems, segment_elems);
 }
 
-size_t shampoo_stats_workspace_bytes(int32_t n_blocks) { return n_blocks > 0 ? stats_workspace_bytes(n_blocks) : 0; }
+size_t shampoo_stats_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks, int32_t only_owner) {
+  return (n_blocks > 0 && blocks_host) ? stats_workspace_bytes(blocks_host, n_blocks, only_owner) : 0;
+}
 
 int shampoo_stats_update(const shampoo_tensor_t* tensors, int32_t n_tensors, const shampoo_block_t* blocks,
-                         int32_t n_blocks, int32_t only_owner, float* stats, double decay, double weight,
-                         double* graft_num, int32_t* block_status, void* workspace, size_t workspace_bytes,
-                         shampoo_stream_t stream) {
+                         const shampoo_block_t* blocks_host, int32_t n_blocks, int32_t only_owner, float* stats,
+                         double decay, double weight, double* graft_num, int32_t* block_status, void* workspace,
+                         size_t workspace_bytes, shampoo_stream_t stream) {
   g_err[0] = 0;
   g_launches = 0;
   if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
   if (n_blocks == 0) return SHAMPOO_OK;
-  if (!tensors || !blocks) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block table");
+  if (!tensors || !blocks || !blocks_host) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block table");
   if (!std::isfinite(decay) || !std::isfinite(weight))
     return set_error(SHAMPOO_ERR_INVALID_ARG, "decay/weight must be finite");
   if (!stats) return set_error(SHAMPOO_ERR_INVALID_ARG, "null statistics buffer");
   if (!aligned16(stats)) return set_error(SHAMPOO_ERR_INVALID_ARG, "statistics buffer not 16-B aligned");
-  int rc = check_ws(workspace, workspace_bytes, stats_workspace_bytes(n_blocks));
+  int rc = check_ws(workspace, workspace_bytes, stats_workspace_bytes(blocks_host, n_blocks, only_owner));
   if (rc) return rc;
   return stats_launch(tensors, n_tensors, blocks, n_blocks, only_owner, stats, decay, weight, graft_num, block_status,
                       workspace, static_cast<cudaStream_t>(stream), &g_launches);

@@ -23,7 +23,7 @@ int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* 
                     void* ws, cudaStream_t stream, int64_t* launches);
 
 // stats.cu
-size_t stats_workspace_bytes(int n_blocks);
+size_t stats_workspace_bytes(const shampoo_block_t* blocks_host, int n_blocks, int only_owner);
 int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_block_t* blocks, int n_blocks,
                  int only_owner, float* stats, double decay, double weight, double* graft_num, int32_t* block_status,
                  void* ws, cudaStream_t stream, int64_t* launches);

@@ -8,7 +8,9 @@
 // (double)a_k*(double)b_k in fp64; t1 = weight*acc; t2 = decay*old; (float)(t1+t2).
 //
 // Launch sequence (one step, all blocks of all tensors):
-//   memset(flags) -> check (non-finite G per block) -> prep (tile prefix sums)
+//   memset(flags) -> check (non-finite G per block) -> prep (tile / buffer prefix sums)
+//   -> widen (owned blocks: fp32 G_b -> zero-padded fp64 row panels, G_b and G_b^T,
+//      so the DMMA tiles stream from the cp.async fp64 pipeline of the Newton core)
 //   -> stats (persistent DMMA tiles, L and R, owned blocks only)
 //   -> diag (D update + per-chunk graft partials) -> finish (fixed-order sums)
 #include <algorithm>
@@ -19,20 +21,36 @@
 namespace shp {
 
 constexpr int kChunks = 64;  // row chunks per block for the elementwise passes
-constexpr int kPrefixSmem = 4096;  // prefix entries cached in shared memory (32 KB)
-constexpr int kStatsGemmBytes = 4 * kAsyncTile * 8;  // 2 stages x (A, B) fp64 tiles, 64 KB
+constexpr int kPrefixSmem = 1536;  // prefix entries cached in shared memory (12 KB; 2 CTAs/SM)
 
 struct StatsWs {
   int* flag;         // n_blocks (non-finite marker)
   int64_t* prefix;   // n_blocks + 1 (stats tiles)
+  int64_t* offL;     // n_blocks: fp64 offset of the widened G_b   (rows_p64 x roundup(cols, 32)), -1 if none
+  int64_t* offR;     // n_blocks: fp64 offset of the widened G_b^T (cols_p64 x roundup(rows, 32)), -1 if none
   double* part;      // n_blocks * kChunks
+  double* wide;      // widened operands
 };
 
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+static int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-size_t stats_workspace_bytes(int n_blocks) {
-  return al((size_t)n_blocks * sizeof(int)) + al((size_t)(n_blocks + 1) * sizeof(int64_t)) +
+static bool owns_l(const shampoo_block_t& b, int only_owner) { return b.p_left && (only_owner < 0 || b.owner_left == only_owner); }
+static bool owns_r(const shampoo_block_t& b, int only_owner) { return b.p_right && (only_owner < 0 || b.owner_right == only_owner); }
+
+static size_t fixed_bytes(int n_blocks) {
+  return al((size_t)n_blocks * sizeof(int)) + 3 * al((size_t)(n_blocks + 1) * sizeof(int64_t)) +
          al((size_t)n_blocks * kChunks * sizeof(double));
+}
+
+size_t stats_workspace_bytes(const shampoo_block_t* blocks_host, int n_blocks, int only_owner) {
+  size_t wide = 0;
+  for (int b = 0; b < n_blocks; ++b) {
+    const shampoo_block_t& k = blocks_host[b];
+    if (owns_l(k, only_owner)) wide += (size_t)rup(k.rows, 64) * rup(k.cols, 32);
+    if (owns_r(k, only_owner)) wide += (size_t)rup(k.cols, 64) * rup(k.rows, 32);
+  }
+  return fixed_bytes(n_blocks) + al(wide * sizeof(double));
 }
 
 static StatsWs carve(void* ws, int n_blocks) {
@@ -40,9 +58,16 @@ static StatsWs carve(void* ws, int n_blocks) {
   StatsWs w;
   w.flag = reinterpret_cast<int*>(q);
   q += al((size_t)n_blocks * sizeof(int));
+  const size_t pb = al((size_t)(n_blocks + 1) * sizeof(int64_t));
   w.prefix = reinterpret_cast<int64_t*>(q);
-  q += al((size_t)(n_blocks + 1) * sizeof(int64_t));
+  q += pb;
+  w.offL = reinterpret_cast<int64_t*>(q);
+  q += pb;
+  w.offR = reinterpret_cast<int64_t*>(q);
+  q += pb;
   w.part = reinterpret_cast<double*>(q);
+  q += al((size_t)n_blocks * kChunks * sizeof(double));
+  w.wide = reinterpret_cast<double*>(q);
   return w;
 }
 
@@ -71,37 +96,97 @@ __global__ void __launch_bounds__(kThreads) check_kernel(const shampoo_tensor_t*
 }
 
 // ----------------------------------------------------- tile prefix sums
-// Single CTA of 1024 threads: chunked exclusive scan of per-block tile counts.
+// Single CTA of 1024 threads: chunked exclusive scans of the per-block tile
+// counts and of the widened-operand sizes.
+SHP_DEV int64_t rupd(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+SHP_DEV void block_sizes(const shampoo_block_t& blk, int only_owner, int64_t& tiles, int64_t& szl, int64_t& szr) {
+  const bool l = blk.p_left && (only_owner < 0 || blk.owner_left == only_owner);
+  const bool r = blk.p_right && (only_owner < 0 || blk.owner_right == only_owner);
+  tiles = (l ? upper_count(blk.rows) : 0) + (r ? upper_count(blk.cols) : 0);
+  szl = l ? rupd(blk.rows, 64) * rupd(blk.cols, 32) : 0;
+  szr = r ? rupd(blk.cols, 64) * rupd(blk.rows, 32) : 0;
+}
+
 __global__ void __launch_bounds__(1024) prep_kernel(const shampoo_block_t* blocks, int n_blocks, int only_owner,
-                                                    int64_t* prefix) {
-  __shared__ int64_t part[1024];
+                                                    int64_t* prefix, int64_t* offL, int64_t* offR) {
+  __shared__ int64_t pt[1024], pw[1024];
   const int t = threadIdx.x;
   const int per = (n_blocks + 1023) / 1024;
   const int b0 = t * per, b1 = min(n_blocks, b0 + per);
-  int64_t s = 0;
+  int64_t st = 0, sw = 0;
   for (int b = b0; b < b1; ++b) {
-    const shampoo_block_t blk = blocks[b];
-    if (blk.p_left && (only_owner < 0 || blk.owner_left == only_owner)) s += upper_count(blk.rows);
-    if (blk.p_right && (only_owner < 0 || blk.owner_right == only_owner)) s += upper_count(blk.cols);
+    int64_t tl, zl, zr;
+    block_sizes(blocks[b], only_owner, tl, zl, zr);
+    st += tl;
+    sw += zl + zr;
   }
-  part[t] = s;
+  pt[t] = st;
+  pw[t] = sw;
   __syncthreads();
   if (t == 0) {
-    int64_t acc = 0;
+    int64_t a = 0, c = 0;
     for (int i = 0; i < 1024; ++i) {
-      const int64_t v = part[i];
-      part[i] = acc;
-      acc += v;
+      const int64_t v = pt[i], u = pw[i];
+      pt[i] = a;
+      pw[i] = c;
+      a += v;
+      c += u;
     }
-    prefix[n_blocks] = acc;
+    prefix[n_blocks] = a;
   }
   __syncthreads();
-  int64_t acc = part[t];
+  int64_t a = pt[t], c = pw[t];
   for (int b = b0; b < b1; ++b) {
-    prefix[b] = acc;
-    const shampoo_block_t blk = blocks[b];
-    if (blk.p_left && (only_owner < 0 || blk.owner_left == only_owner)) acc += upper_count(blk.rows);
-    if (blk.p_right && (only_owner < 0 || blk.owner_right == only_owner)) acc += upper_count(blk.cols);
+    prefix[b] = a;
+    int64_t tl, zl, zr;
+    block_sizes(blocks[b], only_owner, tl, zl, zr);
+    offL[b] = zl ? c : -1;
+    offR[b] = zr ? c + zl : -1;
+    a += tl;
+    c += zl + zr;
+  }
+}
+
+// ------------------------------------------------- widen fp32 -> fp64 panels
+// For every owned side: GL = G_b (rows_p64 x kp, kp = roundup(cols, 32)) and
+// GR = G_b^T (cols_p64 x roundup(rows, 32)), zero-padded; 64x64 tiles through
+// shared memory so both the straight and the transposed writes are coalesced.
+constexpr int kWideCTAs = 64;
+
+__global__ void __launch_bounds__(256) widen_kernel(const shampoo_tensor_t* tensors, const shampoo_block_t* blocks,
+                                                    const int* flag, const int64_t* offL, const int64_t* offR,
+                                                    double* wide) {
+  __shared__ float tile[64][65];
+  const int b = blockIdx.x / kWideCTAs, c = blockIdx.x % kWideCTAs;
+  if (flag[b] || (offL[b] < 0 && offR[b] < 0)) return;
+  const shampoo_block_t blk = blocks[b];
+  const shampoo_tensor_t ten = tensors[blk.tensor_id];
+  const int tr = (blk.rows + 63) / 64, tc = (blk.cols + 63) / 64;
+  const int kpl = (int)rupd(blk.cols, 32), kpr = (int)rupd(blk.rows, 32);
+  for (int t = c; t < tr * tc; t += kWideCTAs) {
+    const int i0 = (t / tc) * 64, j0 = (t % tc) * 64;
+    for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+      const int i = e >> 6, j = e & 63;
+      const bool v = i0 + i < blk.rows && j0 + j < blk.cols;
+      tile[i][j] = v ? ten.G[(blk.row0 + i0 + i) * ten.ldg + blk.col0 + j0 + j] : 0.0f;
+    }
+    __syncthreads();
+    if (offL[b] >= 0) {  // rows i0.., columns j0.. (< kpl)
+      double* dst = wide + offL[b];
+      for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+        const int i = e >> 6, j = e & 63;
+        if (j0 + j < kpl) dst[(int64_t)(i0 + i) * kpl + j0 + j] = (double)tile[i][j];
+      }
+    }
+    if (offR[b] >= 0) {  // rows j0.. of G^T, columns i0.. (< kpr)
+      double* dst = wide + offR[b];
+      for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+        const int j = e >> 6, i = e & 63;
+        if (i0 + i < kpr) dst[(int64_t)(j0 + j) * kpr + i0 + i] = (double)tile[i][j];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -117,15 +202,16 @@ SHP_DEV int find_block(const int64_t* prefix, int n_blocks, int64_t item) {
 
 // ------------------------------------------------------------ statistics
 __global__ void __launch_bounds__(kNThreads, 2)
-    stats_kernel(const shampoo_tensor_t* tensors, const shampoo_block_t* blocks, int n_blocks, int only_owner,
-                 float* stats, double decay, double weight, const int* flag, const int64_t* prefix) {
+    stats_kernel(const shampoo_block_t* blocks, int n_blocks, int only_owner, float* stats, double decay,
+                 double weight, const int* flag, const int64_t* prefix, const int64_t* offL, const int64_t* offR,
+                 const double* wide) {
   extern __shared__ __align__(16) double smem[];
   const int64_t total = prefix[n_blocks];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // tile -> block lookups binary-search the prefix array; keep it in shared
   // memory (after the GEMM buffers) when it fits, instead of 9 dependent
   // global loads at every tile start
-  int64_t* spre = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(smem) + kStatsGemmBytes);
+  int64_t* spre = reinterpret_cast<int64_t*>(smem + kAsyncSmemDoubles);
   const bool pre_in_smem = n_blocks + 1 <= kPrefixSmem;
   if (pre_in_smem)
     for (int i = threadIdx.x; i <= n_blocks; i += kNThreads) spre[i] = prefix[i];
@@ -148,10 +234,10 @@ __global__ void __launch_bounds__(kNThreads, 2)
     const int K = side == 0 ? blk.cols : blk.rows;
     int ti, tj;
     upper_tile((int)local, tiles_of(nvalid), ti, tj);
-    const shampoo_tensor_t ten = tensors[blk.tensor_id];
-    const float* gb = ten.G + blk.row0 * ten.ldg + blk.col0;
-    F32PanelN la{gb, ten.ldg, side, ti * kNT, nvalid, K};
-    F32PanelN lb{gb, ten.ldg, side, tj * kNT, nvalid, K};
+    // widened, zero-padded fp64 panels (K padded with zeros at its END: the
+    // ascending-k sequential sum is unchanged)
+    const int kp = (int)rupd(K, 32);
+    const double* base = wide + (side == 0 ? offL[b] : offR[b]);
     // the old statistic values of this thread's outputs, loaded before the k loop
     // so their latency hides behind the DMMAs
     float* S = stats + (side == 0 ? blk.left_off : blk.right_off);
@@ -168,7 +254,7 @@ __global__ void __launch_bounds__(kNThreads, 2)
           oldv[mt][nt][e] = (i < nvalid && j < nvalid && i <= j) ? S[(int64_t)i * ld + j] : 0.0f;
         }
     }
-    gemm_tile_f32n(acc, la, lb, (K + kAsyncK - 1) / kAsyncK, smem);
+    gemm_tile_f64(acc, base + (int64_t)ti * kNT * kp, base + (int64_t)tj * kNT * kp, kp, kp / kAsyncK, smem);
     // epilogue: EMA with the fixed rounding sequence, upper triangle + mirror
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
@@ -244,8 +330,9 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
   if (n_blocks == 0) return SHAMPOO_OK;
   StatsWs w = carve(ws, n_blocks);
   static bool configured = false;
-  const size_t smem_max = (size_t)kStatsGemmBytes + (size_t)kPrefixSmem * sizeof(int64_t);
-  const size_t smem = (size_t)kStatsGemmBytes + (size_t)std::min(n_blocks + 1, kPrefixSmem) * sizeof(int64_t);
+  const size_t smem_max = (size_t)kAsyncSmemDoubles * sizeof(double) + (size_t)kPrefixSmem * sizeof(int64_t);
+  const size_t smem =
+      (size_t)kAsyncSmemDoubles * sizeof(double) + (size_t)std::min(n_blocks + 1, kPrefixSmem) * sizeof(int64_t);
   if (!configured) {
     if (cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max) != cudaSuccess)
       return set_cuda_error("cudaFuncSetAttribute(stats_kernel)");
@@ -255,12 +342,13 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
     return set_cuda_error("cudaMemsetAsync");
   const unsigned eg = (unsigned)n_blocks * kChunks;
   check_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.flag);
-  prep_kernel<<<1, 1024, 0, stream>>>(blocks, n_blocks, only_owner, w.prefix);
-  stats_kernel<<<2 * num_sms(), kNThreads, smem, stream>>>(tensors, blocks, n_blocks, only_owner, stats, decay, weight,
-                                                      w.flag, w.prefix);
+  prep_kernel<<<1, 1024, 0, stream>>>(blocks, n_blocks, only_owner, w.prefix, w.offL, w.offR);
+  widen_kernel<<<(unsigned)n_blocks * kWideCTAs, 256, 0, stream>>>(tensors, blocks, w.flag, w.offL, w.offR, w.wide);
+  stats_kernel<<<2 * num_sms(), kNThreads, smem, stream>>>(blocks, n_blocks, only_owner, stats, decay, weight, w.flag,
+                                                           w.prefix, w.offL, w.offR, w.wide);
   diag_kernel<<<eg, kThreads, 0, stream>>>(tensors, blocks, w.flag, w.part);
   finish_kernel<<<(n_blocks + 255) / 256, 256, 0, stream>>>(n_blocks, w.flag, w.part, graft_num, block_status);
-  *launches += 5;
+  *launches += 6;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("stats kernels", e);
   return SHAMPOO_OK;

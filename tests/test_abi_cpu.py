@@ -107,14 +107,16 @@ def test_host_checked_errors_need_no_device(shp):
     assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 4, 1e-6, 1e-7, 100, 100, fake, fake,
                                               16, None) == 4
     # statistics: non-finite decay
-    assert L.shampoo_stats_update(fake, 1, fake, 1, -1, fake, float("inf"), 1.0, None, None, fake, 1 << 30,
+    assert L.shampoo_stats_update(fake, 1, fake, fake, 1, -1, fake, float("inf"), 1.0, None, None, fake, 1 << 30,
                                   None) == 1
     # empty batch is a no-op
     assert L.shampoo_inverse_pth_root_batched(None, 0, 0, None, 0, 0, 0, 8, 4, 1e-6, 1e-7, 100, 100, None, None, 0,
                                               None) == 0
     # workspace sizes are pure host functions
     assert L.shampoo_root_workspace_bytes(2, 1024, 4, 100) >= 2 * 7 * 1024 * 1024 * 8
-    assert L.shampoo_stats_workspace_bytes(10) > 0
+    blk = np.zeros(1, _lib.BLOCK_DTYPE)
+    blk["rows"], blk["cols"], blk["p_left"], blk["p_right"] = 100, 70, 4, 4
+    assert L.shampoo_stats_workspace_bytes(blk.ctypes.data, 1, -1) >= (128 * 96 + 128 * 128) * 8
 
 
 def test_product_package_does_not_import_oracle():
