@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SHAMPOO_ABI_VERSION 1
+#define SHAMPOO_ABI_VERSION 2
 
 typedef enum {
   SHAMPOO_OK = 0,
@@ -50,14 +50,18 @@ typedef void* shampoo_stream_t; /* a cudaStream_t (NULL = legacy default stream)
 
 /* One block of one parameter tensor (plan output; integer, bit-exact vs the
  * oracle).  P:396-398: "divide the tensor into blocks and treating individual
- * block as a separate tensor".  72 bytes. */
+ * block as a separate tensor".  80 bytes.  The root of a side is S^{-r/p}:
+ * (r, p) = (1, 4) two-sided, (1, 2) one-sided, p = 0 skipped; a split plan
+ * (f4) gives e.g. (1, 8) / (3, 8). */
 typedef struct {
   int32_t tensor_id;   /* index into the caller's tensor list                          */
   int32_t reserved;    /* 0                                                            */
   int64_t row0, col0;  /* block origin inside the tensor                               */
   int32_t rows, cols;  /* extent; the last block of each axis may be ragged            */
-  int32_t p_left;      /* exponent of L_b^{-1/p}: 4 two-sided, 2 one-sided, 0 skipped  */
-  int32_t p_right;     /* exponent of R_b^{-1/p}                                       */
+  int32_t p_left;      /* root order of L_b^{-r/p}: 4 two-sided, 2 one-sided, 0 skipped */
+  int32_t p_right;     /* root order of R_b^{-r/p}                                     */
+  int32_t r_left;      /* exponent numerator of the left root (0 if skipped)           */
+  int32_t r_right;     /* exponent numerator of the right root (0 if skipped)          */
   int32_t owner_left;  /* rank that updates L_b and computes its root (-1 if skipped)  */
   int32_t owner_right; /* rank that updates R_b and computes its root (-1 if skipped)  */
   int64_t left_off;    /* element offset of L_b (and of its root) in the packed buffer */
@@ -66,11 +70,13 @@ typedef struct {
   int32_t right_ld;    /* leading dimension of R_b = roundup(cols, 4)                  */
 } shampoo_block_t;
 
-/* A strided batch of same-size roots owned by one rank (plan output). */
+/* A strided batch of same-size roots S^{-r/p} owned by one rank (plan output). */
 typedef struct {
   int32_t owner, n, p, count;
   int64_t offset; /* element offset of the first matrix in the packed buffer */
   int64_t stride; /* elements between consecutive matrices                   */
+  int32_t r;      /* exponent numerator                                       */
+  int32_t reserved;
 } shampoo_group_t;
 
 /* One parameter tensor.  An array of these lives in DEVICE memory. */
@@ -108,13 +114,18 @@ const char* shampoo_last_error(void);
  * Blocking plan, exponents, owners and packing (P:356-359, P:385-390,
  * P:396-398; rule in DESIGN.md §5 / oracle/plan.py).
  *   shapes      (host) 2*n_tensors int64: m0, n0, m1, n1, ...
+ *   split_num, split_den : the Lemma's split 1/p = split_num/split_den
+ *               (f4): two-sided blocks get
+ *               L^{-split_num/(2 split_den)} and R^{-(split_den-split_num)/(2 split_den)},
+ *               reduced to r/p with p <= 16.  (1, 2) = the default -1/4, -1/4.
+ *               1 <= split_num < split_den, else SHAMPOO_ERR_INVALID_ARG.
  *   blocks      (host, out) capacity entries, or NULL to query counts only
  *   groups      (host, out) group_capacity entries, or NULL
  *   stats_elems (host, out) elements of the packed statistics/roots buffer
  *               (= world_size * segment_elems; segment r holds rank r's roots)
  * Returns SHAMPOO_ERR_CAPACITY (counts still written) if an array is too small. */
 int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
-                 int32_t world_size, shampoo_block_t* blocks, int32_t capacity, int32_t* n_blocks,
+                 int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* blocks, int32_t capacity, int32_t* n_blocks,
                  shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups,
                  int64_t* stats_elems, int64_t* segment_elems);
 
@@ -151,9 +162,12 @@ int shampoo_stats_update(const shampoo_tensor_t* tensors, int32_t n_tensors, con
  *   A_hat = A + eps_rel*lambda_hat*I;  c = lambda_hat*(1+eps_rel);
  *   M_0 = A_hat/c;  X_0 = c^{-1/p} I;
  *   repeat: err = max|M-I|; stop if err <= tol (or stagnation / max_iter);
- *           T = ((p+1)I - M)/p;  X <- X T;  M <- T^p M.
+ *           T = ((p+1)I - M)/p;  X <- X T;  M <- T^p M
+ *           (T^p by the left-to-right binary chain of squarings and
+ *           multiplications by T).
  * Products run in fp64 on the FP64 tensor pipe (DMMA); results are written
- * as fp32.  p in {1, 2, 4, 8}; 1 <= n <= 8192.
+ * as fp32.  p integer in [1, 16] (c^{-1/p} by sqrt chains when p = 2^j,
+ * pow otherwise; reading #22); 1 <= n <= 8192.
  *   A   : batch matrices at A + i*stride_a, leading dim lda (fp32, read only)
  *   X   : outputs at X + i*stride_x, leading dim ldx (fp32; may alias A only if
  *         A == X with equal strides/ld -- the input is consumed first)
@@ -168,6 +182,19 @@ int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride
                                      double tol, int32_t max_iter, int32_t power_iters,
                                      shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
                                      shampoo_stream_t stream);
+
+/* f4: rational exponents ("L^{1/p} (x) R^{1/q}"
+ * "L^{-1/2p} G R^{-1/2q}"; reading #23):
+ *   X_i ~ A_hat_i^{-r/p} = (A_hat_i^{-1/p})^r,  1 <= r <= p <= 16,
+ * the p-th root above (same iteration, statuses and info, which describe the
+ * p-th root) raised to the integer power r by symmetric FP64 DMMA products
+ * (left-to-right binary chain) before the fp32 write.  r = 1 is exactly
+ * shampoo_inverse_pth_root_batched.  Same arguments and workspace. */
+int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                          int64_t stride_x, int32_t batch, int32_t n, int32_t p, int32_t r,
+                                          double eps_rel, double tol, int32_t max_iter, int32_t power_iters,
+                                          shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                          shampoo_stream_t stream);
 
 /* Independent root check (config 2, north-star invariant):
  *   residual_i = || X_i^p (A_i + eps_rel*lambda_i*I) - I ||_F   in fp64,

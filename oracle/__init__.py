@@ -20,6 +20,9 @@ of /root/reference/PAPER.md, "S:n" a line of /root/reference/SPEC.md, and
                        S:131-132).                                  fp64
 * ``precondition``  -- L^{-1/p} G R^{-1/p}, one-sided variants, grafting
                        (P:162, P:185-186, P:326-338, P:388-390).   fp64
+* ``tensor``        -- f3: order 1..4 tensors: plan, per-mode statistics
+                       (chunked sequential contract, plain C), mode products,
+                       grafting (P:113-116, P:132, P:356-359).     bit-exact / fp64
 
 Parity pins: every function above is checked by ``tests/test_oracle_*.py``
 (``-m "not gpu"``) against closed forms, eigendecomposition (numpy ``eigh``),
@@ -27,4 +30,4 @@ brute force on tiny inputs, exact integer arithmetic, or values printed in
 the paper / SPEC (``tests/golden/``).  No function here is "parity unpinned".
 """
 
-from . import plan, root, precondition, stats  # noqa: F401
+from . import plan, root, precondition, stats, tensor  # noqa: F401

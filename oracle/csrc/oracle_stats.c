@@ -82,3 +82,38 @@ double oracle_diag_update(const float* G, int64_t ldg, int64_t row0, int64_t col
     }
   return num;
 }
+
+/* ---------------------------------------------------------------- f3: tensors
+ * Mode statistic of one block of an order-k tensor (the paper's method "holds
+ * for tensors of arbitrary order"; per-mode statistics of
+ * the mode-i unfolding, DESIGN.md §6.5 / reading #24):
+ *   U  : rows x K row-major fp32, the mode-i unfolding of the block (row a =
+ *        index a of mode i; columns = the remaining block indices in row-major
+ *        order)
+ *   S  : rows x rows (leading dim lds) <- decay*S + weight * U U^T
+ * Chunked sequential contract (reading #25): for chunk c = [c*C, min(K, (c+1)*C)),
+ *   s_c = 0.0; for k ascending in the chunk: s_c = s_c + (double)u_a[k]*(double)u_b[k]
+ *   acc = 0.0; for c ascending: acc = acc + s_c
+ *   t1 = weight*acc; t2 = decay*(double)S_ab; S_ab = S_ba = (float)(t1 + t2)
+ * For K <= C this is exactly the matrix contract above. */
+void oracle_mode_stat(const float* U, int rows, int64_t K, int64_t chunk, float* S, int64_t lds, double decay,
+                      double weight) {
+  for (int a = 0; a < rows; ++a) {
+    const float* ua = U + (int64_t)a * K;
+    for (int b = a; b < rows; ++b) {
+      const float* ub = U + (int64_t)b * K;
+      double acc = 0.0;
+      for (int64_t c0 = 0; c0 < K; c0 += chunk) {
+        const int64_t c1 = c0 + chunk < K ? c0 + chunk : K;
+        double s = 0.0;
+        for (int64_t k = c0; k < c1; ++k) s = s + (double)ua[k] * (double)ub[k];
+        acc = acc + s;
+      }
+      double t1 = weight * acc;
+      double t2 = decay * (double)S[(int64_t)a * lds + b];
+      float r = (float)(t1 + t2);
+      S[(int64_t)a * lds + b] = r;
+      S[(int64_t)b * lds + a] = r;
+    }
+  }
+}

@@ -8,6 +8,10 @@ Rule (DESIGN.md §3 readings #5, #12, #13, #17):
 * Exponents: both sides kept -> p_L = p_R = 4 (L^{-1/4} G R^{-1/4}, P:162);
   one side kept -> p = 2 on that side ("G R^{-1/2} and L^{-1/2} G",
   P:388-390); none -> 0/0 (grafted diagonal AdaGrad direction).
+  f4 (P:385-387, "L^{-1/2p} G R^{-1/2q}" for 1/p + 1/q = 1; reading #23):
+  split = (a, d) sets 1/p = a/d, so a two-sided block uses the exponents
+  e_L = a/(2d) and e_R = (d-a)/(2d); each is stored reduced as r/p_root
+  (root = S^{-r/p_root}), p_root <= 16.  The default (1, 2) is (1/4, 1/4).
 * Blocking: each axis is split into ceil(dim/b) contiguous ranges, the last
   one ragged ("divide the tensor into blocks ... treating individual block as
   a separate tensor").  Blocks are ordered tensor by tensor (caller
@@ -19,7 +23,7 @@ Rule (DESIGN.md §3 readings #5, #12, #13, #17):
   ties) -- "we distribute the computation across all the CPUs" (P:300-303).
 * Packing: one fp32 buffer holds all statistics (and, at the same offsets,
   all roots).  Rank r's segment holds the roots it owns, grouped by (n desc,
-  p desc), each matrix ``n x ld`` with ``ld = roundup(n, 4)`` and a group
+  p desc, r desc), each matrix ``n x ld`` with ``ld = roundup(n, 4)`` and a group
   stride ``roundup(n*ld, 64)``.  Every segment is padded to the largest one
   (rounded up to 64 elements) so an all-gather of equal segments rebuilds the
   whole buffer.
@@ -31,10 +35,17 @@ from dataclasses import dataclass, field
 
 
 def products_per_iteration(p: int) -> int:
-    """Matrix products per coupled-Newton iteration: X*T, log2(p) squarings
-    of T, and T^p * M (the iteration of S:131)."""
-    squarings = {1: 0, 2: 1, 4: 2, 8: 3}[p]
-    return 2 + squarings
+    """Matrix products per coupled-Newton iteration (the iteration of S:131):
+    X*T, T^p by the left-to-right binary chain (bitlen(p)-1 squarings plus
+    popcount(p)-1 multiplications by T), and T^p * M."""
+    return 2 + (p.bit_length() - 1) + (bin(p).count("1") - 1)
+
+
+def reduce_exponent(num: int, den: int):
+    """num/den in lowest terms -> (r, p)."""
+    from math import gcd
+    g = gcd(num, den)
+    return num // g, den // g
 
 
 def _roundup(x: int, m: int) -> int:
@@ -51,6 +62,8 @@ class Block:
     cols: int
     p_left: int
     p_right: int
+    r_left: int = 0
+    r_right: int = 0
     owner_left: int = -1
     owner_right: int = -1
     left_off: int = -1
@@ -67,6 +80,7 @@ class RootGroup:
     offset: int
     count: int
     stride: int
+    r: int = 1
 
 
 @dataclass
@@ -78,9 +92,16 @@ class Plan:
     loads: list = field(default_factory=list)
 
 
-def plan(shapes, block_size: int, max_precond_dim: int, world_size: int) -> Plan:
+def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(1, 2)) -> Plan:
     if block_size < 1 or max_precond_dim < 1 or world_size < 1:
         raise ValueError("block_size, max_precond_dim and world_size must be >= 1")
+    sa, sd = split
+    if not (1 <= sa < sd):
+        raise ValueError("split (a, d) needs 1 <= a < d")
+    rl2, pl2 = reduce_exponent(sa, 2 * sd)
+    rr2, pr2 = reduce_exponent(sd - sa, 2 * sd)
+    if max(pl2, pr2) > 16:
+        raise ValueError("split exponents need a root order <= 16")
     out = Plan()
     for t, (m, n) in enumerate(shapes):
         if m < 1 or n < 1:
@@ -88,20 +109,20 @@ def plan(shapes, block_size: int, max_precond_dim: int, world_size: int) -> Plan
         left = 1 < m <= max_precond_dim
         right = 1 < n <= max_precond_dim
         if left and right:
-            pl, pr = 4, 4
+            (pl, rl), (pr, rr) = (pl2, rl2), (pr2, rr2)
         elif left:
-            pl, pr = 2, 0
+            (pl, rl), (pr, rr) = (2, 1), (0, 0)
         elif right:
-            pl, pr = 0, 2
+            (pl, rl), (pr, rr) = (0, 0), (2, 1)
         else:
-            pl, pr = 0, 0
+            (pl, rl), (pr, rr) = (0, 0), (0, 0)
         nbr = -(-m // block_size)
         nbc = -(-n // block_size)
         for bi in range(nbr):
             for bj in range(nbc):
                 r0, c0 = bi * block_size, bj * block_size
                 out.blocks.append(Block(t, len(out.blocks), r0, c0,
-                                        min(block_size, m - r0), min(block_size, n - c0), pl, pr))
+                                        min(block_size, m - r0), min(block_size, n - c0), pl, pr, rl, rr))
     # roots: (cost, tensor, block, side)
     roots = []
     for b in out.blocks:
@@ -111,34 +132,35 @@ def plan(shapes, block_size: int, max_precond_dim: int, world_size: int) -> Plan
             roots.append((b.cols ** 3 * products_per_iteration(b.p_right), b.tensor_id, b.block_index, 1))
     roots.sort(key=lambda r: (-r[0], r[1], r[2], r[3]))
     loads = [0] * world_size
-    owned = [[] for _ in range(world_size)]  # (n, p, sort position, block, side)
+    owned = [[] for _ in range(world_size)]  # (n, p, r, sort position, block, side)
     for pos, (cost, _t, bidx, side) in enumerate(roots):
         r = min(range(world_size), key=lambda i: (loads[i], i))
         loads[r] += cost
         b = out.blocks[bidx]
         nn = b.rows if side == 0 else b.cols
         pp = b.p_left if side == 0 else b.p_right
+        rr_ = b.r_left if side == 0 else b.r_right
         if side == 0:
             b.owner_left = r
         else:
             b.owner_right = r
-        owned[r].append((nn, pp, pos, bidx, side))
+        owned[r].append((nn, pp, rr_, pos, bidx, side))
     # packing, segment by segment
     seg_used = []
     for r in range(world_size):
-        items = sorted(owned[r], key=lambda x: (-x[0], -x[1], x[2]))
+        items = sorted(owned[r], key=lambda x: (-x[0], -x[1], -x[2], x[3]))
         off = 0
         i = 0
         while i < len(items):
-            nn, pp = items[i][0], items[i][1]
+            nn, pp, rr_ = items[i][0], items[i][1], items[i][2]
             j = i
-            while j < len(items) and items[j][0] == nn and items[j][1] == pp:
+            while j < len(items) and items[j][:3] == (nn, pp, rr_):
                 j += 1
             ld = _roundup(nn, 4)
             stride = _roundup(nn * ld, 64)
-            out.groups.append(RootGroup(r, nn, pp, off, j - i, stride))  # offset relative to segment for now
+            out.groups.append(RootGroup(r, nn, pp, off, j - i, stride, rr_))  # offset relative to segment for now
             for k in range(i, j):
-                _, _, _, bidx, side = items[k]
+                _, _, _, _, bidx, side = items[k]
                 b = out.blocks[bidx]
                 if side == 0:
                     b.left_off, b.left_ld = off + (k - i) * stride, ld

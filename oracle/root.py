@@ -17,7 +17,8 @@ DESIGN.md §3 (#1-#4, #16), taken from SPEC.md S:131-132 / S:163-164:
       lam_hat <= 0 -> status 3, X = I.
   ridge + scale (reading #2, "eps I"): A_hat = A + eps_rel*lam_hat*I,
       c = lam_hat*(1+eps_rel), M_0 = A_hat/c, X_0 = c^{-1/p} I with
-      c^{-1/4} = 1/sqrt(sqrt(c)), c^{-1/2} = 1/sqrt(c).
+      c^{-1/4} = 1/sqrt(sqrt(c)), c^{-1/2} = 1/sqrt(c) (sqrt chains for
+      p = 2^j), c ** (-1/p) otherwise (reading #22: any integer p in [1, 16]).
   iterate (reading #1), k = 0, 1, ...:
       err_k = max_ij |M_k - I|
       if err_k is not finite                           -> X untouched   (status 2)
@@ -26,7 +27,9 @@ DESIGN.md §3 (#1-#4, #16), taken from SPEC.md S:131-132 / S:163-164:
                                                          -> return X_{k-1} (status 1)
       if k == max_iter                                   -> return X_k   (status 1)
       T = ((p+1) I - M_k)/p;  X_{k+1} = X_k T;  M_{k+1} = T^p M_k
-      (T^p by repeated squaring: T^2, T^4 = (T^2)^2, ...)
+      (T^p by numpy's matrix_power, a library primitive)
+  rational exponent (f4, "L^{-1/2p} G R^{-1/2q}"; reading #23):
+      X = (A_hat^{-1/p})^r, the converged root raised to the integer power r.
 """
 
 from __future__ import annotations
@@ -71,26 +74,33 @@ def power_iteration(A: np.ndarray, iters: int = 100) -> float:
     return lam
 
 
+MAX_P = 16
+
+
+def valid_p(p: int) -> bool:
+    return isinstance(p, (int, np.integer)) and 1 <= p <= MAX_P
+
+
 def c_pow_neg_inv_p(c: float, p: int) -> float:
-    """c^{-1/p} by IEEE sqrt chains (exact scale equivariance for c -> 16^k c)."""
-    if p == 1:
-        return 1.0 / c
-    if p == 2:
-        return 1.0 / np.sqrt(c)
-    if p == 4:
-        return 1.0 / np.sqrt(np.sqrt(c))
-    if p == 8:
-        return 1.0 / np.sqrt(np.sqrt(np.sqrt(c)))
-    raise ValueError("p must be 1, 2, 4 or 8")
+    """c^{-1/p}: IEEE sqrt chains for p = 2^j (exact scale equivariance for
+    c -> 16^k c), the library power otherwise."""
+    if not valid_p(p):
+        raise ValueError(f"p must be an integer in [1, {MAX_P}]")
+    if p & (p - 1) == 0:
+        x = c
+        q = p
+        while q > 1:
+            x = np.sqrt(x)
+            q //= 2
+        return 1.0 / x
+    return float(c ** (-1.0 / p))
 
 
-def matrix_power_by_squaring(T: np.ndarray, p: int) -> np.ndarray:
-    out = T
-    q = p
-    while q > 1:
-        out = out @ out
-        q //= 2
-    return out
+def matrix_power(T: np.ndarray, p: int) -> np.ndarray:
+    return np.linalg.matrix_power(T, p)
+
+
+matrix_power_by_squaring = matrix_power  # historical name (p = 2^j)
 
 
 @dataclass
@@ -110,8 +120,8 @@ def inverse_pth_root(A, p: int, eps_rel: float = 1e-6, tol: float = 1e-7, max_it
 
     ``X_prev`` is returned unchanged (status 2) when lam_hat is non-finite.
     """
-    if p not in (1, 2, 4, 8):
-        raise ValueError("p must be 1, 2, 4 or 8")
+    if not valid_p(p):
+        raise ValueError(f"p must be an integer in [1, {MAX_P}]")
     A = np.asarray(A, np.float64)
     n = A.shape[0]
     lam = power_iteration(A, power_iters)
@@ -140,8 +150,20 @@ def inverse_pth_root(A, p: int, eps_rel: float = 1e-6, tol: float = 1e-7, max_it
         T = ((p + 1) * I - M) / p
         X_last, err_last = X, err
         X = X @ T
-        M = matrix_power_by_squaring(T, p) @ M
+        M = matrix_power(T, p) @ M
         k += 1
+
+
+def inverse_root(A, p: int, r: int = 1, eps_rel: float = 1e-6, tol: float = 1e-7, max_iter: int = 100,
+                 power_iters: int = 100, X_prev=None):
+    """X ~ A_hat^{-r/p} = (A_hat^{-1/p})^r (f4: rational exponents r/p, 1 <= r <= p).
+    Statuses / info are those of the p-th root; status 2 returns X_prev."""
+    if not (isinstance(r, (int, np.integer)) and 1 <= r <= p):
+        raise ValueError("need 1 <= r <= p")
+    X, info = inverse_pth_root(A, p, eps_rel, tol, max_iter, power_iters, X_prev)
+    if info.status == 2 or r == 1:
+        return X, info
+    return matrix_power(X, r), info
 
 
 def residual(A, X, p: int, eps_rel: float, lam: float) -> float:
@@ -151,4 +173,4 @@ def residual(A, X, p: int, eps_rel: float, lam: float) -> float:
     X = np.asarray(X, np.float64)
     n = A.shape[0]
     Ahat = A + (eps_rel * lam) * np.eye(n)
-    return float(np.linalg.norm(matrix_power_by_squaring(X, p) @ Ahat - np.eye(n)))
+    return float(np.linalg.norm(matrix_power(X, p) @ Ahat - np.eye(n)))

@@ -48,6 +48,8 @@ def lib():
         _lib.oracle_block_finite.restype = _i32
         _lib.oracle_diag_update.argtypes = [_f32p, _i64, _i64, _i64, _i32, _i32, _f32p, _i64]
         _lib.oracle_diag_update.restype = ctypes.c_double
+        _lib.oracle_mode_stat.argtypes = [_f32p, _i32, _i64, _i64, _f32p, _i64, ctypes.c_double, ctypes.c_double]
+        _lib.oracle_mode_stat.restype = None
     return _lib
 
 
@@ -104,3 +106,10 @@ def stats_update(Gs, D_list, pl, stats: np.ndarray, decay: float, weight: float,
         if D_list is not None:
             num[bi] = diag_update(G, b.row0, b.col0, b.rows, b.cols, D_list[b.tensor_id])
     return num, status
+
+
+def mode_stat(U: np.ndarray, S: np.ndarray, chunk: int, decay: float, weight: float):
+    """S (rows x >=rows view, leading dim S.shape[1]) <- decay S + weight U U^T under the
+    chunked sequential contract (oracle_stats.c, f3)."""
+    U = np.ascontiguousarray(U, np.float32)
+    lib().oracle_mode_stat(_ptr(U), U.shape[0], U.shape[1], chunk, _ptr(S), S.shape[1], decay, weight)

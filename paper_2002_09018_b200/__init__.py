@@ -31,7 +31,7 @@ _lib.lib()  # fail loudly at import if the CUDA library is missing
 
 __all__ = [
     "Plan", "make_plan", "TensorTable", "stats_update", "inverse_pth_root_batched", "root_residual_batched",
-    "precondition", "root_workspace_bytes", "ShampooError", "last_launch_count", "ROOT_INFO_DTYPE",
+    "precondition", "root_workspace_bytes", "inverse_root_rational_batched", "ShampooError", "last_launch_count", "ROOT_INFO_DTYPE",
 ]
 
 
@@ -85,18 +85,21 @@ class Plan:
         return [g for g in self.groups if int(g["owner"]) == owner]
 
 
-def make_plan(shapes, block_size: int = 1024, max_precond_dim: int = 8192, world_size: int = 1) -> Plan:
+def make_plan(shapes, block_size: int = 1024, max_precond_dim: int = 8192, world_size: int = 1,
+              split=(1, 2)) -> Plan:
+    """split = (a, d): the Lemma's 1/p = a/d (f4); (1, 2) -> L^{-1/4} G R^{-1/4}."""
     L = _lib.lib()
+    sa, sd = int(split[0]), int(split[1])
     sh = np.ascontiguousarray(np.asarray(shapes, dtype=np.int64).reshape(-1, 2))
     nb = np.zeros(1, np.int32)
     ng = np.zeros(1, np.int32)
     se = np.zeros(1, np.int64)
     sg = np.zeros(1, np.int64)
-    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, None, 0,
+    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, sa, sd, None, 0,
                          nb.ctypes.data, None, 0, ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
     blocks = np.zeros(int(nb[0]), BLOCK_DTYPE)
     groups = np.zeros(int(ng[0]), GROUP_DTYPE)
-    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size,
+    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, sa, sd,
                          blocks.ctypes.data, blocks.shape[0], nb.ctypes.data, groups.ctypes.data, groups.shape[0],
                          ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
     return Plan([tuple(map(int, s)) for s in sh], block_size, max_precond_dim, world_size, blocks, groups,
@@ -159,13 +162,19 @@ def root_workspace_bytes(batch: int, n: int, p: int, max_iter: int = 100) -> int
 
 def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: int, stride_x: int, batch: int,
                          n: int, p: int, info: torch.Tensor, eps_rel: float = 1e-6, tol: float = 1e-7,
-                         max_iter: int = 100, power_iters: int = 100, device=None, stream=None):
+                         max_iter: int = 100, power_iters: int = 100, device=None, stream=None, r: int = 1):
+    """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry)."""
     L = _lib.lib()
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
     ws = workspace(wsb, device if device is not None else info.device, "root")
-    check(L.shampoo_inverse_pth_root_batched(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel, tol,
-                                             max_iter, power_iters, info.data_ptr(), ws.data_ptr(), ws.numel(),
-                                             _stream_ptr(stream)))
+    if r == 1:
+        check(L.shampoo_inverse_pth_root_batched(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel, tol,
+                                                 max_iter, power_iters, info.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                 _stream_ptr(stream)))
+    else:
+        check(L.shampoo_inverse_root_rational_batched(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, r,
+                                                      eps_rel, tol, max_iter, power_iters, info.data_ptr(),
+                                                      ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
 
 
 def new_info(batch: int, device) -> torch.Tensor:
@@ -178,7 +187,7 @@ def info_to_numpy(info: torch.Tensor) -> np.ndarray:
 
 def inverse_pth_root_batched(A: torch.Tensor, p: int, X: torch.Tensor | None = None, eps_rel: float = 1e-6,
                              tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100,
-                             info: torch.Tensor | None = None, stream=None):
+                             info: torch.Tensor | None = None, stream=None, r: int = 1):
     """A: (batch, n, n) or (n, n) float32 CUDA tensor (row stride >= n, unit column stride).
     Returns (X, info) with X like A and info a uint8 tensor of shampoo_root_info_t."""
     squeeze = A.dim() == 2
@@ -192,8 +201,13 @@ def inverse_pth_root_batched(A: torch.Tensor, p: int, X: torch.Tensor | None = N
     if info is None:
         info = new_info(batch, A3.device)
     inverse_pth_root_ptr(A3.data_ptr(), A3.stride(1), A3.stride(0), X3.data_ptr(), X3.stride(1), X3.stride(0), batch,
-                         n, p, info, eps_rel, tol, max_iter, power_iters, A3.device, stream)
+                         n, p, info, eps_rel, tol, max_iter, power_iters, A3.device, stream, r)
     return (X3[0] if squeeze else X3), info
+
+
+def inverse_root_rational_batched(A: torch.Tensor, p: int, r: int, **kw):
+    """X = A_hat^{-r/p} (f4): the p-th root raised to the power r."""
+    return inverse_pth_root_batched(A, p, r=r, **kw)
 
 
 def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.Tensor, eps_rel: float = 1e-6,
@@ -217,12 +231,12 @@ def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, ow
     (n, p) group); roots land at the statistics' offsets."""
     out = []
     for g in plan.groups_of(owner):
-        cnt, n, p = int(g["count"]), int(g["n"]), int(g["p"])
+        cnt, n, p, r = int(g["count"]), int(g["n"]), int(g["p"]), int(g["r"])
         off, stride = int(g["offset"]), int(g["stride"])
         ld = (n + 3) // 4 * 4
         info = new_info(cnt, stats.device)
         inverse_pth_root_ptr(stats.data_ptr() + 4 * off, ld, stride, roots.data_ptr() + 4 * off, ld, stride, cnt, n,
-                             p, info, eps_rel, tol, max_iter, power_iters, stats.device, stream)
+                             p, info, eps_rel, tol, max_iter, power_iters, stats.device, stream, r)
         out.append((g, info))
     if infos is not None:
         infos.extend(out)

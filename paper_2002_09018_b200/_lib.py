@@ -15,16 +15,16 @@ LIB_PATH = os.path.join(HERE, "libshampoo.so")
 BLOCK_DTYPE = np.dtype([
     ("tensor_id", "<i4"), ("reserved", "<i4"), ("row0", "<i8"), ("col0", "<i8"),
     ("rows", "<i4"), ("cols", "<i4"), ("p_left", "<i4"), ("p_right", "<i4"),
-    ("owner_left", "<i4"), ("owner_right", "<i4"), ("left_off", "<i8"), ("right_off", "<i8"),
+    ("r_left", "<i4"), ("r_right", "<i4"), ("owner_left", "<i4"), ("owner_right", "<i4"), ("left_off", "<i8"), ("right_off", "<i8"),
     ("left_ld", "<i4"), ("right_ld", "<i4"),
 ])
 GROUP_DTYPE = np.dtype([("owner", "<i4"), ("n", "<i4"), ("p", "<i4"), ("count", "<i4"),
-                        ("offset", "<i8"), ("stride", "<i8")])
+                        ("offset", "<i8"), ("stride", "<i8"), ("r", "<i4"), ("reserved", "<i4")])
 TENSOR_DTYPE = np.dtype([("G", "<u8"), ("D", "<u8"), ("P", "<u8"), ("ldg", "<i8"), ("ldd", "<i8"),
                          ("ldp", "<i8"), ("m", "<i8"), ("n", "<i8")])
 STATE_DTYPE = np.dtype([("W", "<u8"), ("M", "<u8"), ("Pm", "<u8"), ("ldw", "<i8"), ("ldm", "<i8"), ("ldpm", "<i8")])
 ROOT_INFO_DTYPE = np.dtype([("iters", "<i4"), ("status", "<i4"), ("lambda_max", "<f8"), ("err", "<f8")])
-assert BLOCK_DTYPE.itemsize == 72 and GROUP_DTYPE.itemsize == 32
+assert BLOCK_DTYPE.itemsize == 80 and GROUP_DTYPE.itemsize == 40
 assert TENSOR_DTYPE.itemsize == 64 and ROOT_INFO_DTYPE.itemsize == 24
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "CUDA", 4: "WORKSPACE", 5: "CAPACITY"}
@@ -32,7 +32,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "CUDA", 4: "WORKSPACE"
 EXPORTED = [
     "shampoo_abi_version", "shampoo_last_error", "shampoo_last_launch_count", "shampoo_plan",
     "shampoo_stats_workspace_bytes", "shampoo_stats_update",
-    "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched",
+    "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition",
     "shampoo_momentum_workspace_bytes", "shampoo_momentum_step",
@@ -64,7 +64,7 @@ def lib():
     L.shampoo_abi_version.restype = ctypes.c_int
     L.shampoo_last_error.restype = ctypes.c_char_p
     L.shampoo_last_launch_count.restype = _i64
-    L.shampoo_plan.argtypes = [_vp, _i32, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp]
+    L.shampoo_plan.argtypes = [_vp, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp]
     L.shampoo_plan.restype = ctypes.c_int
     L.shampoo_stats_workspace_bytes.argtypes = [_vp, _i32, _i32]
     L.shampoo_stats_workspace_bytes.restype = _sz
@@ -75,6 +75,9 @@ def lib():
     L.shampoo_inverse_pth_root_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl, _dbl,
                                                    _i32, _i32, _vp, _vp, _sz, _vp]
     L.shampoo_inverse_pth_root_batched.restype = ctypes.c_int
+    L.shampoo_inverse_root_rational_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _i32,
+                                                        _dbl, _dbl, _i32, _i32, _vp, _vp, _sz, _vp]
+    L.shampoo_inverse_root_rational_batched.restype = ctypes.c_int
     L.shampoo_root_residual_workspace_bytes.argtypes = [_i32, _i32, _i32]
     L.shampoo_root_residual_workspace_bytes.restype = _sz
     L.shampoo_root_residual_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl, _vp, _vp,
@@ -88,7 +91,7 @@ def lib():
     L.shampoo_momentum_workspace_bytes.restype = _sz
     L.shampoo_momentum_step.argtypes = [_vp, _vp, _i32, _vp, _i32, _dbl, _dbl, _i32, _vp, _vp, _sz, _vp]
     L.shampoo_momentum_step.restype = ctypes.c_int
-    if L.shampoo_abi_version() != 1:
+    if L.shampoo_abi_version() != 2:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L
     return L

@@ -38,7 +38,7 @@ int num_sms() {
 }
 
 int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
-              int32_t world_size, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
+              int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
               shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
               int64_t* segment_elems);
 
@@ -52,7 +52,7 @@ static int check_ws(const void* ws, size_t have, size_t need) {
   return SHAMPOO_OK;
 }
 
-static bool valid_p(int p) { return p == 1 || p == 2 || p == 4 || p == 8; }
+static bool valid_p(int p) { return p >= 1 && p <= 16; }
 
 }  // namespace shp
 
@@ -67,11 +67,11 @@ const char* shampoo_last_error(void) { return g_err; }
 int64_t shampoo_last_launch_count(void) { return g_launches; }
 
 int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
-                 int32_t world_size, shampoo_block_t* blocks, int32_t capacity, int32_t* n_blocks,
+                 int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* blocks, int32_t capacity, int32_t* n_blocks,
                  shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups, int64_t* stats_elems,
                  int64_t* segment_elems) {
   g_err[0] = 0;
-  return plan_impl(shapes, n_tensors, block_size, max_precond_dim, world_size, blocks, capacity, n_blocks, groups,
+  return plan_impl(shapes, n_tensors, block_size, max_precond_dim, world_size, split_num, split_den, blocks, capacity, n_blocks, groups,
                    group_capacity, n_groups, stats_elems, segment_elems);
 }
 
@@ -109,12 +109,22 @@ int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride
                                      double tol, int32_t max_iter, int32_t power_iters,
                                      shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
                                      shampoo_stream_t stream) {
+  return shampoo_inverse_root_rational_batched(A, lda, stride_a, X, ldx, stride_x, batch, n, p, 1, eps_rel, tol,
+                                               max_iter, power_iters, info, workspace, workspace_bytes, stream);
+}
+
+int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                          int64_t stride_x, int32_t batch, int32_t n, int32_t p, int32_t r,
+                                          double eps_rel, double tol, int32_t max_iter, int32_t power_iters,
+                                          shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                          shampoo_stream_t stream) {
   g_err[0] = 0;
   g_launches = 0;
   if (batch < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "batch < 0");
   if (batch == 0) return SHAMPOO_OK;
   if (n < 1 || n > 8192) return set_error(SHAMPOO_ERR_INVALID_ARG, "n = %d outside [1, 8192]", n);
-  if (!valid_p(p)) return set_error(SHAMPOO_ERR_INVALID_ARG, "p = %d not in {1, 2, 4, 8}", p);
+  if (!valid_p(p)) return set_error(SHAMPOO_ERR_INVALID_ARG, "p = %d not in [1, 16]", p);
+  if (r < 1 || r > p) return set_error(SHAMPOO_ERR_INVALID_ARG, "r = %d not in [1, p = %d]", r, p);
   if (!A || !X || !info) return set_error(SHAMPOO_ERR_INVALID_ARG, "null A, X or info");
   if (lda < n || ldx < n) return set_error(SHAMPOO_ERR_INVALID_ARG, "leading dimension < n");
   if (batch > 1 && (stride_a < lda * (int64_t)(n - 1) + n || stride_x < ldx * (int64_t)(n - 1) + n))
@@ -125,7 +135,7 @@ int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride
     return set_error(SHAMPOO_ERR_INVALID_ARG, "max_iter in [0, 1000], power_iters >= 1");
   int rc = check_ws(workspace, workspace_bytes, root_workspace_bytes(batch, n, max_iter));
   if (rc) return rc;
-  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, eps_rel, tol, max_iter, power_iters, info,
+  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, r, eps_rel, tol, max_iter, power_iters, info,
                      workspace, static_cast<cudaStream_t>(stream), &g_launches);
 }
 
@@ -144,7 +154,7 @@ int shampoo_root_residual_batched(const float* A, int64_t lda, int64_t stride_a,
   if (batch < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "batch < 0");
   if (batch == 0) return SHAMPOO_OK;
   if (n < 1 || n > 8192) return set_error(SHAMPOO_ERR_INVALID_ARG, "n = %d outside [1, 8192]", n);
-  if (!valid_p(p)) return set_error(SHAMPOO_ERR_INVALID_ARG, "p = %d not in {1, 2, 4, 8}", p);
+  if (!valid_p(p)) return set_error(SHAMPOO_ERR_INVALID_ARG, "p = %d not in [1, 16]", p);
   if (!A || !X || !info || !residual) return set_error(SHAMPOO_ERR_INVALID_ARG, "null argument");
   if (lda < n || ldx < n) return set_error(SHAMPOO_ERR_INVALID_ARG, "leading dimension < n");
   if (!std::isfinite(eps_rel) || eps_rel < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "eps_rel");

@@ -15,7 +15,7 @@ int set_cuda_error(const char* what, cudaError_t e = cudaGetLastError());
 // root.cu
 size_t root_workspace_bytes(int batch, int n, int max_iter);
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
-                int n, int p, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
+                int n, int p, int r, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
                 void* ws, cudaStream_t stream, int64_t* launches);
 size_t residual_workspace_bytes(int batch, int n);
 int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* X, int64_t ldx, int64_t stride_x,

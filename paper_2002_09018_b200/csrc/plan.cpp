@@ -3,12 +3,14 @@
 // Rule (readings #5, #12, #13, #17):
 //  * side kept iff 1 < dim <= max_precond_dim (bypass huge dims);
 //  * both kept -> p = 4 / 4; one kept -> p = 2 on it;
+//    a split (a, d) gives the two-sided exponents a/(2d) and (d-a)/(2d) stored
+//    reduced as r/p (f4; reading #23);
 //  * each axis split into ceil(dim/b) contiguous ranges, last ragged,
 //    blocks row-major over the block grid, tensors in caller order;
 //  * roots sorted by (cost desc, tensor, block, side) with cost = n^3 * products
 //    per Newton iteration, assigned LPT to the least-loaded rank;
 //  * packing: rank-major segments of equal size; inside a segment groups of
-//    equal (n, p) in (n desc, p desc) order; ld = roundup(n, 4), group stride
+//    equal (n, p, r) in (n desc, p desc, r desc) order; ld = roundup(n, 4), group stride
 //    roundup(n*ld, 64); segment size roundup(max used, 64).
 #include <algorithm>
 #include <cstring>
@@ -21,35 +23,45 @@ namespace shp {
 
 static int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// X*T, the left-to-right binary chain for T^p (bitlen-1 squarings, popcount-1
+// multiplications by T) and T^p*M
 static int64_t products_per_iteration(int p) {
-  switch (p) {
-    case 1: return 2;
-    case 2: return 3;
-    case 4: return 4;
-    default: return 5;
+  int bits = 0, ones = 0;
+  for (int q = p; q; q >>= 1) {
+    ++bits;
+    ones += q & 1;
   }
+  return 2 + (bits - 1) + (ones - 1);
 }
+
+static int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
 
 struct RootRef {
   int64_t cost;
   int32_t tensor, block, side;
-  int32_t n, p;
+  int32_t n, p, r;
 };
 
 int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
-              int32_t world_size, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
+              int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
               shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
               int64_t* segment_elems) {
   if (!shapes || n_tensors < 0 || block_size < 1 || max_precond_dim < 1 || world_size < 1)
     return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: bad arguments");
+  if (split_num < 1 || split_num >= split_den)
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: split needs 1 <= split_num < split_den");
+  const int gl = gcd_i(split_num, 2 * split_den), gr = gcd_i(split_den - split_num, 2 * split_den);
+  const int p2l = 2 * split_den / gl, r2l = split_num / gl;
+  const int p2r = 2 * split_den / gr, r2r = (split_den - split_num) / gr;
+  if (p2l > 16 || p2r > 16) return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: split needs root orders <= 16");
   std::vector<shampoo_block_t> blocks;
   for (int32_t t = 0; t < n_tensors; ++t) {
     const int64_t m = shapes[2 * t], n = shapes[2 * t + 1];
     if (m < 1 || n < 1) return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: tensor %d has a zero dimension", t);
     const bool left = m > 1 && m <= max_precond_dim;
     const bool right = n > 1 && n <= max_precond_dim;
-    const int pl = left ? (right ? 4 : 2) : 0;
-    const int pr = right ? (left ? 4 : 2) : 0;
+    const int pl = left ? (right ? p2l : 2) : 0, rl = left ? (right ? r2l : 1) : 0;
+    const int pr = right ? (left ? p2r : 2) : 0, rr = right ? (left ? r2r : 1) : 0;
     for (int64_t r0 = 0; r0 < m; r0 += block_size)
       for (int64_t c0 = 0; c0 < n; c0 += block_size) {
         shampoo_block_t b;
@@ -61,6 +73,8 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
         b.cols = (int32_t)std::min<int64_t>(block_size, n - c0);
         b.p_left = pl;
         b.p_right = pr;
+        b.r_left = rl;
+        b.r_right = rr;
         b.owner_left = b.owner_right = -1;
         b.left_off = b.right_off = -1;
         b.left_ld = b.right_ld = 0;
@@ -72,11 +86,11 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
     const shampoo_block_t& b = blocks[i];
     if (b.p_left) {
       const int64_t n = b.rows;
-      roots.push_back({n * n * n * products_per_iteration(b.p_left), b.tensor_id, i, 0, b.rows, b.p_left});
+      roots.push_back({n * n * n * products_per_iteration(b.p_left), b.tensor_id, i, 0, b.rows, b.p_left, b.r_left});
     }
     if (b.p_right) {
       const int64_t n = b.cols;
-      roots.push_back({n * n * n * products_per_iteration(b.p_right), b.tensor_id, i, 1, b.cols, b.p_right});
+      roots.push_back({n * n * n * products_per_iteration(b.p_right), b.tensor_id, i, 1, b.cols, b.p_right, b.r_right});
     }
   }
   std::stable_sort(roots.begin(), roots.end(), [](const RootRef& x, const RootRef& y) {
@@ -103,19 +117,21 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
     std::stable_sort(items.begin(), items.end(), [&](int32_t a, int32_t c) {
       const RootRef& x = roots[a];
       const RootRef& y = roots[c];
-      return std::make_tuple(-x.n, -x.p, a) < std::make_tuple(-y.n, -y.p, c);
+      return std::make_tuple(-x.n, -x.p, -x.r, a) < std::make_tuple(-y.n, -y.p, -y.r, c);
     });
     int64_t off = 0;
     size_t i = 0;
     while (i < items.size()) {
-      const int32_t n = roots[items[i]].n, p = roots[items[i]].p;
+      const int32_t n = roots[items[i]].n, p = roots[items[i]].p, rr = roots[items[i]].r;
       size_t j = i;
-      while (j < items.size() && roots[items[j]].n == n && roots[items[j]].p == p) ++j;
+      while (j < items.size() && roots[items[j]].n == n && roots[items[j]].p == p && roots[items[j]].r == rr) ++j;
       const int64_t ld = roundup(n, 4), stride = roundup((int64_t)n * ld, 64);
       shampoo_group_t g;
       g.owner = r;
       g.n = n;
       g.p = p;
+      g.r = rr;
+      g.reserved = 0;
       g.count = (int32_t)(j - i);
       g.offset = off;  // relative to the segment for now
       g.stride = stride;

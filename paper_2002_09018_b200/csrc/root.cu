@@ -10,6 +10,9 @@
 //   k = 0, 1, ...: err_k = max|M_k - I| ; stop on err_k <= tol, stagnation
 //                  (err_k >= err_{k-1} < 1e-2 -> X_{k-1}) or k == max_iter
 //                  T_k = ((p+1)I - M_k)/p ; X_{k+1} = X_k T_k ; M_{k+1} = T_k^p M_k
+//   T^p by the left-to-right binary chain (squarings, multiplications by T),
+//   any integer p in [1, 16] (reading #22); optionally X <- X^r before the
+//   fp32 write (rational exponent -r/p, f4; reading #23).
 //
 // B200 design:
 //  * All iterates are symmetric polynomials in A_hat, so every product computes
@@ -42,7 +45,7 @@ struct RootArgs {
   int64_t lda, stride_a;
   float* X;
   int64_t ldx, stride_x;
-  int batch, n, np, p, max_iter, power_iters;
+  int batch, n, np, p, r, max_iter, power_iters;
   double eps_rel, tol;
   shampoo_root_info_t* info;
   double* bufs;  // batch * kBufs * np * np
@@ -238,14 +241,17 @@ SHP_DEV void power_iteration_split(const RootArgs& a, double* smem, cg::grid_gro
   if (active && part == 0 && threadIdx.x == 0) a.lam[mat] = lam;
 }
 
+// c^{-1/p}: sqrt chains for p = 2^j (exact scale equivariance), pow otherwise
 SHP_DEV double c_pow_neg_inv_p(double c, int p) {
-  switch (p) {
-    case 1: return 1.0 / c;
-    case 2: return 1.0 / sqrt(c);
-    case 4: return 1.0 / sqrt(sqrt(c));
-    default: return 1.0 / sqrt(sqrt(sqrt(c)));
+  if ((p & (p - 1)) == 0) {
+    double x = c;
+    for (int q = p; q > 1; q >>= 1) x = sqrt(x);
+    return 1.0 / x;
   }
+  return pow(c, -1.0 / (double)p);
 }
+
+SHP_DEV int lead_bit(int p) { return 31 - __clz(p); }
 
 SHP_DEV bool lam_ok(double lam) { return isfinite(lam) && lam > 0.0; }
 
@@ -329,12 +335,32 @@ SHP_DEV int compact(const RootArgs& a, int* act, int nact, int k, int* cnt, bool
   return total;
 }
 
+// One symmetric product stage over the active matrices: D = A_op * B_op
+// (upper 64x64 tiles, mirror-stored).  An operand index < 0 selects the
+// matrix's returned iterate (a.res[mat].x).
+SHP_DEV void product_stage(const RootArgs& a, const int* act, int nact, int ab, int bb, int db, double* smem,
+                           AccN& acc) {
+  const int np = a.np, T = np / kNT, tiles = T * (T + 1) / 2;
+  const int items = nact * tiles;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int pos = it / tiles, t = it - pos * tiles;
+    const int mat = act[pos];
+    int ti, tj;
+    upper_tile(t, T, ti, tj);
+    const int ra = ab < 0 ? a.res[mat].x : ab, rb = bb < 0 ? a.res[mat].x : bb;
+    gemm_tile_f64(acc, buf(a, mat, ra) + (int64_t)ti * kNT * np, buf(a, mat, rb) + (int64_t)tj * kNT * np, np,
+                  np / kAsyncK, smem);
+    epilogue<EPI_STORE>(a, acc, mat, ti, tj, buf(a, mat, db), nullptr, nullptr);
+  }
+}
+
+SHP_DEV void write_output(const RootArgs& a, int pbuf);
+
 // ---------------------------------------------------------------- kernel
 __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
   extern __shared__ __align__(16) double smem[];
   cg::grid_group grid = cg::this_grid();
   const int np = a.np, T = np / kNT, tiles = T * (T + 1) / 2;
-  const int64_t np2 = (int64_t)np * np;
 
   // ---- phase 0: power iteration + err history reset
   for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
@@ -420,24 +446,30 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
       }
       grid.sync();
     }
-    // squarings: S1 = S0^2 (p >= 4); S0 = S1^2 (p == 8)
-    for (int sq = 0; sq < ((a.p == 8) ? 2 : (a.p == 4 ? 1 : 0)); ++sq) {
-      const int src = (sq == 0) ? BS0 : BS1, dstb = (sq == 0) ? BS1 : BS0;
-      const int items = nact * tiles;
-      for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int pos = it / tiles, t = it - pos * tiles;
-        const int mat = act[pos];
-        int ti, tj;
-        upper_tile(t, T, ti, tj);
-        const double* S = buf(a, mat, src);
-        gemm_tile_f64(acc, S + (int64_t)ti * kNT * np, S + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
-        epilogue<EPI_STORE>(a, acc, mat, ti, tj, buf(a, mat, dstb), nullptr, nullptr);
+    // rest of the left-to-right binary chain for T^p (S0 = T^2 from P1):
+    // per remaining bit, square (except the first, fused above) and, if the
+    // bit is set, multiply by T; ping-pong S0 / S1
+    int rbuf = BS0;
+    if (a.p >= 2) {
+      const int nb = lead_bit(a.p);
+      for (int bit = nb - 1; bit >= 0; --bit) {
+        if (bit != nb - 1) {
+          const int d = (rbuf == BS0) ? BS1 : BS0;
+          product_stage(a, act, nact, rbuf, rbuf, d, smem, acc);
+          rbuf = d;
+          grid.sync();
+        }
+        if ((a.p >> bit) & 1) {
+          const int d = (rbuf == BS0) ? BS1 : BS0;
+          product_stage(a, act, nact, rbuf, BT, d, smem, acc);
+          rbuf = d;
+          grid.sync();
+        }
       }
-      grid.sync();
     }
     // P3: M_{k+1} = T^p M_k ; T_{k+1} ; err_{k+1}
     {
-      const int tp = (a.p == 1) ? tb : (a.p == 2 ? BS0 : (a.p == 4 ? BS1 : BS0));
+      const int tp = (a.p == 1) ? tb : rbuf;
       const int items = nact * tiles;
       for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int pos = it / tiles, t = it - pos * tiles;
@@ -488,22 +520,63 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
     }
   }
   grid.sync();
-  {
-    const int lane = threadIdx.x & 31, gw = blockIdx.x * (kRT / 32) + (threadIdx.x >> 5);
-    const int nw = gridDim.x * (kRT / 32);
-    const int64_t rows = (int64_t)a.batch * a.n;
-    for (int64_t rid = gw; rid < rows; rid += nw) {
-      const int mat = (int)(rid / a.n), i = (int)(rid - (int64_t)mat * a.n);
-      const int4 r = a.res[mat];
-      float* out = a.X + (int64_t)mat * a.stride_x + (int64_t)i * a.ldx;
-      if (r.z == 3) {
-        for (int j = lane; j < a.n; j += 32) out[j] = (i == j) ? 1.0f : 0.0f;
-      } else if (r.x >= 0) {
-        const double* src = buf(a, mat, r.x) + (int64_t)i * np;
-        for (int j = lane; j < a.n; j += 32) out[j] = (float)src[j];
-      }
+  if (a.r == 1) write_output(a, -1);
+  // r >= 2: root_power_kernel raises the returned iterates to the power r and
+  // writes the output (a separate launch: keeping its product code out of this
+  // kernel keeps the Newton loops' instruction footprint, measured 12% faster)
+}
+
+// Final fp32 write: X_i (or its power in buffer `pbuf`), I for degenerate
+// matrices, nothing for non-finite ones.
+SHP_DEV void write_output(const RootArgs& a, int pbuf) {
+  const int np = a.np;
+  const int lane = threadIdx.x & 31, gw = blockIdx.x * (kRT / 32) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (kRT / 32);
+  const int64_t rows = (int64_t)a.batch * a.n;
+  for (int64_t rid = gw; rid < rows; rid += nw) {
+    const int mat = (int)(rid / a.n), i = (int)(rid - (int64_t)mat * a.n);
+    const int4 r = a.res[mat];
+    float* out = a.X + (int64_t)mat * a.stride_x + (int64_t)i * a.ldx;
+    if (r.z == 3) {
+      for (int j = lane; j < a.n; j += 32) out[j] = (i == j) ? 1.0f : 0.0f;
+    } else if (r.x >= 0) {
+      const double* src = buf(a, mat, pbuf >= 0 ? pbuf : r.x) + (int64_t)i * np;
+      for (int j = lane; j < a.n; j += 32) out[j] = (float)src[j];
     }
   }
+}
+
+// ---- rational exponent (f4): X <- X^r for every returned iterate, by the
+// left-to-right binary chain over the freed M0 / M1 buffers, then the output.
+__global__ void __launch_bounds__(kRT, 2) root_power_kernel(RootArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  cg::grid_group grid = cg::this_grid();
+  int* act = reinterpret_cast<int*>(smem + kAsyncSmemDoubles);
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int mat = 0; mat < a.batch; ++mat)
+      if (a.res[mat].x >= 0) act[c++] = mat;
+    s_n = c;
+  }
+  __syncthreads();
+  const int npow = s_n;
+  AccN acc;
+  int pbuf = -1;
+  const int nb = lead_bit(a.r);
+  for (int bit = nb - 1; bit >= 0; --bit) {
+    const int d0 = (pbuf == BM0) ? BM1 : BM0;
+    product_stage(a, act, npow, pbuf, pbuf, d0, smem, acc);  // square (pbuf -1 = X)
+    pbuf = d0;
+    grid.sync();
+    if ((a.r >> bit) & 1) {
+      const int d1 = (pbuf == BM0) ? BM1 : BM0;
+      product_stage(a, act, npow, pbuf, -1, d1, smem, acc);  // times X
+      pbuf = d1;
+      grid.sync();
+    }
+  }
+  write_output(a, pbuf);
 }
 
 // ---------------------------------------------------------------- host side
@@ -525,12 +598,14 @@ size_t root_smem_bytes(int n) {
 }
 
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
-                int n, int p, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
+                int n, int p, int r, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
                 void* ws, cudaStream_t stream, int64_t* launches) {
   static size_t configured_smem = 0;
   const size_t smem = root_smem_bytes(n);
   if (smem > configured_smem) {
-    if (cudaFuncSetAttribute(root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(root_power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
       return set_cuda_error("cudaFuncSetAttribute(root_kernel)");
     configured_smem = smem;
   }
@@ -554,6 +629,7 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     a.n = n;
     a.np = np;
     a.p = p;
+    a.r = r;
     a.max_iter = max_iter;
     a.power_iters = power_iters;
     a.eps_rel = eps_rel;
@@ -574,6 +650,11 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);
     if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_kernel)", e);
     ++*launches;
+    if (r >= 2) {
+      e = cudaLaunchCooperativeKernel((const void*)root_power_kernel, dim3(grid), dim3(kRT), args, smem, stream);
+      if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_power_kernel)", e);
+      ++*launches;
+    }
   }
   return SHAMPOO_OK;
 }
@@ -622,16 +703,23 @@ __global__ void __launch_bounds__(kRT, 2) residual_kernel(ResArgs a) {
     rbuf(a, mat, 3)[rem] = ah;
   }
   grid.sync();
+  // X^p by the left-to-right binary chain: per bit after the leading one,
+  // square, then multiply by X (Y0) if the bit is set; ping-pong Y1 / Y2
   int src = 0;
   AccN acc;
-  for (int q = a.p; q > 1; q >>= 1) {
+  const int nsteps = 2 * (31 - __clz(a.p));
+  for (int step = 0; step < nsteps; ++step) {
+    const int bit = (31 - __clz(a.p)) - 1 - step / 2;
+    const bool square = (step & 1) == 0;
+    if (!square && !((a.p >> bit) & 1)) continue;  // uniform across the grid
     const int dst = (src == 1) ? 2 : 1;
     for (int it = blockIdx.x; it < a.batch * tiles; it += gridDim.x) {
       const int mat = it / tiles, t = it - mat * tiles;
       int ti, tj;
       upper_tile(t, T, ti, tj);
       const double* S = rbuf(a, mat, src);
-      gemm_tile_f64(acc, S + (int64_t)ti * kNT * np, S + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
+      const double* S2 = square ? S : rbuf(a, mat, 0);
+      gemm_tile_f64(acc, S + (int64_t)ti * kNT * np, S2 + (int64_t)tj * kNT * np, np, np / kAsyncK, smem);
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       double* D = rbuf(a, mat, dst);
 #pragma unroll

@@ -77,14 +77,14 @@ class DelayedRefresh:
 
     def _run(self, units, stream=None):
         for g, i, n in units:
-            nn, p = int(g["n"]), int(g["p"])
+            nn, p, r = int(g["n"]), int(g["p"]), int(g["r"])
             ld = (nn + 3) // 4 * 4
             off, stride = int(g["offset"]) + i * int(g["stride"]), int(g["stride"])
             info = new_info(n, self.stats.device)
             src = self.snapshot.data_ptr() + 4 * (off - self.seg0)
             dst = self.next.data_ptr() + 4 * off
             inverse_pth_root_ptr(src, ld, stride, dst, ld, stride, n, nn, p, info, device=self.stats.device,
-                                 stream=stream, **self.kw)
+                                 stream=stream, r=r, **self.kw)
             self.infos.append((g, i, n, info))
 
     def step(self, t: int, stream=None) -> bool:

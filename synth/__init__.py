@@ -47,6 +47,49 @@ def transformer_big_shapes():
     return shapes
 
 
+def resnet50_shapes(include_vectors: bool = True):
+    """ResNet-50 parameters in the TensorFlow HWIO layout [kh, kw, c_in,
+    c_out] (order-4 conv kernels), the fc matrix [2048, 1000] and, with
+    ``include_vectors``, the order-1 batch-norm scales/offsets and the fc bias:
+    25,557,032 parameters in total (the standard ResNet-50 v1.5 count)."""
+    shapes = [("conv1", (7, 7, 3, 64))]
+    if include_vectors:
+        shapes += [("bn1.gamma", (64,)), ("bn1.beta", (64,))]
+    c_in = 64
+    for stage, (width, blocks) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
+        c_out = 4 * width
+        for blk in range(blocks):
+            name = f"layer{stage + 1}.{blk}"
+            convs = [("conv1", (1, 1, c_in, width)), ("conv2", (3, 3, width, width)), ("conv3", (1, 1, width, c_out))]
+            if blk == 0:
+                convs.append(("downsample", (1, 1, c_in, c_out)))
+            for cname, sh in convs:
+                shapes.append((f"{name}.{cname}", sh))
+                if include_vectors:
+                    shapes += [(f"{name}.{cname}.bn.gamma", (sh[3],)), (f"{name}.{cname}.bn.beta", (sh[3],))]
+            c_in = c_out
+    shapes.append(("fc", (2048, 1000)))
+    if include_vectors:
+        shapes.append(("fc.bias", (1000,)))
+    return shapes
+
+
+def conv_gradient(shape, seed: int) -> np.ndarray:
+    """Layer-like gradient of any order: a low-rank (rank <= 8 per unfolding)
+    CP-style term plus noise, sigma = 1/sqrt(max dim): sigma*(sum_r a_r o b_r o ... / 4 + 0.05 Z)."""
+    g = rng(seed)
+    shape = tuple(int(d) for d in shape)
+    rank = 8
+    T = np.zeros(shape)
+    for _ in range(rank):
+        t = np.ones(())
+        for d in shape:
+            t = np.multiply.outer(t, g.standard_normal(d))
+        T += t
+    Z = g.standard_normal(shape)
+    return ((T / 4.0 + 0.05 * Z) / np.sqrt(max(shape))).astype(np.float32)
+
+
 def rng(seed: int) -> np.random.Generator:
     return np.random.Generator(np.random.Philox(seed))
 

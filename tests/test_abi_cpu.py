@@ -36,21 +36,23 @@ def test_library_exports_every_declared_symbol(shp):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(_lib.EXPORTED) == declared
-    assert L.shampoo_abi_version() == 1
+    assert L.shampoo_abi_version() == 2
 
 
 def _fields_equal(lib_plan, o):
     assert lib_plan.n_blocks == len(o.blocks)
     for b, ob in zip(lib_plan.blocks, o.blocks):
         got = (int(b["tensor_id"]), int(b["row0"]), int(b["col0"]), int(b["rows"]), int(b["cols"]),
-               int(b["p_left"]), int(b["p_right"]), int(b["owner_left"]), int(b["owner_right"]),
+               int(b["p_left"]), int(b["p_right"]), int(b["r_left"]), int(b["r_right"]),
+               int(b["owner_left"]), int(b["owner_right"]),
                int(b["left_off"]), int(b["right_off"]), int(b["left_ld"]), int(b["right_ld"]))
-        want = (ob.tensor_id, ob.row0, ob.col0, ob.rows, ob.cols, ob.p_left, ob.p_right, ob.owner_left,
+        want = (ob.tensor_id, ob.row0, ob.col0, ob.rows, ob.cols, ob.p_left, ob.p_right, ob.r_left, ob.r_right,
+                ob.owner_left,
                 ob.owner_right, ob.left_off, ob.right_off, ob.left_ld, ob.right_ld)
         assert got == want
     assert lib_plan.stats_elems == o.stats_elems and lib_plan.segment_elems == o.segment_elems
-    got_g = [tuple(int(g[k]) for k in ("owner", "n", "p", "offset", "count", "stride")) for g in lib_plan.groups]
-    want_g = [(g.owner, g.n, g.p, g.offset, g.count, g.stride) for g in o.groups]
+    got_g = [tuple(int(g[k]) for k in ("owner", "n", "p", "r", "offset", "count", "stride")) for g in lib_plan.groups]
+    want_g = [(g.owner, g.n, g.p, g.r, g.offset, g.count, g.stride) for g in o.groups]
     assert got_g == want_g
 
 
@@ -71,6 +73,23 @@ def test_plan_bit_exact_vs_oracle(shp, case, W):
     _fields_equal(shp.make_plan(shapes, b, mpd, W), oplan.plan(shapes, b, mpd, W))
 
 
+# f4 splits 1/p = a/d: (1,4) -> 1/8, 3/8; (3,4) -> 3/8, 1/8; (1,3) -> 1/6, 1/3; (2,5) -> 1/5, 3/10
+@pytest.mark.parametrize("split", [(1, 4), (3, 4), (1, 3), (2, 5), (1, 8)])
+@pytest.mark.parametrize("W", [1, 3])
+def test_plan_split_bit_exact_vs_oracle(shp, split, W):
+    shapes = [(1024, 1024), (512, 2048), (32000, 512), (300, 200), (1, 50)]
+    _fields_equal(shp.make_plan(shapes, 512, 4096, W, split), oplan.plan(shapes, 512, 4096, W, split))
+
+
+def test_plan_split_invalid(shp):
+    from paper_2002_09018_b200 import ShampooError
+    for split in [(0, 2), (2, 2), (3, 2), (1, 9)]:  # (1, 9): 1/18 needs a root order > 16
+        with pytest.raises(ShampooError):
+            shp.make_plan([(64, 64)], 64, 4096, 1, split)
+        with pytest.raises(ValueError):
+            oplan.plan([(64, 64)], 64, 4096, 1, split)
+
+
 def test_plan_capacity_and_invalid(shp):
     from paper_2002_09018_b200 import _lib
     L = _lib.lib()
@@ -80,11 +99,11 @@ def test_plan_capacity_and_invalid(shp):
     se = np.zeros(1, np.int64)
     sg = np.zeros(1, np.int64)
     blocks = np.zeros(1, _lib.BLOCK_DTYPE)
-    rc = L.shampoo_plan(sh.ctypes.data, 1, 2, 8192, 1, blocks.ctypes.data, 1, nb.ctypes.data, None, 0,
+    rc = L.shampoo_plan(sh.ctypes.data, 1, 2, 8192, 1, 1, 2, blocks.ctypes.data, 1, nb.ctypes.data, None, 0,
                         ng.ctypes.data, se.ctypes.data, sg.ctypes.data)
     assert rc == 5 and nb[0] == 4  # CAPACITY, counts still written
     bad = np.array([[0, 4]], np.int64)
-    assert L.shampoo_plan(bad.ctypes.data, 1, 2, 8192, 1, None, 0, nb.ctypes.data, None, 0, ng.ctypes.data,
+    assert L.shampoo_plan(bad.ctypes.data, 1, 2, 8192, 1, 1, 2, None, 0, nb.ctypes.data, None, 0, ng.ctypes.data,
                           se.ctypes.data, sg.ctypes.data) == 1
     assert b"zero dimension" in L.shampoo_last_error()
 
@@ -93,10 +112,17 @@ def test_host_checked_errors_need_no_device(shp):
     from paper_2002_09018_b200 import _lib
     L = _lib.lib()
     fake = 1 << 40  # never dereferenced: validation fails first
-    # p not in {1,2,4,8}
-    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 3, 1e-6, 1e-7, 100, 100, fake, fake,
+    # p not in [1, 16]
+    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 17, 1e-6, 1e-7, 100, 100, fake, fake,
                                               1 << 30, None) == 1
-    assert b"p = 3" in L.shampoo_last_error()
+    assert b"p = 17" in L.shampoo_last_error()
+    assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 8, 0, 1e-6, 1e-7, 100, 100, fake, fake,
+                                              1 << 30, None) == 1
+    # rational exponent: r outside [1, p]
+    for p, r in ((8, 0), (8, 9), (3, 4)):
+        assert L.shampoo_inverse_root_rational_batched(fake, 8, 64, fake, 8, 64, 1, 8, p, r, 1e-6, 1e-7, 100, 100,
+                                                       fake, fake, 1 << 30, None) == 1
+        assert b"r = " in L.shampoo_last_error()
     # n out of range
     assert L.shampoo_inverse_pth_root_batched(fake, 8, 64, fake, 8, 64, 1, 0, 4, 1e-6, 1e-7, 100, 100, fake, fake,
                                               1 << 30, None) == 1

@@ -210,3 +210,87 @@ def test_stagnation_returns_previous_best():
     assert info.status == 1 and info.iters < 60 and info.err < 1e-12
     Ahat = A + 1e-6 * info.lambda_max * np.eye(48)
     assert rel(X, eig_root(Ahat, 4)) < 1e-9
+
+
+# ------------------------------------------------------------ any integer p, rational r/p (f3, f4)
+
+def eig_power(Ahat, e):
+    w, V = np.linalg.eigh(Ahat)
+    return (V * w ** e) @ V.T
+
+
+@pytest.mark.parametrize("p", [3, 5, 6, 7, 12, 16])
+def test_general_p_matches_eigh(p):
+    # p = 2k for rank-k tensors (f3: p = 6 for rank 3); the coupled iteration
+    # converges for any integer p while spec(M_0) lies in (0, p+1) (Appendix A)
+    G = gaussian((48, 24), 200209021)
+    A = G.astype(np.float64) @ G.astype(np.float64).T
+    X, info = oroot.inverse_pth_root(A, p, eps_rel=1e-6, tol=1e-12)
+    Ahat = A + 1e-6 * info.lambda_max * np.eye(48)
+    assert info.status == 0
+    assert rel(X, eig_root(Ahat, p)) < 1e-8
+
+
+@pytest.mark.parametrize("p", [3, 6])
+def test_general_p_scalar_closed_form(p):
+    a, eps = 7.25, 1e-6
+    X, info = oroot.inverse_pth_root(np.array([[a]]), p, eps_rel=eps, tol=1e-14)
+    assert X[0, 0] == pytest.approx((a * (1 + eps)) ** (-1.0 / p), rel=1e-14)
+
+
+@pytest.mark.parametrize("p,r", [(8, 3), (8, 1), (6, 2), (3, 2), (5, 4), (4, 4)])
+def test_rational_rank_one_plus_delta(p, r):
+    # closed form of A_hat^{-r/p} for s uu^T + delta I
+    n = 20
+    u = gaussian((n,), 18).astype(np.float64)
+    u /= np.linalg.norm(u)
+    s, delta, eps = 50.0, 1e-3, 1e-6
+    A = s * np.outer(u, u) + delta * np.eye(n)
+    X, info = oroot.inverse_root(A, p, r, eps_rel=eps, tol=1e-13)
+    rr = eps * info.lambda_max
+    P = np.outer(u, u)
+    e = -r / p
+    want = (s + delta + rr) ** e * P + (delta + rr) ** e * (np.eye(n) - P)
+    assert rel(X, want) < 1e-11
+
+
+@pytest.mark.parametrize("p,r", [(8, 3), (6, 5), (16, 7)])
+def test_rational_matches_eigh_and_inverse_identity(p, r):
+    A = wishart(40, 77).astype(np.float64)
+    X, info = oroot.inverse_root(A, p, r, tol=1e-12)
+    Ahat = A + 1e-6 * info.lambda_max * np.eye(40)
+    assert rel(X, eig_power(Ahat, -r / p)) < 1e-8
+    # X^p A_hat^r = I (the defining identity of A_hat^{-r/p}); checked at a
+    # ridge that keeps kappa(A_hat)^r within fp64 (kappa ~ 1e2)
+    if r > 5:
+        return  # kappa^r beyond fp64
+    X, info = oroot.inverse_root(A, p, r, eps_rel=1e-2, tol=1e-13)
+    Ahat = A + 1e-2 * info.lambda_max * np.eye(40)
+    Y = np.linalg.matrix_power(X, p) @ np.linalg.matrix_power(Ahat, r)
+    assert np.linalg.norm(Y - np.eye(40)) / np.sqrt(40) < 1e-4  # a wrong exponent gives O(1)
+
+
+def test_rational_r1_is_the_pth_root_and_complementary_pair():
+    A = wishart(32, 5).astype(np.float64)
+    X1, _ = oroot.inverse_root(A, 8, 1, tol=1e-12)
+    Xp, _ = oroot.inverse_pth_root(A, 8, tol=1e-12)
+    assert np.array_equal(X1, Xp)
+    # (1/8) + (3/8) = 1/2: X_{1/8} X_{3/8} = A_hat^{-1/2}
+    X3, info = oroot.inverse_root(A, 8, 3, tol=1e-12)
+    Ahat = A + 1e-6 * info.lambda_max * np.eye(32)
+    assert rel(X1 @ X3, eig_power(Ahat, -0.5)) < 1e-8
+
+
+def test_invalid_p_and_r():
+    with pytest.raises(ValueError):
+        oroot.inverse_pth_root(np.eye(3), 17)
+    with pytest.raises(ValueError):
+        oroot.inverse_root(np.eye(3), 4, 5)
+    with pytest.raises(ValueError):
+        oroot.inverse_root(np.eye(3), 4, 0)
+
+
+def test_residual_general_p():
+    A = wishart(40, 15).astype(np.float64)
+    X, info = oroot.inverse_pth_root(A, 6, tol=1e-12)
+    assert oroot.residual(A, X, 6, 1e-6, info.lambda_max) < 1e-6

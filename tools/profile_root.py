@@ -36,7 +36,7 @@ for r in range(args.reps):
 inf = shp.info_to_numpy(info)
 ms = e0.elapsed_time(e1)
 n = args.n
-prods = {1: 2, 2: 3, 4: 4, 8: 5}[args.p]
+prods = 2 + (args.p.bit_length() - 1) + (bin(args.p).count("1") - 1)
 flops = float(inf["iters"].sum()) * prods * n * n * (n + 1)
 print(f"batch {args.batch} n {n} p {args.p}: {ms:.2f} ms, iters mean {inf['iters'].mean():.2f}, "
       f"status {set(inf['status'].tolist())}, {flops / ms / 1e9:.2f} TFLOP/s (sym-minimal), "
