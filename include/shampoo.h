@@ -247,6 +247,81 @@ int shampoo_momentum_step(const shampoo_tensor_t* tensors, const shampoo_state_t
                           int32_t shampoo_branch, double* eta_out, void* workspace, size_t workspace_bytes,
                           shampoo_stream_t stream);
 
+/* ===================================================== f3: tensors of order 1..4
+ * The paper's method "holds for tensors of arbitrary order";
+ * per-mode Shampoo (readings #24-#26): mode i of an order-k tensor is
+ * preconditioned iff 1 < d_i <= max_precond_dim; with k' kept modes each gets
+ * the root H_i^{-1/(2k')} (exponents sum to -1/2); H_i accumulates
+ * U_i U_i^T of the mode-i unfolding of each block; P_B = B x_0 X_0 x_1 X_1 ...
+ * Every mode is blocked by block_size.  Roots are computed with
+ * shampoo_inverse_pth_root_batched over the groups of the tensor plan (the
+ * packing is the matrix plan's). */
+#define SHAMPOO_MAX_ORDER 4
+
+/* One parameter tensor (HOST array): contiguous row-major fp32 of dims[0..order-1]. */
+typedef struct {
+  const float* G; /* gradient                                   */
+  float* D;       /* diagonal AdaGrad accumulator (nullable)     */
+  float* P;       /* preconditioned-gradient output (nullable for the statistics call) */
+  int64_t dims[SHAMPOO_MAX_ORDER]; /* unused trailing entries = 1 */
+  int32_t order;                   /* 1..4                         */
+  int32_t reserved;
+} shampoo_ttensor_t;
+
+/* One block (sub-tensor) of an order-k tensor (plan output; integer, bit-exact
+ * vs oracle/tensor.py).  136 bytes.  Entries i >= order: extent 1, p 0. */
+typedef struct {
+  int32_t tensor_id, order;
+  int64_t origin[SHAMPOO_MAX_ORDER];
+  int32_t extent[SHAMPOO_MAX_ORDER];
+  int32_t p[SHAMPOO_MAX_ORDER];     /* root order of mode i (2k'), 0 = not preconditioned */
+  int32_t owner[SHAMPOO_MAX_ORDER]; /* rank that updates H_i and computes its root, -1    */
+  int32_t ld[SHAMPOO_MAX_ORDER];    /* leading dim of H_i = roundup(extent_i, 4)         */
+  int64_t off[SHAMPOO_MAX_ORDER];   /* packed offset of H_i (and its root), -1           */
+} shampoo_tblock_t;
+
+/* Plan for tensors (rule above; blocks row-major over each tensor's block grid,
+ * tensors in caller order; roots sorted by (n^3 products(p) desc, tensor, block,
+ * mode), LPT owners; packing as shampoo_plan, r = 1).
+ *   dims (host) SHAMPOO_MAX_ORDER int64 per tensor; orders (host) int32 per tensor.
+ * Returns SHAMPOO_ERR_CAPACITY (counts still written) if an array is too small. */
+int shampoo_tensor_plan(const int64_t* dims, const int32_t* orders, int32_t n_tensors, int32_t block_size,
+                        int64_t max_precond_dim, int32_t world_size, shampoo_tblock_t* blocks, int32_t capacity,
+                        int32_t* n_blocks, shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups,
+                        int64_t* stats_elems, int64_t* segment_elems);
+
+/* Statistics step for every block (Alg. 1 P:594-601 per mode):
+ *   non-finite G_B: block_status 2, H/D untouched, graft_num 0;
+ *   else H_i <- decay*H_i + weight*U_i U_i^T for every kept mode i owned by
+ *   only_owner (or all if < 0) under the CHUNKED sequential contract (reading
+ *   #25: fp64 sums over chunks of 4096 unfolding columns, chunk sums added in
+ *   ascending order, then the §6.2 epilogue) -- BIT-EXACT with the oracle;
+ *   D_B <- D_B + G_B o G_B and graft_num[b] = sum g^2 / max(D, 1e-30) for every block.
+ * tensors_host / blocks_host: HOST tables (job tables are derived and uploaded
+ * into the workspace).  workspace >= shampoo_tensor_stats_workspace_bytes(...). */
+size_t shampoo_tensor_stats_workspace_bytes(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                            const shampoo_tblock_t* blocks_host, int32_t n_blocks,
+                                            int32_t only_owner);
+int shampoo_tensor_stats_update(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                const shampoo_tblock_t* blocks_host, int32_t n_blocks, int32_t only_owner,
+                                float* stats, double decay, double weight, double* graft_num,
+                                int32_t* block_status, void* workspace, size_t workspace_bytes,
+                                shampoo_stream_t stream);
+
+/* Preconditioned gradient and graft scale for every block:
+ *   P_B = B x_0 X_0 x_1 X_1 ... over the kept modes (X_i = root at off[i]);
+ *   no kept mode: P_B = D_B^{-1/2} o G_B (reading #17);
+ *   graft_scale[b] = sqrt(graft_num[b]) / ||P_B||_F (0 if ||P_B|| = 0).
+ * Mode products run in fp64 (FP64 DMMA tiles for modes > 32, fp64 FMA fibres
+ * for small modes) with fp32 intermediates; parity is tolerance-based (1e-3).
+ * workspace >= shampoo_tensor_precondition_workspace_bytes(...). */
+size_t shampoo_tensor_precondition_workspace_bytes(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                                   const shampoo_tblock_t* blocks_host, int32_t n_blocks);
+int shampoo_tensor_precondition(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                const shampoo_tblock_t* blocks_host, int32_t n_blocks, const float* roots,
+                                const double* graft_num, float* graft_scale, double* den, void* workspace,
+                                size_t workspace_bytes, shampoo_stream_t stream);
+
 /* Number of kernel launches the last compute call on this host thread
  * enqueued (bench accounting, "gpu_launches"). */
 int64_t shampoo_last_launch_count(void);

@@ -14,6 +14,11 @@ Rows of the hot path:
         root_residual_batched       ||X^p A_hat - I||_F check
   a7  dist.refresh_roots            owner-sharded roots + NCCL all-gather
   a8-a9 precondition                L^{-1/p} G R^{-1/p} and the graft scale
+  f2  momentum_step                 Alg. 1 tail (momentum, grafted step, update)
+  f3  make_tensor_plan, tensor_stats_update, tensor_precondition
+                                    order-1..4 tensors (per-mode statistics, mode products)
+  f4  make_plan(split=(a, d)), inverse_root_rational_batched
+                                    L^{-a/2d} G R^{-(d-a)/2d}, roots S^{-r/p}
 """
 
 from __future__ import annotations
@@ -24,8 +29,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (BLOCK_DTYPE, GROUP_DTYPE, ROOT_INFO_DTYPE, STATE_DTYPE, TENSOR_DTYPE, ShampooError, check,
-                   last_launch_count)
+from ._lib import (BLOCK_DTYPE, GROUP_DTYPE, ROOT_INFO_DTYPE, STATE_DTYPE, TBLOCK_DTYPE, TENSOR_DTYPE,
+                   TTENSOR_DTYPE, ShampooError, check, last_launch_count)
 
 _lib.lib()  # fail loudly at import if the CUDA library is missing
 
@@ -287,3 +292,92 @@ def momentum_step(table: TensorTable, states: StateTable, plan: Plan, beta1: flo
                                   plan.device_blocks(table.device).data_ptr(), nb, float(beta1), float(eta0),
                                   1 if shampoo_branch else 0, eta_out.data_ptr() if eta_out is not None else None,
                                   ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+
+
+# ----------------------------------------------------------------------- f3
+def make_tensor_plan(shapes, block_size: int = 1024, max_precond_dim: int = 8192, world_size: int = 1) -> Plan:
+    """Plan for tensors of order 1..4 (shampoo_tensor_plan); ``blocks`` holds TBLOCK_DTYPE."""
+    L = _lib.lib()
+    n = len(shapes)
+    dims = np.ones((max(n, 1), 4), np.int64)
+    orders = np.zeros(max(n, 1), np.int32)
+    for i, s in enumerate(shapes):
+        s = tuple(int(d) for d in s)
+        if not 1 <= len(s) <= 4:
+            raise ValueError(f"tensor {i}: order must be 1..4")
+        dims[i, :len(s)] = s
+        orders[i] = len(s)
+    nb = np.zeros(1, np.int32)
+    ng = np.zeros(1, np.int32)
+    se = np.zeros(1, np.int64)
+    sg = np.zeros(1, np.int64)
+    check(L.shampoo_tensor_plan(dims.ctypes.data, orders.ctypes.data, n, block_size, max_precond_dim, world_size,
+                                None, 0, nb.ctypes.data, None, 0, ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
+    blocks = np.zeros(int(nb[0]), TBLOCK_DTYPE)
+    groups = np.zeros(int(ng[0]), GROUP_DTYPE)
+    check(L.shampoo_tensor_plan(dims.ctypes.data, orders.ctypes.data, n, block_size, max_precond_dim, world_size,
+                                blocks.ctypes.data, blocks.shape[0], nb.ctypes.data, groups.ctypes.data,
+                                groups.shape[0], ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
+    return Plan([tuple(int(d) for d in s) for s in shapes], block_size, max_precond_dim, world_size, blocks, groups,
+                int(se[0]), int(sg[0]))
+
+
+class TTensorTable:
+    """HOST table of shampoo_ttensor_t for lists of contiguous G / D / P tensors (order 1..4)."""
+
+    def __init__(self, Gs, Ds=None, Ps=None):
+        n = len(Gs)
+        Ds = Ds if Ds is not None else [None] * n
+        Ps = Ps if Ps is not None else [None] * n
+        host = np.zeros(n, TTENSOR_DTYPE)
+        self.device = Gs[0].device
+        for i, (G, D, P) in enumerate(zip(Gs, Ds, Ps)):
+            if not 1 <= G.dim() <= 4:
+                raise ValueError(f"tensor {i}: order must be 1..4")
+            for name, T in (("G", G), ("D", D), ("P", P)):
+                if T is None:
+                    continue
+                if T.dtype != torch.float32 or not T.is_contiguous() or T.device != self.device:
+                    raise ValueError(f"tensor {i} {name}: need a contiguous float32 tensor on {self.device}")
+                if tuple(T.shape) != tuple(G.shape):
+                    raise ValueError(f"tensor {i} {name}: shape {tuple(T.shape)} != G {tuple(G.shape)}")
+            host[i]["G"] = G.data_ptr()
+            host[i]["D"] = D.data_ptr() if D is not None else 0
+            host[i]["P"] = P.data_ptr() if P is not None else 0
+            host[i]["dims"][:] = 1
+            host[i]["dims"][:G.dim()] = G.shape
+            host[i]["order"] = G.dim()
+        self.host = host
+        self.n = n
+        self._keep = (list(Gs), list(Ds), list(Ps))
+
+
+def tensor_stats_update(table: TTensorTable, plan: Plan, stats: torch.Tensor, decay: float = 1.0,
+                        weight: float = 1.0, only_owner: int = -1, graft_num: torch.Tensor | None = None,
+                        block_status: torch.Tensor | None = None, stream=None):
+    """Per-mode statistics, D and graft numerator for every tensor block (f3)."""
+    L = _lib.lib()
+    nb = plan.n_blocks
+    th, bh = table.host, plan.blocks
+    wsb = L.shampoo_tensor_stats_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb, only_owner)
+    ws = workspace(wsb, stats.device, "tstats")
+    check(L.shampoo_tensor_stats_update(th.ctypes.data, table.n, bh.ctypes.data, nb, only_owner, stats.data_ptr(),
+                                        float(decay), float(weight),
+                                        graft_num.data_ptr() if graft_num is not None else None,
+                                        block_status.data_ptr() if block_status is not None else None,
+                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+
+
+def tensor_precondition(table: TTensorTable, plan: Plan, roots: torch.Tensor, graft_num: torch.Tensor | None = None,
+                        graft_scale: torch.Tensor | None = None, den: torch.Tensor | None = None, stream=None):
+    """P_B = B x_0 X_0 x_1 X_1 ... for every tensor block and the graft scale (f3)."""
+    L = _lib.lib()
+    nb = plan.n_blocks
+    th, bh = table.host, plan.blocks
+    wsb = L.shampoo_tensor_precondition_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb)
+    ws = workspace(wsb, roots.device, "tprecondition")
+    check(L.shampoo_tensor_precondition(th.ctypes.data, table.n, bh.ctypes.data, nb, roots.data_ptr(),
+                                        graft_num.data_ptr() if graft_num is not None else None,
+                                        graft_scale.data_ptr() if graft_scale is not None else None,
+                                        den.data_ptr() if den is not None else None, ws.data_ptr(), ws.numel(),
+                                        _stream_ptr(stream)))

@@ -23,9 +23,14 @@ GROUP_DTYPE = np.dtype([("owner", "<i4"), ("n", "<i4"), ("p", "<i4"), ("count", 
 TENSOR_DTYPE = np.dtype([("G", "<u8"), ("D", "<u8"), ("P", "<u8"), ("ldg", "<i8"), ("ldd", "<i8"),
                          ("ldp", "<i8"), ("m", "<i8"), ("n", "<i8")])
 STATE_DTYPE = np.dtype([("W", "<u8"), ("M", "<u8"), ("Pm", "<u8"), ("ldw", "<i8"), ("ldm", "<i8"), ("ldpm", "<i8")])
+TTENSOR_DTYPE = np.dtype([("G", "<u8"), ("D", "<u8"), ("P", "<u8"), ("dims", "<i8", (4,)), ("order", "<i4"),
+                          ("reserved", "<i4")])
+TBLOCK_DTYPE = np.dtype([("tensor_id", "<i4"), ("order", "<i4"), ("origin", "<i8", (4,)), ("extent", "<i4", (4,)),
+                         ("p", "<i4", (4,)), ("owner", "<i4", (4,)), ("ld", "<i4", (4,)), ("off", "<i8", (4,))])
 ROOT_INFO_DTYPE = np.dtype([("iters", "<i4"), ("status", "<i4"), ("lambda_max", "<f8"), ("err", "<f8")])
 assert BLOCK_DTYPE.itemsize == 80 and GROUP_DTYPE.itemsize == 40
 assert TENSOR_DTYPE.itemsize == 64 and ROOT_INFO_DTYPE.itemsize == 24
+assert TTENSOR_DTYPE.itemsize == 64 and TBLOCK_DTYPE.itemsize == 136
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "CUDA", 4: "WORKSPACE", 5: "CAPACITY"}
 
@@ -36,6 +41,8 @@ EXPORTED = [
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition",
     "shampoo_momentum_workspace_bytes", "shampoo_momentum_step",
+    "shampoo_tensor_plan", "shampoo_tensor_stats_workspace_bytes", "shampoo_tensor_stats_update",
+    "shampoo_tensor_precondition_workspace_bytes", "shampoo_tensor_precondition",
 ]
 
 
@@ -91,6 +98,16 @@ def lib():
     L.shampoo_momentum_workspace_bytes.restype = _sz
     L.shampoo_momentum_step.argtypes = [_vp, _vp, _i32, _vp, _i32, _dbl, _dbl, _i32, _vp, _vp, _sz, _vp]
     L.shampoo_momentum_step.restype = ctypes.c_int
+    L.shampoo_tensor_plan.argtypes = [_vp, _vp, _i32, _i32, _i64, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp]
+    L.shampoo_tensor_plan.restype = ctypes.c_int
+    L.shampoo_tensor_stats_workspace_bytes.argtypes = [_vp, _i32, _vp, _i32, _i32]
+    L.shampoo_tensor_stats_workspace_bytes.restype = _sz
+    L.shampoo_tensor_stats_update.argtypes = [_vp, _i32, _vp, _i32, _i32, _vp, _dbl, _dbl, _vp, _vp, _vp, _sz, _vp]
+    L.shampoo_tensor_stats_update.restype = ctypes.c_int
+    L.shampoo_tensor_precondition_workspace_bytes.argtypes = [_vp, _i32, _vp, _i32]
+    L.shampoo_tensor_precondition_workspace_bytes.restype = _sz
+    L.shampoo_tensor_precondition.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    L.shampoo_tensor_precondition.restype = ctypes.c_int
     if L.shampoo_abi_version() != 2:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L

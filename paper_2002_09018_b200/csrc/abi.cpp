@@ -42,6 +42,42 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
               shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
               int64_t* segment_elems);
 
+int tensor_plan_impl(const int64_t* dims, const int32_t* orders, int32_t n_tensors, int32_t block_size,
+                     int64_t max_precond_dim, int32_t world_size, shampoo_tblock_t* out_blocks, int32_t capacity,
+                     int32_t* n_blocks_out, shampoo_group_t* out_groups, int32_t group_capacity,
+                     int32_t* n_groups_out, int64_t* stats_elems, int64_t* segment_elems);
+
+// host tables of the tensor path: orders, extents inside the tensor, pointers
+static int check_tensor_tables(const shampoo_ttensor_t* T, int32_t n_tensors, const shampoo_tblock_t* B,
+                               int32_t n_blocks, bool need_p) {
+  if (!T || !B) return set_error(SHAMPOO_ERR_INVALID_ARG, "null tensor/block table");
+  for (int32_t t = 0; t < n_tensors; ++t) {
+    if (T[t].order < 1 || T[t].order > SHAMPOO_MAX_ORDER)
+      return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor %d: order %d", t, T[t].order);
+    if (!T[t].G || (need_p && !T[t].P)) return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor %d: null G or P", t);
+    for (int i = 0; i < T[t].order; ++i)
+      if (T[t].dims[i] < 1) return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor %d: dim %d < 1", t, i);
+  }
+  for (int32_t b = 0; b < n_blocks; ++b) {
+    const shampoo_tblock_t& k = B[b];
+    if (k.tensor_id < 0 || k.tensor_id >= n_tensors)
+      return set_error(SHAMPOO_ERR_INVALID_ARG, "block %d: tensor_id out of range", b);
+    const shampoo_ttensor_t& t = T[k.tensor_id];
+    if (k.order != t.order) return set_error(SHAMPOO_ERR_INVALID_ARG, "block %d: order mismatch", b);
+    bool any = false;
+    for (int i = 0; i < k.order; ++i) {
+      if (k.extent[i] < 1 || k.origin[i] < 0 || k.origin[i] + k.extent[i] > t.dims[i])
+        return set_error(SHAMPOO_ERR_INVALID_ARG, "block %d: mode %d outside the tensor", b, i);
+      if (k.p[i] && (k.p[i] > 16 || k.off[i] < 0 || k.ld[i] < k.extent[i]))
+        return set_error(SHAMPOO_ERR_INVALID_ARG, "block %d: mode %d has a bad root entry", b, i);
+      any |= k.p[i] != 0;
+    }
+    if (need_p && !any && !t.D)
+      return set_error(SHAMPOO_ERR_INVALID_ARG, "block %d: diagonal-only block needs D", b);
+  }
+  return SHAMPOO_OK;
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static int check_ws(const void* ws, size_t have, size_t need) {
@@ -188,6 +224,68 @@ int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors
     return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
   return precondition_launch(tensors_host, n_tensors, blocks_host, n_blocks, roots, graft_num, graft_scale, den,
                              workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
+}
+
+int shampoo_tensor_plan(const int64_t* dims, const int32_t* orders, int32_t n_tensors, int32_t block_size,
+                        int64_t max_precond_dim, int32_t world_size, shampoo_tblock_t* blocks, int32_t capacity,
+                        int32_t* n_blocks, shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups,
+                        int64_t* stats_elems, int64_t* segment_elems) {
+  g_err[0] = 0;
+  return tensor_plan_impl(dims, orders, n_tensors, block_size, max_precond_dim, world_size, blocks, capacity,
+                          n_blocks, groups, group_capacity, n_groups, stats_elems, segment_elems);
+}
+
+size_t shampoo_tensor_stats_workspace_bytes(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                            const shampoo_tblock_t* blocks_host, int32_t n_blocks,
+                                            int32_t only_owner) {
+  if (n_blocks <= 0 || check_tensor_tables(tensors_host, n_tensors, blocks_host, n_blocks, false)) return 0;
+  return tensor_stats_workspace_bytes(tensors_host, blocks_host, n_blocks, only_owner);
+}
+
+int shampoo_tensor_stats_update(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                const shampoo_tblock_t* blocks_host, int32_t n_blocks, int32_t only_owner,
+                                float* stats, double decay, double weight, double* graft_num,
+                                int32_t* block_status, void* workspace, size_t workspace_bytes,
+                                shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
+  if (n_blocks == 0) return SHAMPOO_OK;
+  int rc = check_tensor_tables(tensors_host, n_tensors, blocks_host, n_blocks, false);
+  if (rc) return rc;
+  if (!std::isfinite(decay) || !std::isfinite(weight))
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "decay/weight must be finite");
+  if (!stats) return set_error(SHAMPOO_ERR_INVALID_ARG, "null statistics buffer");
+  if (!workspace) return set_error(SHAMPOO_ERR_WORKSPACE, "null workspace");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
+  return tensor_stats_launch(tensors_host, blocks_host, n_blocks, only_owner, stats, decay, weight, graft_num,
+                             block_status, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
+                             &g_launches);
+}
+
+size_t shampoo_tensor_precondition_workspace_bytes(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                                   const shampoo_tblock_t* blocks_host, int32_t n_blocks) {
+  if (n_blocks <= 0 || check_tensor_tables(tensors_host, n_tensors, blocks_host, n_blocks, false)) return 0;
+  return tensor_precondition_workspace_bytes(tensors_host, blocks_host, n_blocks);
+}
+
+int shampoo_tensor_precondition(const shampoo_ttensor_t* tensors_host, int32_t n_tensors,
+                                const shampoo_tblock_t* blocks_host, int32_t n_blocks, const float* roots,
+                                const double* graft_num, float* graft_scale, double* den, void* workspace,
+                                size_t workspace_bytes, shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
+  if (n_blocks == 0) return SHAMPOO_OK;
+  int rc = check_tensor_tables(tensors_host, n_tensors, blocks_host, n_blocks, true);
+  if (rc) return rc;
+  if (!roots) return set_error(SHAMPOO_ERR_INVALID_ARG, "null roots");
+  if (!workspace) return set_error(SHAMPOO_ERR_WORKSPACE, "null workspace");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
+  return tensor_precondition_launch(tensors_host, blocks_host, n_blocks, roots, graft_num, graft_scale, den,
+                                    workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
 }
 
 size_t shampoo_momentum_workspace_bytes(int32_t n_blocks) { return n_blocks > 0 ? momentum_workspace_bytes(n_blocks) : 0; }

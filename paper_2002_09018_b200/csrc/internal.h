@@ -41,6 +41,17 @@ int momentum_launch(const shampoo_tensor_t* tensors, const shampoo_state_t* stat
                     int n_blocks, double beta1, double eta0, int shampoo_branch, double* eta_out, void* ws,
                     cudaStream_t stream, int64_t* launches);
 
+// tensor.cu (f3)
+size_t tensor_stats_workspace_bytes(const shampoo_ttensor_t* T, const shampoo_tblock_t* B, int n_blocks,
+                                    int only_owner);
+int tensor_stats_launch(const shampoo_ttensor_t* T, const shampoo_tblock_t* B, int n_blocks, int only_owner,
+                        float* stats, double decay, double weight, double* graft_num, int32_t* block_status,
+                        void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
+size_t tensor_precondition_workspace_bytes(const shampoo_ttensor_t* T, const shampoo_tblock_t* B, int n_blocks);
+int tensor_precondition_launch(const shampoo_ttensor_t* T, const shampoo_tblock_t* B, int n_blocks,
+                               const float* roots, const double* graft_num, float* graft_scale, double* den,
+                               void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
+
 int num_sms();
 
 }  // namespace shp

@@ -42,6 +42,71 @@ struct RootRef {
   int32_t n, p, r;
 };
 
+// Roots sorted by (cost desc, tensor, block, side/mode), assigned LPT to the
+// least-loaded rank (lowest rank on ties), then packed per rank: groups of
+// equal (n, p, r) in (n desc, p desc, r desc) order, ld = roundup(n, 4), group
+// stride roundup(n*ld, 64); segments padded to the largest (roundup 64).
+// set(root, owner, absolute offset, ld) records each root's placement.
+// Returns the segment size.
+template <class Set>
+static int64_t assign_and_pack(std::vector<RootRef>& roots, int world_size, std::vector<shampoo_group_t>& groups,
+                               Set set) {
+  std::stable_sort(roots.begin(), roots.end(), [](const RootRef& x, const RootRef& y) {
+    return std::make_tuple(-x.cost, x.tensor, x.block, x.side) < std::make_tuple(-y.cost, y.tensor, y.block, y.side);
+  });
+  std::vector<int64_t> load(world_size, 0);
+  std::vector<std::vector<int32_t>> owned(world_size);  // sorted positions
+  std::vector<int> owner_of(roots.size(), 0);
+  for (int32_t pos = 0; pos < (int32_t)roots.size(); ++pos) {
+    int r = 0;
+    for (int q = 1; q < world_size; ++q)
+      if (load[q] < load[r]) r = q;
+    load[r] += roots[pos].cost;
+    owned[r].push_back(pos);
+    owner_of[pos] = r;
+  }
+  std::vector<int64_t> used(world_size, 0), rel_off(roots.size(), 0), ld_of(roots.size(), 0);
+  const size_t g0 = groups.size();
+  for (int r = 0; r < world_size; ++r) {
+    std::vector<int32_t> items = owned[r];
+    std::stable_sort(items.begin(), items.end(), [&](int32_t a, int32_t c) {
+      const RootRef& x = roots[a];
+      const RootRef& y = roots[c];
+      return std::make_tuple(-x.n, -x.p, -x.r, a) < std::make_tuple(-y.n, -y.p, -y.r, c);
+    });
+    int64_t off = 0;
+    size_t i = 0;
+    while (i < items.size()) {
+      const int32_t n = roots[items[i]].n, p = roots[items[i]].p, rr = roots[items[i]].r;
+      size_t j = i;
+      while (j < items.size() && roots[items[j]].n == n && roots[items[j]].p == p && roots[items[j]].r == rr) ++j;
+      const int64_t ld = roundup(n, 4), stride = roundup((int64_t)n * ld, 64);
+      shampoo_group_t g;
+      g.owner = r;
+      g.n = n;
+      g.p = p;
+      g.r = rr;
+      g.reserved = 0;
+      g.count = (int32_t)(j - i);
+      g.offset = off;  // relative to the segment for now
+      g.stride = stride;
+      groups.push_back(g);
+      for (size_t k = i; k < j; ++k) {
+        rel_off[items[k]] = off + (int64_t)(k - i) * stride;
+        ld_of[items[k]] = ld;
+      }
+      off += (int64_t)(j - i) * stride;
+      i = j;
+    }
+    used[r] = off;
+  }
+  const int64_t seg = roundup(world_size ? *std::max_element(used.begin(), used.end()) : 0, 64);
+  for (size_t q = g0; q < groups.size(); ++q) groups[q].offset += (int64_t)groups[q].owner * seg;
+  for (size_t pos = 0; pos < roots.size(); ++pos)
+    set(roots[pos], owner_of[pos], rel_off[pos] + (int64_t)owner_of[pos] * seg, (int)ld_of[pos]);
+  return seg;
+}
+
 int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
               int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
               shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
@@ -93,71 +158,19 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
       roots.push_back({n * n * n * products_per_iteration(b.p_right), b.tensor_id, i, 1, b.cols, b.p_right, b.r_right});
     }
   }
-  std::stable_sort(roots.begin(), roots.end(), [](const RootRef& x, const RootRef& y) {
-    return std::make_tuple(-x.cost, x.tensor, x.block, x.side) < std::make_tuple(-y.cost, y.tensor, y.block, y.side);
-  });
-  // LPT owners
-  std::vector<int64_t> load(world_size, 0);
-  std::vector<std::vector<int32_t>> owned(world_size);  // indices into roots (sorted positions)
-  for (int32_t pos = 0; pos < (int32_t)roots.size(); ++pos) {
-    int r = 0;
-    for (int q = 1; q < world_size; ++q)
-      if (load[q] < load[r]) r = q;
-    load[r] += roots[pos].cost;
-    owned[r].push_back(pos);
-    shampoo_block_t& b = blocks[roots[pos].block];
-    if (roots[pos].side == 0) b.owner_left = r;
-    else b.owner_right = r;
-  }
-  // packing
   std::vector<shampoo_group_t> groups;
-  std::vector<int64_t> used(world_size, 0);
-  for (int r = 0; r < world_size; ++r) {
-    std::vector<int32_t> items = owned[r];
-    std::stable_sort(items.begin(), items.end(), [&](int32_t a, int32_t c) {
-      const RootRef& x = roots[a];
-      const RootRef& y = roots[c];
-      return std::make_tuple(-x.n, -x.p, -x.r, a) < std::make_tuple(-y.n, -y.p, -y.r, c);
-    });
-    int64_t off = 0;
-    size_t i = 0;
-    while (i < items.size()) {
-      const int32_t n = roots[items[i]].n, p = roots[items[i]].p, rr = roots[items[i]].r;
-      size_t j = i;
-      while (j < items.size() && roots[items[j]].n == n && roots[items[j]].p == p && roots[items[j]].r == rr) ++j;
-      const int64_t ld = roundup(n, 4), stride = roundup((int64_t)n * ld, 64);
-      shampoo_group_t g;
-      g.owner = r;
-      g.n = n;
-      g.p = p;
-      g.r = rr;
-      g.reserved = 0;
-      g.count = (int32_t)(j - i);
-      g.offset = off;  // relative to the segment for now
-      g.stride = stride;
-      groups.push_back(g);
-      for (size_t k = i; k < j; ++k) {
-        const RootRef& rr = roots[items[k]];
-        shampoo_block_t& b = blocks[rr.block];
-        if (rr.side == 0) {
-          b.left_off = off + (int64_t)(k - i) * stride;
-          b.left_ld = (int32_t)ld;
-        } else {
-          b.right_off = off + (int64_t)(k - i) * stride;
-          b.right_ld = (int32_t)ld;
-        }
-      }
-      off += (int64_t)(j - i) * stride;
-      i = j;
+  const int64_t seg = assign_and_pack(roots, world_size, groups, [&](const RootRef& rr, int owner, int64_t off, int ld) {
+    shampoo_block_t& b = blocks[rr.block];
+    if (rr.side == 0) {
+      b.owner_left = owner;
+      b.left_off = off;
+      b.left_ld = ld;
+    } else {
+      b.owner_right = owner;
+      b.right_off = off;
+      b.right_ld = ld;
     }
-    used[r] = off;
-  }
-  const int64_t seg = roundup(world_size ? *std::max_element(used.begin(), used.end()) : 0, 64);
-  for (auto& g : groups) g.offset += (int64_t)g.owner * seg;
-  for (auto& b : blocks) {
-    if (b.left_off >= 0) b.left_off += (int64_t)b.owner_left * seg;
-    if (b.right_off >= 0) b.right_off += (int64_t)b.owner_right * seg;
-  }
+  });
   if (n_blocks_out) *n_blocks_out = (int32_t)blocks.size();
   if (n_groups_out) *n_groups_out = (int32_t)groups.size();
   if (stats_elems) *stats_elems = seg * world_size;
@@ -173,6 +186,88 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
   }
   if (!cap_ok) return set_error(SHAMPOO_ERR_CAPACITY, "plan: output capacity too small (%zu blocks, %zu groups)",
                                 blocks.size(), groups.size());
+  return SHAMPOO_OK;
+}
+
+// ------------------------------------------------------------- f3: tensors
+// Rule (oracle/tensor.py; readings #24-#26): mode i kept iff 1 < d_i <=
+// max_precond_dim, p = 2 * (#kept) on every kept mode; every mode split into
+// ceil(d_i / b) ranges, blocks row-major over the block grid; roots and
+// packing exactly as the matrix plan (side = mode).
+int tensor_plan_impl(const int64_t* dims, const int32_t* orders, int32_t n_tensors, int32_t block_size,
+                     int64_t max_precond_dim, int32_t world_size, shampoo_tblock_t* out_blocks, int32_t capacity,
+                     int32_t* n_blocks_out, shampoo_group_t* out_groups, int32_t group_capacity,
+                     int32_t* n_groups_out, int64_t* stats_elems, int64_t* segment_elems) {
+  constexpr int K = SHAMPOO_MAX_ORDER;
+  if (!dims || !orders || n_tensors < 0 || block_size < 1 || max_precond_dim < 1 || world_size < 1)
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor plan: bad arguments");
+  std::vector<shampoo_tblock_t> blocks;
+  for (int32_t t = 0; t < n_tensors; ++t) {
+    const int k = orders[t];
+    if (k < 1 || k > K) return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor plan: tensor %d has order %d", t, k);
+    const int64_t* d = dims + (int64_t)K * t;
+    int kept = 0;
+    int64_t grid[K], total = 1;
+    for (int i = 0; i < k; ++i) {
+      if (d[i] < 1) return set_error(SHAMPOO_ERR_INVALID_ARG, "tensor plan: tensor %d has a zero dimension", t);
+      kept += (d[i] > 1 && d[i] <= max_precond_dim) ? 1 : 0;
+      grid[i] = (d[i] + block_size - 1) / block_size;
+      total *= grid[i];
+    }
+    for (int64_t flat = 0; flat < total; ++flat) {
+      shampoo_tblock_t b;
+      std::memset(&b, 0, sizeof b);
+      b.tensor_id = t;
+      b.order = k;
+      int64_t rem = flat;
+      for (int i = k - 1; i >= 0; --i) {
+        const int64_t idx = rem % grid[i];
+        rem /= grid[i];
+        b.origin[i] = idx * block_size;
+        b.extent[i] = (int32_t)std::min<int64_t>(block_size, d[i] - b.origin[i]);
+      }
+      for (int i = 0; i < K; ++i) {
+        if (i >= k) b.extent[i] = 1;
+        b.p[i] = (i < k && d[i] > 1 && d[i] <= max_precond_dim) ? 2 * kept : 0;
+        b.owner[i] = -1;
+        b.off[i] = -1;
+        b.ld[i] = 0;
+      }
+      blocks.push_back(b);
+    }
+  }
+  std::vector<RootRef> roots;
+  for (int32_t i = 0; i < (int32_t)blocks.size(); ++i) {
+    const shampoo_tblock_t& b = blocks[i];
+    for (int m = 0; m < b.order; ++m)
+      if (b.p[m]) {
+        const int64_t n = b.extent[m];
+        roots.push_back({n * n * n * products_per_iteration(b.p[m]), b.tensor_id, i, m, b.extent[m], b.p[m], 1});
+      }
+  }
+  std::vector<shampoo_group_t> groups;
+  const int64_t seg = assign_and_pack(roots, world_size, groups, [&](const RootRef& rr, int owner, int64_t off, int ld) {
+    shampoo_tblock_t& b = blocks[rr.block];
+    b.owner[rr.side] = owner;
+    b.off[rr.side] = off;
+    b.ld[rr.side] = ld;
+  });
+  if (n_blocks_out) *n_blocks_out = (int32_t)blocks.size();
+  if (n_groups_out) *n_groups_out = (int32_t)groups.size();
+  if (stats_elems) *stats_elems = seg * world_size;
+  if (segment_elems) *segment_elems = seg;
+  bool cap_ok = true;
+  if (out_blocks) {
+    if (capacity < (int32_t)blocks.size()) cap_ok = false;
+    else std::memcpy(out_blocks, blocks.data(), blocks.size() * sizeof(shampoo_tblock_t));
+  }
+  if (out_groups) {
+    if (group_capacity < (int32_t)groups.size()) cap_ok = false;
+    else std::memcpy(out_groups, groups.data(), groups.size() * sizeof(shampoo_group_t));
+  }
+  if (!cap_ok)
+    return set_error(SHAMPOO_ERR_CAPACITY, "tensor plan: output capacity too small (%zu blocks, %zu groups)",
+                     blocks.size(), groups.size());
   return SHAMPOO_OK;
 }
 

@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 from oracle import plan as oplan
+import synth
 from synth import transformer_big_shapes
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -153,3 +154,55 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
                 assert "liboracle" not in src and "oracle_stats" not in re.sub(r"(#|//).*", "", src), f
+
+
+# ------------------------------------------------------------------ f3 tensor plan
+def _tplan_equal(lib_plan, o):
+    assert lib_plan.n_blocks == len(o.blocks) and lib_plan.stats_elems == o.stats_elems
+    assert lib_plan.segment_elems == o.segment_elems
+    for b, ob in zip(lib_plan.blocks, o.blocks):
+        got = (int(b["tensor_id"]), int(b["order"]), [int(x) for x in b["origin"]], [int(x) for x in b["extent"]],
+               [int(x) for x in b["p"]], [int(x) for x in b["owner"]], [int(x) for x in b["ld"]],
+               [int(x) for x in b["off"]])
+        assert got == (ob.tensor_id, ob.order, ob.origin, ob.extent, ob.p, ob.owner, ob.ld, ob.off)
+    got_g = [tuple(int(g[k]) for k in ("owner", "n", "p", "r", "offset", "count", "stride")) for g in lib_plan.groups]
+    assert got_g == [(g.owner, g.n, g.p, g.r, g.offset, g.count, g.stride) for g in o.groups]
+
+
+@pytest.mark.parametrize("W", [1, 2, 8])
+@pytest.mark.parametrize("b", [1024, 128])
+def test_tensor_plan_bit_exact_vs_oracle(shp, W, b):
+    from oracle import tensor as ot
+    shapes = [s for _, s in synth.resnet50_shapes()] + [(5, 3, 7), (1, 1, 1, 9000), (300, 70, 2)]
+    _tplan_equal(shp.make_tensor_plan(shapes, b, 4096, W), ot.plan(shapes, b, 4096, W))
+
+
+def test_tensor_entry_points_validate_host_tables(shp):
+    from paper_2002_09018_b200 import ShampooError, _lib
+    L = _lib.lib()
+    with pytest.raises(ValueError):
+        shp.make_tensor_plan([(2, 3, 4, 5, 6)])
+    dims = np.ones((1, 4), np.int64)
+    orders = np.array([5], np.int32)
+    nb = np.zeros(1, np.int32)
+    ng = np.zeros(1, np.int32)
+    se = np.zeros(1, np.int64)
+    assert L.shampoo_tensor_plan(dims.ctypes.data, orders.ctypes.data, 1, 64, 4096, 1, None, 0, nb.ctypes.data,
+                                 None, 0, ng.ctypes.data, se.ctypes.data, se.ctypes.data) == 1
+    pl = shp.make_tensor_plan([(3, 4, 5)], 64, 4096, 1)
+    t = np.zeros(1, _lib.TTENSOR_DTYPE)
+    t[0]["G"] = 1 << 40
+    t[0]["dims"][:] = (3, 4, 5, 1)
+    t[0]["order"] = 3
+    # block extends beyond its tensor -> INVALID_ARG, nothing enqueued
+    bad = pl.blocks.copy()
+    bad[0]["extent"][0] = 4
+    assert L.shampoo_tensor_stats_update(t.ctypes.data, 1, bad.ctypes.data, 1, -1, 1 << 40, 1.0, 1.0, None, None,
+                                         1 << 40, 1 << 30, None) == 1
+    assert b"outside" in L.shampoo_last_error()
+    # precondition needs P
+    assert L.shampoo_tensor_precondition(t.ctypes.data, 1, pl.blocks.ctypes.data, 1, 1 << 40, None, None, None,
+                                         1 << 40, 1 << 30, None) == 1
+    assert b"null G or P" in L.shampoo_last_error()
+    with pytest.raises(ShampooError):
+        shp.make_tensor_plan([(0, 3)])
