@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--block-size", type=int, default=BLOCK,
                     help="config 5 sweep (128..4096); the metric is quoted at 1024")
     ap.add_argument("--max-precond-dim", type=int, default=MAX_PRECOND)
+    ap.add_argument("--hybrid", action="store_true",
+                    help="hybrid roots: FP64 DMMA iterations, then the 3xTF32 tcgen05 tail (DESIGN.md §6.3b)")
     return ap.parse_args()
 
 
@@ -211,7 +213,8 @@ def main():
         launches[0] += shp.last_launch_count()
         if ev:
             ev[1].record(stream)
-        infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol)
+        infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol,
+                                        fp64_iters=-1 if args.hybrid else None)
         launches[0] += len(infos)
         if ev:
             ev[2].record(stream)
@@ -338,7 +341,8 @@ def main():
                        "block_size": B, "max_precond_dim": args.max_precond_dim, "blocks": nb,
                        "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
                        "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
-                       "parallelism": f"root-shard{world}", "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
+                       "parallelism": f"root-shard{world}",
+                       "root_precision": "hybrid fp64 DMMA -> 3xTF32 tcgen05 (auto switch)" if args.hybrid else "fp64 DMMA", "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
             "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather": ph[2], "precondition": ph[3]},
             "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,
             "root_phase_roots_per_s": n_p4_total / (ph[1] * 1e-3),

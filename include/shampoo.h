@@ -196,6 +196,26 @@ int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t s
                                           shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
                                           shampoo_stream_t stream);
 
+/* Hybrid precision (north star: "3xTF32 error-compensated splits or FP64 DMMA";
+ * DESIGN.md §6.3b): the first fp64_iters coupled-Newton iterations in fp64 on
+ * the DMMA pipe, the rest on the tcgen05 tensor cores with 3xTF32 products
+ * (hi = trunc_tf32(x), lo = x - hi; lo.hi + hi.lo + hi.hi in fp32) and fp32
+ * iterates; symmetric upper tiles only.
+ * fp64_iters = -1: automatic, the smallest k with eps_rel * g^k >= 1e-2
+ * (1e-1 for p <= 3), g = (1 + 1/p)^p (k = 11 for p = 4, eps_rel = 1e-6);
+ * eps_rel = 0 or fp64_iters > max_iter: pure fp64 (= the call above).
+ * Measured on B200 (n = 1024, kappa(A_hat) = 1e6, p = 4): rel. Frobenius
+ * error 9e-5 (bar 1e-3), 1.43x the pure-fp64 rate.  The tensor core's fp32
+ * accumulation is biased on near-identity products (~1e-5): k-tiles are
+ * ordered so the O(1) diagonal blocks come last, and the tail stops at
+ * max|M - I| <= max(tol, 1e-5) or by the stagnation rule (status 1).
+ * Same arguments, statuses and workspace as shampoo_inverse_pth_root_batched. */
+int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                            int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                            double tol, int32_t max_iter, int32_t power_iters, int32_t fp64_iters,
+                                            shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                            shampoo_stream_t stream);
+
 /* Independent root check (config 2, north-star invariant):
  *   residual_i = || X_i^p (A_i + eps_rel*lambda_i*I) - I ||_F   in fp64,
  * lambda_i = info[i].lambda_max from the root call.  out: double[batch]. */

@@ -167,12 +167,21 @@ def root_workspace_bytes(batch: int, n: int, p: int, max_iter: int = 100) -> int
 
 def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: int, stride_x: int, batch: int,
                          n: int, p: int, info: torch.Tensor, eps_rel: float = 1e-6, tol: float = 1e-7,
-                         max_iter: int = 100, power_iters: int = 100, device=None, stream=None, r: int = 1):
-    """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry)."""
+                         max_iter: int = 100, power_iters: int = 100, device=None, stream=None, r: int = 1,
+                         fp64_iters: int | None = None):
+    """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry).
+    fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch)."""
     L = _lib.lib()
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
     ws = workspace(wsb, device if device is not None else info.device, "root")
-    if r == 1:
+    if fp64_iters is not None:
+        if r != 1:
+            raise ValueError("the hybrid root serves r = 1 only")
+        check(L.shampoo_inverse_pth_root_batched_hybrid(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p,
+                                                        eps_rel, tol, max_iter, power_iters, fp64_iters,
+                                                        info.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                        _stream_ptr(stream)))
+    elif r == 1:
         check(L.shampoo_inverse_pth_root_batched(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel, tol,
                                                  max_iter, power_iters, info.data_ptr(), ws.data_ptr(), ws.numel(),
                                                  _stream_ptr(stream)))
@@ -192,7 +201,8 @@ def info_to_numpy(info: torch.Tensor) -> np.ndarray:
 
 def inverse_pth_root_batched(A: torch.Tensor, p: int, X: torch.Tensor | None = None, eps_rel: float = 1e-6,
                              tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100,
-                             info: torch.Tensor | None = None, stream=None, r: int = 1):
+                             info: torch.Tensor | None = None, stream=None, r: int = 1,
+                             fp64_iters: int | None = None):
     """A: (batch, n, n) or (n, n) float32 CUDA tensor (row stride >= n, unit column stride).
     Returns (X, info) with X like A and info a uint8 tensor of shampoo_root_info_t."""
     squeeze = A.dim() == 2
@@ -206,7 +216,7 @@ def inverse_pth_root_batched(A: torch.Tensor, p: int, X: torch.Tensor | None = N
     if info is None:
         info = new_info(batch, A3.device)
     inverse_pth_root_ptr(A3.data_ptr(), A3.stride(1), A3.stride(0), X3.data_ptr(), X3.stride(1), X3.stride(0), batch,
-                         n, p, info, eps_rel, tol, max_iter, power_iters, A3.device, stream, r)
+                         n, p, info, eps_rel, tol, max_iter, power_iters, A3.device, stream, r, fp64_iters)
     return (X3[0] if squeeze else X3), info
 
 
@@ -231,7 +241,8 @@ def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.
 
 
 def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, owner: int, eps_rel: float = 1e-6,
-                        tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100, infos=None, stream=None):
+                        tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100, infos=None, stream=None,
+                        fp64_iters: int | None = None):
     """Inverse p-th roots of every statistic owned by `owner` (one batched call per
     (n, p) group); roots land at the statistics' offsets."""
     out = []
@@ -241,7 +252,8 @@ def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, ow
         ld = (n + 3) // 4 * 4
         info = new_info(cnt, stats.device)
         inverse_pth_root_ptr(stats.data_ptr() + 4 * off, ld, stride, roots.data_ptr() + 4 * off, ld, stride, cnt, n,
-                             p, info, eps_rel, tol, max_iter, power_iters, stats.device, stream, r)
+                             p, info, eps_rel, tol, max_iter, power_iters, stats.device, stream, r,
+                             fp64_iters if r == 1 else None)
         out.append((g, info))
     if infos is not None:
         infos.extend(out)

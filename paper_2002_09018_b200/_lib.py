@@ -38,6 +38,7 @@ EXPORTED = [
     "shampoo_abi_version", "shampoo_last_error", "shampoo_last_launch_count", "shampoo_plan",
     "shampoo_stats_workspace_bytes", "shampoo_stats_update",
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
+    "shampoo_inverse_pth_root_batched_hybrid",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition",
     "shampoo_momentum_workspace_bytes", "shampoo_momentum_step",
@@ -85,6 +86,9 @@ def lib():
     L.shampoo_inverse_root_rational_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _i32,
                                                         _dbl, _dbl, _i32, _i32, _vp, _vp, _sz, _vp]
     L.shampoo_inverse_root_rational_batched.restype = ctypes.c_int
+    L.shampoo_inverse_pth_root_batched_hybrid.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl,
+                                                          _dbl, _i32, _i32, _i32, _vp, _vp, _sz, _vp]
+    L.shampoo_inverse_pth_root_batched_hybrid.restype = ctypes.c_int
     L.shampoo_root_residual_workspace_bytes.argtypes = [_i32, _i32, _i32]
     L.shampoo_root_residual_workspace_bytes.restype = _sz
     L.shampoo_root_residual_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl, _vp, _vp,

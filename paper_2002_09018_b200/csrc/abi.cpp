@@ -149,11 +149,58 @@ int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride
                                                max_iter, power_iters, info, workspace, workspace_bytes, stream);
 }
 
+static int root_entry(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x,
+                      int32_t batch, int32_t n, int32_t p, int32_t r, int32_t k_sw, double eps_rel, double tol,
+                      int32_t max_iter, int32_t power_iters, shampoo_root_info_t* info, void* workspace,
+                      size_t workspace_bytes, shampoo_stream_t stream);
+
 int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
                                           int64_t stride_x, int32_t batch, int32_t n, int32_t p, int32_t r,
                                           double eps_rel, double tol, int32_t max_iter, int32_t power_iters,
                                           shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
                                           shampoo_stream_t stream) {
+  return root_entry(A, lda, stride_a, X, ldx, stride_x, batch, n, p, r, max_iter + 1, eps_rel, tol, max_iter,
+                    power_iters, info, workspace, workspace_bytes, stream);
+}
+
+// a-priori switch of the hybrid root: after k fp64 iterations
+// the smallest eigenvalue of M is at least eps_rel * g^k, g = (1 + 1/p)^p;
+// switch once that reaches 1e-2 (measured on B200, n = 1024, kappa 1e6: a
+// switch at 1e-3 (k = 8) leaves a 1.3e-3 root error -- the tensor core's fp32
+// accumulation is biased on near-identity products -- at 1e-2 (k = 11) ~1e-4;
+// p = 1 at 1e-2 measured 3.1e-4, hence 1e-1 for p <= 3)
+static int auto_fp64_iters(int p, double eps_rel) {
+  if (!(eps_rel > 0.0)) return -1;
+  const double g = std::pow(1.0 + 1.0 / p, (double)p);
+  // low orders amplify product errors more (X ~ A_hat^{-1/p}): p <= 3 switches at 1e-1
+  const double thr = p <= 3 ? 1e-1 : 1e-2;
+  int k = (int)std::ceil(std::log(thr / eps_rel) / std::log(g));
+  return k < 1 ? 1 : k;
+}
+
+int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                            int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                            double tol, int32_t max_iter, int32_t power_iters, int32_t fp64_iters,
+                                            shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                            shampoo_stream_t stream) {
+  int k_sw = fp64_iters;
+  if (k_sw < 0) {
+    k_sw = auto_fp64_iters(p, eps_rel);
+    if (k_sw < 0) k_sw = max_iter + 1;  // no ridge: no a-priori bound, stay in fp64
+  }
+  if (k_sw == 0) {
+    g_err[0] = 0;
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "fp64_iters must be >= 1 (or -1 for automatic)");
+  }
+  if (k_sw > max_iter) k_sw = max_iter + 1;
+  return root_entry(A, lda, stride_a, X, ldx, stride_x, batch, n, p, 1, k_sw, eps_rel, tol, max_iter, power_iters,
+                    info, workspace, workspace_bytes, stream);
+}
+
+static int root_entry(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x,
+                      int32_t batch, int32_t n, int32_t p, int32_t r, int32_t k_sw, double eps_rel, double tol,
+                      int32_t max_iter, int32_t power_iters, shampoo_root_info_t* info, void* workspace,
+                      size_t workspace_bytes, shampoo_stream_t stream) {
   g_err[0] = 0;
   g_launches = 0;
   if (batch < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "batch < 0");
@@ -171,7 +218,7 @@ int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t s
     return set_error(SHAMPOO_ERR_INVALID_ARG, "max_iter in [0, 1000], power_iters >= 1");
   int rc = check_ws(workspace, workspace_bytes, root_workspace_bytes(batch, n, max_iter));
   if (rc) return rc;
-  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, r, eps_rel, tol, max_iter, power_iters, info,
+  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, r, k_sw, eps_rel, tol, max_iter, power_iters, info,
                      workspace, static_cast<cudaStream_t>(stream), &g_launches);
 }
 

@@ -46,6 +46,7 @@ struct RootArgs {
   float* X;
   int64_t ldx, stride_x;
   int batch, n, np, p, r, max_iter, power_iters;
+  int k_sw;  // hybrid: matrices still iterating at check k_sw are handed to the 3xTF32 tail (> max_iter: off)
   double eps_rel, tol;
   shampoo_root_info_t* info;
   double* bufs;  // batch * kBufs * np * np
@@ -53,6 +54,8 @@ struct RootArgs {
   double* errh;  // batch * (max_iter + 1)
   int4* res;     // batch: {result buffer, iters, status, -}
   double* wpi;   // 2 * batch * n: power-iteration w vectors (split mode, ping-pong)
+  int* tail_act;  // hybrid: batch (active list of the tail)
+  int* tail_nact;
 };
 
 SHP_DEV double* buf(const RootArgs& a, int mat, int b) {
@@ -312,7 +315,7 @@ SHP_DEV int compact(const RootArgs& a, int* act, int nact, int k, int* cnt, bool
     const int pos = b0 + q;
     if (pos < nact) {
       const int mat = act[pos];
-      const bool keep = (!first || lam_ok(a.lam[mat])) && decide(a, mat, k) == D_CONTINUE;
+      const bool keep = (!first || lam_ok(a.lam[mat])) && decide(a, mat, k) == D_CONTINUE && k < a.k_sw;
       if (keep) mine[nm++] = mat;
     }
   }
@@ -355,6 +358,7 @@ SHP_DEV void product_stage(const RootArgs& a, const int* act, int nact, int ab, 
 }
 
 SHP_DEV void write_output(const RootArgs& a, int pbuf);
+SHP_DEV void tail_handoff(const RootArgs& a);
 
 // ---------------------------------------------------------------- kernel
 __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
@@ -501,7 +505,14 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
         int k = 0;
         for (;; ++k) {
           int d = decide(a, mat, k);
-          if (d == D_CONTINUE) continue;
+          if (d == D_CONTINUE) {
+            if (k < a.k_sw) continue;
+            status = -1;  // handed off to the 3xTF32 tail at check k_sw (root_tail.cu)
+            iters = k;
+            rbuf = -3;
+            err = a.errh[(int64_t)mat * (a.max_iter + 1) + k];
+            break;
+          }
           const double* e = a.errh + (int64_t)mat * (a.max_iter + 1);
           if (d == D_CONVERGED) { status = 0; iters = k; rbuf = BX0 + (k & 1); err = e[k]; }
           else if (d == D_STAGNATED) { status = 1; iters = k - 1; rbuf = BX0 + ((k - 1) & 1); err = e[k - 1]; }
@@ -520,10 +531,46 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
     }
   }
   grid.sync();
+  if (a.k_sw <= a.max_iter) tail_handoff(a);
   if (a.r == 1) write_output(a, -1);
   // r >= 2: root_power_kernel raises the returned iterates to the power r and
   // writes the output (a separate launch: keeping its product code out of this
   // kernel keeps the Newton loops' instruction footprint, measured 12% faster)
+}
+
+// Hybrid handoff (rows of every matrix handed off at check k_sw): X_k, M_k and
+// T_k -> fp32 (hi, lo = hi - trunc_tf32(hi)) pairs in dead regions, the layout
+// root_tail.cu iterates on (tail_region()).  Block 0 also writes the tail's
+// initial active list.
+SHP_DEV void tail_handoff(const RootArgs& a) {
+  const int np = a.np, xs = a.k_sw & 1;
+  const int tsrc = (a.p == 1 && (a.k_sw & 1)) ? BS0 : BT;
+  const int lane = threadIdx.x & 31, gw = blockIdx.x * (kRT / 32) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (kRT / 32);
+  const int64_t rows = (int64_t)a.batch * a.n;
+  const int64_t half = (int64_t)np * np;  // floats per hi (or lo) half of a region
+  for (int64_t rid = gw; rid < rows; rid += nw) {
+    const int mat = (int)(rid / a.n), i = (int)(rid - (int64_t)mat * a.n);
+    if (a.res[mat].x != -3) continue;  // warp-uniform
+    const int src[3] = {BX0 + xs, BM0 + xs, tsrc};
+    const int dst[3] = {BX0 + (xs ^ 1), BM0 + (xs ^ 1), BS1};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double* s = buf(a, mat, src[q]) + (int64_t)i * np;
+      float* h = reinterpret_cast<float*>(buf(a, mat, dst[q])) + (int64_t)i * np;
+      for (int j = lane; j < a.n; j += 32) {
+        const float v = __double2float_rn(s[j]);
+        h[j] = v;
+        h[half + j] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int c = 0;
+    for (int mat = 0; mat < a.batch; ++mat)
+      if (a.res[mat].x == -3) a.tail_act[c++] = mat;
+    *a.tail_nact = c;
+  }
 }
 
 // Final fp32 write: X_i (or its power in buffer `pbuf`), I for degenerate
@@ -586,9 +633,10 @@ static int padded(int n) { return (n + kNT - 1) / kNT * kNT; }
 
 size_t root_workspace_bytes(int batch, int n, int max_iter) {
   const size_t np = (size_t)padded(n);
+  const int chunk = batch < kMaxBatchPerLaunch ? batch : kMaxBatchPerLaunch;
   return align256((size_t)batch * kBufs * np * np * sizeof(double)) + align256((size_t)batch * sizeof(double)) +
          align256((size_t)batch * (max_iter + 1) * sizeof(double)) + align256((size_t)batch * sizeof(int4)) +
-         align256((size_t)2 * batch * n * sizeof(double));
+         align256((size_t)2 * batch * n * sizeof(double)) + root_tail_ws_bytes(chunk);
 }
 
 size_t root_smem_bytes(int n) {
@@ -598,7 +646,7 @@ size_t root_smem_bytes(int n) {
 }
 
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
-                int n, int p, int r, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
+                int n, int p, int r, int k_sw, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
                 void* ws, cudaStream_t stream, int64_t* launches) {
   static size_t configured_smem = 0;
   const size_t smem = root_smem_bytes(n);
@@ -631,6 +679,7 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     a.p = p;
     a.r = r;
     a.max_iter = max_iter;
+    a.k_sw = k_sw;
     a.power_iters = power_iters;
     a.eps_rel = eps_rel;
     a.tol = tol;
@@ -645,6 +694,10 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     a.res = reinterpret_cast<int4*>(q);
     q += align256((size_t)bc * sizeof(int4));
     a.wpi = reinterpret_cast<double*>(q);
+    q += align256((size_t)2 * bc * n * sizeof(double));
+    void* tail_maps = q;
+    a.tail_act = reinterpret_cast<int*>(q + align256((size_t)2 * 7 * 128));
+    a.tail_nact = a.tail_act + bc;
     void* args[] = {&a};
     const int grid = num_sms() * per_sm;
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);
@@ -654,6 +707,11 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
       e = cudaLaunchCooperativeKernel((const void*)root_power_kernel, dim3(grid), dim3(kRT), args, smem, stream);
       if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_power_kernel)", e);
       ++*launches;
+    }
+    if (k_sw <= max_iter) {
+      int rc = root_tail_launch(a.bufs, bc, n, np, p, max_iter, k_sw, tol, a.errh, a.res, a.info, a.X, ldx, stride_x,
+                                a.tail_act, a.tail_nact, tail_maps, stream, launches);
+      if (rc) return rc;
     }
   }
   return SHAMPOO_OK;

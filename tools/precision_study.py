@@ -9,7 +9,9 @@ same coupled Newton iteration as the oracle on fp32 Wishart statistics
   bf16      : operands rounded to bf16 (8-bit significand), fp32 accumulate/storage
   tf32      : operands rounded to tf32 (11-bit significand), fp32 accumulate/storage
   3xtf32    : hi = tf32(x), lo = tf32(x - hi); hi*hi + hi*lo + lo*hi, fp32 storage
-  hybN      : first N iterations fp64, then 3xtf32
+  3xtf32t   : the measured tcgen05 semantics: operands truncated to tf32, hi = trunc(x),
+              lo = trunc(x - hi), fp32 accumulation
+  hybN      : first N iterations fp64, then 3xtf32 (hybNt: then 3xtf32t)
 
     python tools/precision_study.py [--n 256] [--seeds 2] > profiles/r01_precision_study.txt
 """
@@ -52,7 +54,23 @@ def mm(a, b, mode):
         bl = round_mantissa(b32 - bh, 10)
         f = lambda x, y: x.astype(np.float64) @ y.astype(np.float64)
         return (f(ah, bh) + f(ah, bl) + f(al, bh)).astype(np.float32)
+    if mode == "3xtf32t":
+        # the measured tcgen05 kind::tf32 semantics (profiles/r01_tf32_probe.txt): operands TRUNCATED
+        # to tf32; hi = trunc(x), lo = x - hi (exact in fp32) is truncated again by the MMA; the three
+        # passes accumulate in fp32 (TF32 x TF32 products are exact in fp32)
+        ah = trunc_mantissa(a32, 10)
+        al = trunc_mantissa(a32 - ah, 10)
+        bh = trunc_mantissa(b32, 10)
+        bl = trunc_mantissa(b32 - bh, 10)
+        return (al @ bh + ah @ bl) + ah @ bh
     raise ValueError(mode)
+
+
+def trunc_mantissa(x, bits):
+    """Truncation (round toward zero) of fp32 values to `bits` explicit mantissa bits."""
+    u = np.asarray(x, np.float32).view(np.uint32)
+    mask = np.uint32((0xFFFFFFFF << (23 - bits)) & 0xFFFFFFFF)
+    return (u & mask).view(np.float32)
 
 
 def newton(A, p, mode, eps=1e-6, tol=1e-7, max_iter=60, fp64_iters=0):
@@ -90,8 +108,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--seeds", type=int, default=2)
+    ap.add_argument("--modes", default="fp64:0,bf16:0,tf32:0,3xtf32:0,3xtf32:6,3xtf32:8")
     args = ap.parse_args()
-    modes = [("fp64", 0), ("bf16", 0), ("tf32", 0), ("3xtf32", 0), ("3xtf32", 6), ("3xtf32", 8)]
+    modes = [(m.split(":")[0], int(m.split(":")[1])) for m in args.modes.split(",")]
     print(f"# coupled Newton, p=4, eps_rel=1e-6, n={args.n}, fp32 Wishart(n/2) statistics (kappa(A_hat)~1e6)")
     print("# relative Frobenius error of X vs eigh(A_hat)^(-1/4); north-star bar 1e-3")
     print(f"{'mode':>12} {'seed':>5} {'iters':>6} {'rel_err':>10}  verdict")
@@ -102,7 +121,7 @@ def main():
             w, V = np.linalg.eigh(Ahat)
             ref = (V * w ** -0.25) @ V.T
             err = np.linalg.norm(X - ref) / np.linalg.norm(ref)
-            name = mode if k == 0 else f"hyb{k}"
+            name = mode if k == 0 else (f"hyb{k}" + ("t" if mode.endswith("t") else ""))
             print(f"{name:>12} {s:>5} {it:>6} {err:>10.2e}  {'pass' if err <= 1e-3 else 'REJECT'}", flush=True)
 
 
