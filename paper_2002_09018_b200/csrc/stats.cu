@@ -238,22 +238,8 @@ __global__ void __launch_bounds__(kNThreads, 2)
     // ascending-k sequential sum is unchanged)
     const int kp = (int)rupd(K, 32);
     const double* base = wide + (side == 0 ? offL[b] : offR[b]);
-    // the old statistic values of this thread's outputs, loaded before the k loop
-    // so their latency hides behind the DMMAs
     float* S = stats + (side == 0 ? blk.left_off : blk.right_off);
     const int64_t ld = side == 0 ? blk.left_ld : blk.right_ld;
-    float oldv[4][4][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int i = ti * kNT + accn_row(warp, lane, mt);
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = tj * kNT + accn_col(warp, lane, nt, e);
-          oldv[mt][nt][e] = (i < nvalid && j < nvalid && i <= j) ? S[(int64_t)i * ld + j] : 0.0f;
-        }
-    }
     gemm_tile_f64(acc, base + (int64_t)ti * kNT * kp, base + (int64_t)tj * kNT * kp, kp, kp / kAsyncK, smem);
     // epilogue: EMA with the fixed rounding sequence, upper triangle + mirror
 #pragma unroll
@@ -265,7 +251,7 @@ __global__ void __launch_bounds__(kNThreads, 2)
         for (int e = 0; e < 2; ++e) {
           const int j = tj * kNT + accn_col(warp, lane, nt, e);
           if (i < nvalid && j < nvalid && i <= j) {
-            const double old = (double)oldv[mt][nt][e];
+            const double old = (double)S[(int64_t)i * ld + j];
             const double t1 = __dmul_rn(weight, acc.c[mt][nt][e]);
             const double t2 = __dmul_rn(decay, old);
             const float r = __double2float_rn(__dadd_rn(t1, t2));
@@ -278,6 +264,10 @@ __global__ void __launch_bounds__(kNThreads, 2)
 }
 
 // ------------------------------------------------ D update + graft partials
+// HBM-bound (read G, D; write D: 12 B per element).  A warp owns a row; lanes
+// take float4 column chunks (two in flight) when the row is 16-B aligned, else
+// scalars.  The numerator is summed in a fixed order (per lane, then the
+// fixed butterfly, then the warps in order).
 __global__ void __launch_bounds__(kThreads) diag_kernel(const shampoo_tensor_t* tensors,
                                                         const shampoo_block_t* blocks, const int* flag,
                                                         double* part) {
@@ -289,18 +279,43 @@ __global__ void __launch_bounds__(kThreads) diag_kernel(const shampoo_tensor_t* 
   const int rows_per = (blk.rows + kChunks - 1) / kChunks;
   const int r0 = c * rows_per, r1 = min(blk.rows, r0 + rows_per);
   double num = 0.0;
+  auto one = [&](float gf, float& d) {
+    const double g = (double)gf;
+    const double gg = __dmul_rn(g, g);
+    const float dn = __double2float_rn(__dadd_rn((double)d, gg));
+    d = dn;
+    const double den = (double)dn > 1e-30 ? (double)dn : 1e-30;
+    num = __dadd_rn(num, __ddiv_rn(gg, den));
+  };
   if (!flag[b] && ten.D != nullptr && r0 < r1) {
     for (int r = r0 + warp; r < r1; r += kThreads / 32) {
       const float* grow = ten.G + (blk.row0 + r) * ten.ldg + blk.col0;
       float* drow = ten.D + (blk.row0 + r) * ten.ldd + blk.col0;
-      for (int col = lane; col < blk.cols; col += 32) {
-        const double g = (double)__ldg(grow + col);
-        const double gg = __dmul_rn(g, g);
-        const float dn = __double2float_rn(__dadd_rn((double)drow[col], gg));
-        drow[col] = dn;
-        const double den = (double)dn > 1e-30 ? (double)dn : 1e-30;
-        num = __dadd_rn(num, __ddiv_rn(gg, den));
+      const bool vec = ((reinterpret_cast<uintptr_t>(grow) | reinterpret_cast<uintptr_t>(drow)) & 15) == 0;
+      int col = 0;
+      if (vec) {
+        const int c4 = blk.cols & ~3;
+        for (col = 4 * lane; col + 128 < c4; col += 256) {
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow + col));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow + col + 128));
+          float4 d0 = *reinterpret_cast<const float4*>(drow + col);
+          float4 d1 = *reinterpret_cast<const float4*>(drow + col + 128);
+          one(g0.x, d0.x); one(g0.y, d0.y); one(g0.z, d0.z); one(g0.w, d0.w);
+          one(g1.x, d1.x); one(g1.y, d1.y); one(g1.z, d1.z); one(g1.w, d1.w);
+          *reinterpret_cast<float4*>(drow + col) = d0;
+          *reinterpret_cast<float4*>(drow + col + 128) = d1;
+        }
+        for (; col < c4; col += 128) {
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow + col));
+          float4 d0 = *reinterpret_cast<const float4*>(drow + col);
+          one(g0.x, d0.x); one(g0.y, d0.y); one(g0.z, d0.z); one(g0.w, d0.w);
+          *reinterpret_cast<float4*>(drow + col) = d0;
+        }
+        col = c4 + lane;  // scalar tail
+      } else {
+        col = lane;
       }
+      for (; col < blk.cols; col += 32) one(__ldg(grow + col), drow[col]);
     }
   }
   num = warp_sum_fixed(num);
