@@ -195,6 +195,7 @@ def main():
     table = shp.TensorTable(Gs, Ds, Ps)
     stats = torch.zeros(plan.stats_elems, dtype=torch.float32, device=dev)
     roots = torch.zeros_like(stats)
+    roots_lo = torch.zeros_like(stats)
     nb = plan.n_blocks
     gnum = torch.zeros(nb, dtype=torch.float64, device=dev)
     gscale = torch.zeros(nb, dtype=torch.float32, device=dev)
@@ -219,9 +220,11 @@ def main():
         if ev:
             ev[2].record(stream)
         sdist.all_gather_roots(plan, roots, rank, world)
+        shp.tf32_split(roots, roots_lo)  # once per refresh: the roots' TF32 remainder for the tensor cores
+        launches[0] += 1
         if ev:
             ev[3].record(stream)
-        shp.precondition(table, plan, roots, gnum, gscale)
+        shp.precondition(table, plan, roots, gnum, gscale, roots_lo=roots_lo)
         launches[0] += shp.last_launch_count()
         if ev:
             ev[4].record(stream)
@@ -343,7 +346,7 @@ def main():
                        "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
                        "parallelism": f"root-shard{world}",
                        "root_precision": "hybrid fp64 DMMA -> 3xTF32 tcgen05 (auto switch)" if args.hybrid else "fp64 DMMA", "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
-            "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather": ph[2], "precondition": ph[3]},
+            "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather_and_roots_split": ph[2], "precondition": ph[3]},
             "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,
             "root_phase_roots_per_s": n_p4_total / (ph[1] * 1e-3),
             "newton_iters_mean": iters_mean,

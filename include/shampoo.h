@@ -250,6 +250,20 @@ int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors
                          int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
                          double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream);
 
+/* The same with the roots' TF32 remainder supplied by the caller: roots_lo =
+ * roots - trunc_tf32(roots) over the packed buffer (shampoo_tf32_split), computed
+ * once per root refresh instead of once per step (roots change every kappa
+ * steps).  roots_lo NULL = shampoo_precondition. */
+int shampoo_precondition_split(const shampoo_tensor_t* tensors_host, int32_t n_tensors,
+                               const shampoo_block_t* blocks_host, int32_t n_blocks, const float* roots,
+                               const float* roots_lo, const double* graft_num, float* graft_scale, double* den,
+                               void* workspace, size_t workspace_bytes, shampoo_stream_t stream);
+
+/* lo[i] = x[i] - trunc_tf32(x[i]) for i < n (n % 4 == 0, both 16-B aligned): the
+ * exact remainder of the TF32 split the tensor cores need (they truncate fp32
+ * operands to TF32). */
+int shampoo_tf32_split(const float* x, float* lo, int64_t n, shampoo_stream_t stream);
+
 /* ----------------------------------------- f2: momentum, step size, update
  * The tail of Algorithm 1, per block b (readings #9, #11):
  *   M_t = beta1 M_{t-1} + (1-beta1) D_t^{-1/2} o G_t               (line 12)

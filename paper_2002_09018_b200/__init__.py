@@ -261,15 +261,29 @@ def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, ow
 
 
 # -------------------------------------------------------------------- a8-a9
+def tf32_split(x: torch.Tensor, lo: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """lo = x - trunc_tf32(x) (the remainder of the tensor cores' TF32 split), e.g. of
+    the packed roots once per refresh; pass it to precondition(..., roots_lo=lo)."""
+    assert x.dtype == torch.float32 and x.is_contiguous()
+    if lo is None:
+        lo = torch.empty_like(x)
+    n = x.numel() // 4 * 4
+    check(_lib.lib().shampoo_tf32_split(x.data_ptr(), lo.data_ptr(), n, _stream_ptr(stream)))
+    return lo
+
+
 def precondition(table: TensorTable, plan: Plan, roots: torch.Tensor, graft_num: torch.Tensor | None = None,
-                 graft_scale: torch.Tensor | None = None, den: torch.Tensor | None = None, stream=None):
-    """P for every block (3xTF32 tcgen05 / FP64 DMMA) and the per-block graft scale."""
+                 graft_scale: torch.Tensor | None = None, den: torch.Tensor | None = None, stream=None,
+                 roots_lo: torch.Tensor | None = None):
+    """P for every block (3xTF32 tcgen05 / FP64 DMMA) and the per-block graft scale.
+    roots_lo: optional precomputed tf32_split(roots) (once per refresh)."""
     L = _lib.lib()
     nb = plan.n_blocks
     th, bh = table.host, plan.blocks
     wsb = L.shampoo_precondition_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb)
     ws = workspace(wsb, roots.device, "precondition")
-    check(L.shampoo_precondition(th.ctypes.data, table.n, bh.ctypes.data, nb, roots.data_ptr(),
+    check(L.shampoo_precondition_split(th.ctypes.data, table.n, bh.ctypes.data, nb, roots.data_ptr(),
+                                 roots_lo.data_ptr() if roots_lo is not None else None,
                                  graft_num.data_ptr() if graft_num is not None else None,
                                  graft_scale.data_ptr() if graft_scale is not None else None,
                                  den.data_ptr() if den is not None else None, ws.data_ptr(), ws.numel(),

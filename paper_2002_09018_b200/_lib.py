@@ -40,7 +40,8 @@ EXPORTED = [
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_inverse_pth_root_batched_hybrid",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
-    "shampoo_precondition_workspace_bytes", "shampoo_precondition",
+    "shampoo_precondition_workspace_bytes", "shampoo_precondition", "shampoo_precondition_split",
+    "shampoo_tf32_split",
     "shampoo_momentum_workspace_bytes", "shampoo_momentum_step",
     "shampoo_tensor_plan", "shampoo_tensor_stats_workspace_bytes", "shampoo_tensor_stats_update",
     "shampoo_tensor_precondition_workspace_bytes", "shampoo_tensor_precondition",
@@ -98,6 +99,10 @@ def lib():
     L.shampoo_precondition_workspace_bytes.restype = _sz
     L.shampoo_precondition.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     L.shampoo_precondition.restype = ctypes.c_int
+    L.shampoo_precondition_split.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    L.shampoo_precondition_split.restype = ctypes.c_int
+    L.shampoo_tf32_split.argtypes = [_vp, _vp, _i64, _vp]
+    L.shampoo_tf32_split.restype = ctypes.c_int
     L.shampoo_momentum_workspace_bytes.argtypes = [_i32]
     L.shampoo_momentum_workspace_bytes.restype = _sz
     L.shampoo_momentum_step.argtypes = [_vp, _vp, _i32, _vp, _i32, _dbl, _dbl, _i32, _vp, _vp, _sz, _vp]

@@ -256,6 +256,23 @@ size_t shampoo_precondition_workspace_bytes(const shampoo_tensor_t* tensors_host
 int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors, const shampoo_block_t* blocks_host,
                          int32_t n_blocks, const float* roots, const double* graft_num, float* graft_scale,
                          double* den, void* workspace, size_t workspace_bytes, shampoo_stream_t stream) {
+  return shampoo_precondition_split(tensors_host, n_tensors, blocks_host, n_blocks, roots, nullptr, graft_num,
+                                    graft_scale, den, workspace, workspace_bytes, stream);
+}
+
+int shampoo_tf32_split(const float* x, float* lo, int64_t n, shampoo_stream_t stream) {
+  g_err[0] = 0;
+  g_launches = 0;
+  if (n < 0 || (n & 3)) return set_error(SHAMPOO_ERR_INVALID_ARG, "n must be a non-negative multiple of 4");
+  if (n == 0) return SHAMPOO_OK;
+  if (!x || !lo || !aligned16(x) || !aligned16(lo)) return set_error(SHAMPOO_ERR_INVALID_ARG, "x / lo not 16-B aligned");
+  return split_flat_launch(x, lo, n, static_cast<cudaStream_t>(stream), &g_launches);
+}
+
+int shampoo_precondition_split(const shampoo_tensor_t* tensors_host, int32_t n_tensors,
+                               const shampoo_block_t* blocks_host, int32_t n_blocks, const float* roots,
+                               const float* roots_lo, const double* graft_num, float* graft_scale, double* den,
+                               void* workspace, size_t workspace_bytes, shampoo_stream_t stream) {
   g_err[0] = 0;
   g_launches = 0;
   if (n_blocks < 0 || n_tensors < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "negative counts");
@@ -269,8 +286,9 @@ int shampoo_precondition(const shampoo_tensor_t* tensors_host, int32_t n_tensors
   if (!workspace) return set_error(SHAMPOO_ERR_WORKSPACE, "null workspace");
   if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
     return set_error(SHAMPOO_ERR_WORKSPACE, "workspace not 256-B aligned");
-  return precondition_launch(tensors_host, n_tensors, blocks_host, n_blocks, roots, graft_num, graft_scale, den,
-                             workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
+  if (roots_lo && !aligned16(roots_lo)) return set_error(SHAMPOO_ERR_INVALID_ARG, "roots_lo not 16-B aligned");
+  return precondition_launch(tensors_host, n_tensors, blocks_host, n_blocks, roots, roots_lo, graft_num, graft_scale,
+                             den, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &g_launches);
 }
 
 int shampoo_tensor_plan(const int64_t* dims, const int32_t* orders, int32_t n_tensors, int32_t block_size,

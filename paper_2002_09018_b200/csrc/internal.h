@@ -37,8 +37,10 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
 size_t precondition_workspace_bytes(const shampoo_tensor_t* tensors_host, int n_tensors,
                                     const shampoo_block_t* blocks_host, int n_blocks);
 int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, const shampoo_block_t* blocks_host,
-                        int n_blocks, const float* roots, const double* graft_num, float* graft_scale, double* den,
-                        void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
+                        int n_blocks, const float* roots, const float* roots_lo, const double* graft_num,
+                        float* graft_scale, double* den, void* ws, size_t ws_bytes, cudaStream_t stream,
+                        int64_t* launches);
+int split_flat_launch(const float* x, float* lo, int64_t n, cudaStream_t stream, int64_t* launches);
 
 // momentum.cu
 size_t momentum_workspace_bytes(int n_blocks);

@@ -251,7 +251,7 @@ static size_t put(std::vector<uint8_t>& blob, const T* p, size_t n, size_t align
 
 // Builds the layout; when `ws` is null only sizes are computed (maps need real pointers).
 static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_block_t* B, int n_blocks,
-                        const float* roots, char* ws, PrecLayout& L) {
+                        const float* roots, const float* roots_lo, char* ws, PrecLayout& L) {
   std::vector<int> flags(n_blocks, 0);
   std::vector<char> t_g(n_tensors, 0), t_z(n_tensors, 0);
   size_t y_elems = 0;
@@ -301,7 +301,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
   L.off_pre = region(3 * pb);
   L.off_part = region((size_t)n_blocks * kPChunks * sizeof(double));
   L.off_Y = region(y_elems * sizeof(float));
-  L.off_rlo = region((size_t)rend * sizeof(float));
+  L.off_rlo = region(roots_lo ? 0 : (size_t)rend * sizeof(float));
   std::vector<size_t> goff(n_tensors, 0), zoff(n_tensors, 0);
   size_t gsz = 0, zsz = 0;
   for (int t = 0; t < n_tensors; ++t) {
@@ -324,7 +324,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
     return (int)maps.size() - 1;
   };
   const float* rhi = roots;  // raw fp32 roots: the tensor core reads trunc_tf32
-  float* rlo = reinterpret_cast<float*>(ws + L.off_rlo);
+  float* rlo = roots_lo ? const_cast<float*>(roots_lo) : reinterpret_cast<float*>(ws + L.off_rlo);
   std::vector<int> run_map_hi(runs.size()), run_map_lo(runs.size());
   for (size_t i = 0; i < runs.size(); ++i) {
     const RootRun& r = runs[i];
@@ -369,7 +369,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
     }
   }
   // roots: the whole packed range (a multiple of 4 floats) as one flat segment
-  if (rend) segs.push_back({roots, rlo, rend});
+  if (rend && !roots_lo) segs.push_back({roots, rlo, rend});  // else: the caller's precomputed split
   // ---- jobs
   std::vector<TcJob> j1, j2;
   int64_t t1 = 0, t2 = 0;
@@ -445,20 +445,21 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
 size_t precondition_workspace_bytes(const shampoo_tensor_t* tensors_host, int n_tensors,
                                     const shampoo_block_t* blocks_host, int n_blocks) {
   PrecLayout L;
-  build_layout(tensors_host, n_tensors, blocks_host, n_blocks, nullptr, nullptr, L);
+  build_layout(tensors_host, n_tensors, blocks_host, n_blocks, nullptr, nullptr, nullptr, L);
   return L.total;
 }
 
 int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, const shampoo_block_t* blocks_host,
-                        int n_blocks, const float* roots, const double* graft_num, float* graft_scale, double* den,
-                        void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches) {
+                        int n_blocks, const float* roots, const float* roots_lo, const double* graft_num,
+                        float* graft_scale, double* den, void* ws, size_t ws_bytes, cudaStream_t stream,
+                        int64_t* launches) {
   if (n_blocks == 0) return SHAMPOO_OK;
   PrecLayout L;
-  build_layout(tensors_host, n_tensors, blocks_host, n_blocks, nullptr, nullptr, L);
+  build_layout(tensors_host, n_tensors, blocks_host, n_blocks, nullptr, roots_lo, nullptr, L);
   if (ws_bytes < L.total)
     return set_error(SHAMPOO_ERR_WORKSPACE, "precondition workspace: have %zu bytes, need %zu", ws_bytes, L.total);
   char* w = static_cast<char*>(ws);
-  int rc = build_layout(tensors_host, n_tensors, blocks_host, n_blocks, roots, w, L);
+  int rc = build_layout(tensors_host, n_tensors, blocks_host, n_blocks, roots, roots_lo, w, L);
   if (rc) return rc;
   if (cudaMemcpyAsync(w, L.blob.data(), L.blob.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess)
     return set_cuda_error("cudaMemcpyAsync(precondition tables)");

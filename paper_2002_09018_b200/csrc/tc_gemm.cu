@@ -240,6 +240,27 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const SplitSeg* __restr
   }
 }
 
+// one flat range (the caller-facing shampoo_tf32_split): no table, arguments by value
+__global__ void __launch_bounds__(256) tf32_split_flat_kernel(const float* __restrict__ x, float* __restrict__ lo,
+                                                              int64_t n) {
+  const float4* src = reinterpret_cast<const float4*>(x);
+  float4* dst = reinterpret_cast<float4*>(lo);
+  const int64_t n4 = n >> 2, step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += step) {
+    const float4 v = __ldg(src + i);
+    dst[i] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
+  }
+}
+
+int split_flat_launch(const float* x, float* lo, int64_t n, cudaStream_t stream, int64_t* launches) {
+  if (n == 0) return SHAMPOO_OK;
+  tf32_split_flat_kernel<<<8 * num_sms(), 256, 0, stream>>>(x, lo, n);
+  ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("tf32_split_flat_kernel", e);
+  return SHAMPOO_OK;
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

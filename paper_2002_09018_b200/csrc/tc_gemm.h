@@ -44,5 +44,6 @@ int make_map_f32(CUtensorMap* out, const void* base, int dims, const uint64_t* s
 int tc_gemm_launch(const TcJob* jobs_dev, int n_jobs, int64_t total_tiles, const CUtensorMap* maps_dev,
                    cudaStream_t stream, int64_t* launches);
 int tf32_split_launch(const SplitSeg* segs_dev, int n_segs, cudaStream_t stream, int64_t* launches);
+int split_flat_launch(const float* x, float* lo, int64_t n, cudaStream_t stream, int64_t* launches);
 
 }  // namespace shp

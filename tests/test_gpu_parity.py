@@ -402,6 +402,32 @@ def test_precondition_determinism(shp):
     assert torch.equal(P1, P2)
 
 
+def test_precondition_with_precomputed_roots_split(shp):
+    """shampoo_precondition_split with roots_lo = tf32_split(roots) (once per
+    refresh) gives bit-identical P and scales to the per-call split; the split
+    itself equals x - trunc_tf32(x) computed on the host."""
+    shapes = [(1024, 1024), (300, 2048), (32000 // 16, 1024)]
+    pl = shp.make_plan(shapes, 1024, 8192, 1)
+    Gs = [torch.from_numpy(synth.lowrank_gradient(m, n, 7 + m)).to(DEV) for m, n in shapes]
+    roots = torch.randn(pl.stats_elems, device=DEV) * 0.05
+    lo = shp.tf32_split(roots)
+    r = roots.cpu().numpy()
+    want = r - (r.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    assert np.array_equal(lo.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    gn = torch.ones(pl.n_blocks, dtype=torch.float64, device=DEV)
+    outs = []
+    for roots_lo in (None, lo):
+        Ps = [torch.zeros_like(G) for G in Gs]
+        sc = torch.zeros(pl.n_blocks, device=DEV)
+        shp.precondition(shp.TensorTable(Gs, [torch.ones_like(G) for G in Gs], Ps), pl, roots, gn, sc,
+                         roots_lo=roots_lo)
+        torch.cuda.synchronize()
+        outs.append((Ps, sc))
+    for P1, P2 in zip(outs[0][0], outs[1][0]):
+        assert torch.equal(P1, P2)
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
 def test_root_results_independent_of_batch_size(shp):
     """A root must not depend on which other matrices share its launch: small
     batches split each matrix's power iteration over several CTAs, large ones
