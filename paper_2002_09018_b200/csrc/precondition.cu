@@ -293,7 +293,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
   size_t q = 0;
   auto region = [&](size_t bytes) { size_t o = q; q = al(q + bytes); return o; };
   // header blob size is unknown until maps are built; reserve generously
-  const size_t n_maps_max = 2 * runs.size() + 4 * (size_t)n_tensors;
+  const size_t n_maps_max = 4 * runs.size() + 4 * (size_t)n_tensors;
   const size_t hdr = al((size_t)n_tensors * sizeof(shampoo_tensor_t)) + al((size_t)n_blocks * sizeof(shampoo_block_t)) +
                      al((size_t)n_blocks * sizeof(int)) + al(n_maps_max * sizeof(CUtensorMap)) +
                      2 * al((size_t)n_blocks * sizeof(TcJob)) + al(((size_t)n_tensors + 64) * sizeof(SplitSeg)) + 4096;
@@ -316,30 +316,34 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
 
   // ---- tensor maps
   std::vector<CUtensorMap> maps;
-  auto add_map = [&](const void* base, int dims, const uint64_t* size, const uint64_t* strides) -> int {
+  auto add_map = [&](const void* base, int dims, const uint64_t* size, const uint64_t* strides,
+                     int box = 128) -> int {
     CUtensorMap m;
-    int rc = make_map_f32(&m, base, dims, size, strides, 128);
+    int rc = make_map_f32(&m, base, dims, size, strides, box);
     if (rc) return -1;
     maps.push_back(m);
     return (int)maps.size() - 1;
   };
   const float* rhi = roots;  // raw fp32 roots: the tensor core reads trunc_tf32
   float* rlo = roots_lo ? const_cast<float*>(roots_lo) : reinterpret_cast<float*>(ws + L.off_rlo);
-  std::vector<int> run_map_hi(runs.size()), run_map_lo(runs.size());
+  std::vector<int> run_map_hi(runs.size()), run_map_lo(runs.size()), run_map_hib(runs.size()),
+      run_map_lob(runs.size());  // ...b: the B-operand (kTcGemmBN-row box) variants
   for (size_t i = 0; i < runs.size(); ++i) {
     const RootRun& r = runs[i];
     uint64_t size[3] = {(uint64_t)r.n, (uint64_t)r.n, (uint64_t)r.count};
     uint64_t st[2] = {(uint64_t)r.ld * 4, (uint64_t)r.stride * 4};
     run_map_hi[i] = add_map(rhi + r.off0, 3, size, st);
     run_map_lo[i] = add_map(rlo + r.off0, 3, size, st);
-    if (run_map_hi[i] < 0 || run_map_lo[i] < 0) return SHAMPOO_ERR_CUDA;
+    run_map_hib[i] = add_map(rhi + r.off0, 3, size, st, kTcGemmBN);
+    run_map_lob[i] = add_map(rlo + r.off0, 3, size, st, kTcGemmBN);
+    if (run_map_hi[i] < 0 || run_map_lo[i] < 0 || run_map_hib[i] < 0 || run_map_lob[i] < 0) return SHAMPOO_ERR_CUDA;
   }
-  auto find_root = [&](int64_t off, int& map_hi, int& map_lo, int& z) {
+  auto find_root = [&](int64_t off, int& map_hi, int& map_lo, int& z, bool as_b) {
     for (size_t i = 0; i < runs.size(); ++i) {
       const RootRun& r = runs[i];
       if (off >= r.off0 && off < r.off0 + (int64_t)r.count * r.stride) {
-        map_hi = run_map_hi[i];
-        map_lo = run_map_lo[i];
+        map_hi = as_b ? run_map_hib[i] : run_map_hi[i];
+        map_lo = as_b ? run_map_lob[i] : run_map_lo[i];
         z = (int)((off - r.off0) / r.stride);
         return;
       }
@@ -363,8 +367,8 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
       float* zl = reinterpret_cast<float*>(ws + L.off_zlo + zoff[t]);
       uint64_t size[2] = {(uint64_t)T[t].m, (uint64_t)T[t].n};
       uint64_t st[1] = {(uint64_t)ldz * 4};
-      z_hi[t] = add_map(zh, 2, size, st);
-      z_lo[t] = add_map(zl, 2, size, st);
+      z_hi[t] = add_map(zh, 2, size, st, kTcGemmBN);
+      z_lo[t] = add_map(zl, 2, size, st, kTcGemmBN);
       if (z_hi[t] < 0 || z_lo[t] < 0) return SHAMPOO_ERR_CUDA;
     }
   }
@@ -377,13 +381,13 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
     if (!flags[b]) continue;
     const shampoo_block_t& bk = B[b];
     const shampoo_tensor_t& tt = T[bk.tensor_id];
-    const int tm = (bk.rows + 127) / 128, tn = (bk.cols + 127) / 128;
+    const int tm = (bk.rows + 127) / 128, tn = (bk.cols + kTcGemmBN - 1) / kTcGemmBN;
     TcJob j;
     std::memset(&j, 0, sizeof j);
     // phase 1: C = G_b . X_R   (M = rows, N = cols, K = cols)
     j.a = {g_hi[bk.tensor_id], g_lo[bk.tensor_id], (int32_t)bk.col0, (int32_t)bk.row0, 0, 2};
     int mh = -1, ml = -1, z = 0;
-    find_root(bk.right_off, mh, ml, z);
+    find_root(bk.right_off, mh, ml, z, true);
     j.b = {mh, ml, 0, 0, z, 3};
     j.M = bk.rows;
     j.N = bk.cols;
@@ -409,7 +413,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
       // phase 2: P = X_L . Z   (B_j[k] = Zt[col0 + j][row0 + k]; K = rows)
       TcJob k2;
       std::memset(&k2, 0, sizeof k2);
-      find_root(bk.left_off, mh, ml, z);
+      find_root(bk.left_off, mh, ml, z, false);
       k2.a = {mh, ml, 0, 0, z, 3};
       k2.b = {z_hi[bk.tensor_id], z_lo[bk.tensor_id], (int32_t)bk.row0, (int32_t)bk.col0, 0, 2};
       k2.M = bk.rows;

@@ -28,10 +28,15 @@
 
 namespace shp {
 
-constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;  // BK in fp32 elements (128 bytes)
-constexpr int kTcStages = 3;
-constexpr int kTcTileBytes = kTcBM * kTcBK * 4;      // 16 KB
-constexpr int kTcStageBytes = 4 * kTcTileBytes;      // A_hi, A_lo, B_hi, B_lo
+// 128 x 256 output tiles: per 32-deep k-tile the MMAs read 4 KB of A and 8 KB
+// of B per 128x256x8 step (180 cycles) and TMA writes 96 KB per 2160 MMA
+// cycles -- ~112 B/clk of shared-memory traffic, under the 128 B/clk port
+// (128 x 128 tiles needed ~150 B/clk and were shared-memory bound at 64%).
+constexpr int kTcBM = 128, kTcBN = 256, kTcBK = 32;  // BK in fp32 elements (128 bytes)
+constexpr int kTcStages = 2;
+constexpr int kTcTileBytes = kTcBM * kTcBK * 4;      // 16 KB (A)
+constexpr int kTcBTileBytes = kTcBN * kTcBK * 4;     // 32 KB (B)
+constexpr int kTcStageBytes = 2 * kTcTileBytes + 2 * kTcBTileBytes;  // A_hi, A_lo, B_hi, B_lo
 constexpr int kTcThreads = 192;
 constexpr uint32_t kTcTmemCols = 2 * kTcBN;          // two fp32 accumulators
 
@@ -113,8 +118,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           uint8_t* st = smem + stage * kTcStageBytes;
           tc::mbar_arrive_expect_tx(full + stage, kTcStageBytes);
           tc_load_operand(job.a, maps, st, st + kTcTileBytes, full + stage, kt * kTcBK, ti * kTcBM);
-          tc_load_operand(job.b, maps, st + 2 * kTcTileBytes, st + 3 * kTcTileBytes, full + stage, kt * kTcBK,
-                          tj * kTcBN);
+          tc_load_operand(job.b, maps, st + 2 * kTcTileBytes, st + 2 * kTcTileBytes + kTcBTileBytes, full + stage,
+                          kt * kTcBK, tj * kTcBN);
           if (++stage == kTcStages) {
             stage = 0;
             phase ^= 1;
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t s0 = tc::smem_u32(smem + stage * kTcStageBytes);
           const uint64_t a_hi = tc::umma_desc_sw128(s0), a_lo = tc::umma_desc_sw128(s0 + kTcTileBytes);
           const uint64_t b_hi = tc::umma_desc_sw128(s0 + 2 * kTcTileBytes);
-          const uint64_t b_lo = tc::umma_desc_sw128(s0 + 3 * kTcTileBytes);
+          const uint64_t b_lo = tc::umma_desc_sw128(s0 + 2 * kTcTileBytes + kTcBTileBytes);
 #pragma unroll
           for (int k = 0; k < kTcBK / 8; ++k) {
             const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // 32 bytes per K=8 step
@@ -189,9 +194,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (row_ok) {
           if (job.out_mode == 0) {
             float* o = job.out_hi + (int64_t)i * job.ld_out + j0;
+            if (j0 + 16 <= job.N && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+              // 16-byte stores: lanes hold different rows, so this quarters the
+              // number of scattered store transactions
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              if (j0 + e < job.N) o[e] = __uint_as_float(r[e]);
+              for (int q = 0; q < 4; ++q)
+                reinterpret_cast<float4*>(o)[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                              __uint_as_float(r[4 * q + 2]),
+                                                              __uint_as_float(r[4 * q + 3]));
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (j0 + e < job.N) o[e] = __uint_as_float(r[e]);
+            }
           } else {
 #pragma unroll
             for (int e = 0; e < 16; ++e)

@@ -15,7 +15,8 @@ struct TcOperand {
   int32_t dims;            // 2 or 3
 };
 
-// C[M x N] = A[M x K] . B[N x K]^T over 128x128 tiles (tiles_n = ceil(N/128)).
+// C[M x N] = A[M x K] . B[N x K]^T over 128x256 tiles (tiles_n = ceil(N/256)).
+// A maps use a 128-row TMA box, B maps a kTcGemmBN-row box.
 // out_mode 0: out_hi[i*ld + j] = C;  1: out_hi[j*ld + i] = C, out_lo[j*ld + i] = C - trunc_tf32(C).
 struct TcJob {
   TcOperand a, b;
@@ -38,6 +39,7 @@ struct SplitSeg {
   int64_t n;
 };
 
+constexpr int kTcGemmBN = 256;  // output tile columns (= B box rows)
 size_t tc_gemm_smem_bytes();
 int make_map_f32(CUtensorMap* out, const void* base, int dims, const uint64_t* size, const uint64_t* stride_bytes,
                  int box_rows);
