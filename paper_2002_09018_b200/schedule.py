@@ -26,7 +26,7 @@ import math
 
 import torch
 
-from . import Plan, inverse_pth_root_ptr, new_info
+from . import Plan, inverse_pth_root_ptr, new_info, tf32_split
 from .dist import all_gather_roots
 
 
@@ -41,6 +41,9 @@ class DelayedRefresh:
         self.group = group
         self.current = roots                       # roots the step uses (stale by <= 2 kappa)
         self.next = torch.zeros_like(roots)        # roots being built from the last snapshot
+        # TF32 remainder of the current roots for shampoo_precondition_split,
+        # recomputed only when roots are adopted (once per kappa steps)
+        self.current_lo = tf32_split(self.current)
         seg = plan.segment_elems
         self.seg0 = rank * seg
         self.snapshot = torch.empty(seg, dtype=stats.dtype, device=stats.device)
@@ -94,6 +97,7 @@ class DelayedRefresh:
         if t % self.kappa == 0:
             if self.ready:
                 self.current, self.next = self.next, self.current
+                tf32_split(self.current, self.current_lo, stream)
                 self.ready = False
                 adopted = True
             seg = self.plan.segment_elems

@@ -191,3 +191,50 @@ def test_resnet50_full_plan_sampled_blocks(shp):
                 n, off, ld = b.extent[i], b.off[i], b.ld[i]
                 assert np.array_equal(sg[off:off + n * ld].view(np.uint32), so[off:off + n * ld].view(np.uint32))
         assert gnc[bi] == pytest.approx(num_o[bi], rel=1e-12)
+
+
+def test_resnet50_full_step_sampled_precondition(shp):
+    """ResNet-50 at full size: statistics, every root on the GPU (tensor plan
+    groups, p in {2, 4, 8}), preconditioning; the oracle recomputes P for a
+    sample of blocks from the GPU's fp32 roots (kernel-isolated, bar 1e-5) and
+    the roots of the sample from the GPU statistics (bar 2e-6)."""
+    named = synth.resnet50_shapes()
+    shapes = [s for _, s in named]
+    Gs = [synth.conv_gradient(s, synth.BASE_SEED + 26 + i) for i, s in enumerate(shapes)]
+    pl = shp.make_tensor_plan(shapes, 1024, 8192, 1)
+    po = ot.plan(shapes, 1024, 8192, 1)
+    Gd = [torch.from_numpy(G).to(DEV) for G in Gs]
+    Dd = [torch.zeros(s, dtype=torch.float32, device=DEV) for s in shapes]
+    Pd = [torch.zeros(s, dtype=torch.float32, device=DEV) for s in shapes]
+    table = shp.TTensorTable(Gd, Dd, Pd)
+    stats = torch.zeros(pl.stats_elems, dtype=torch.float32, device=DEV)
+    gn = torch.zeros(pl.n_blocks, dtype=torch.float64, device=DEV)
+    shp.tensor_stats_update(table, pl, stats, 1.0, 1.0, -1, gn)
+    roots = torch.zeros_like(stats)
+    infos = shp.refresh_group_roots(pl, stats, roots, 0)
+    sc = torch.zeros(pl.n_blocks, dtype=torch.float32, device=DEV)
+    shp.tensor_precondition(table, pl, roots, gn, sc)
+    torch.cuda.synchronize()
+    for _, info in infos:
+        assert set(shp.info_to_numpy(info)["status"].tolist()) <= {0, 1}
+    names = [n for n, _ in named]
+    want = {names.index("conv1"), names.index("layer2.1.conv2"), names.index("layer1.0.conv3"),
+            names.index("layer3.0.conv1.bn.beta")}
+    sample = [b.block_index for b in po.blocks if b.tensor_id in want]
+    sg, rg = stats.cpu().numpy(), roots.cpu().numpy()
+    for bi in sample:
+        b = po.blocks[bi]
+        for i in range(b.order):
+            if b.p[i]:
+                n, off, ld = b.extent[i], b.off[i], b.ld[i]
+                Xo, _ = oroot.inverse_pth_root(ot.root_view(sg, off, n, ld).astype(np.float64), b.p[i])
+                assert rel(ot.root_view(rg, off, n, ld), Xo) < 2e-6
+    Ds = [D.cpu().numpy() for D in Dd]
+    Po, sco, _ = ot.precondition_plan(Gs, Ds, po, rg.astype(np.float64), gn.cpu().numpy(), blocks=sample)
+    scg = sc.cpu().numpy()
+    for bi in sample:
+        b = po.blocks[bi]
+        t = b.tensor_id
+        sl = b.slices()
+        assert rel(Pd[t].cpu().numpy()[sl], Po[t][sl]) < 1e-5
+        assert scg[bi] == pytest.approx(sco[bi], rel=1e-5)

@@ -50,21 +50,25 @@ def timed(fn, n):
     return e0.elapsed_time(e1) / n
 
 
+roots_lo = shp.tf32_split(roots)
+
+
 def plain(t):
     shp.stats_update(table, plan, stats, 1.0, 1.0, -1, gn)
-    shp.precondition(table, plan, roots, gn, sc)
+    shp.precondition(table, plan, roots, gn, sc, roots_lo=roots_lo)
 
 
 def delayed(t):
     shp.stats_update(table, plan, stats, 1.0, 1.0, -1, gn)
     dr.step(t)
-    shp.precondition(table, plan, dr.current, gn, sc)
+    shp.precondition(table, plan, dr.current, gn, sc, roots_lo=dr.current_lo)
 
 
 def synchronous(t):
     shp.stats_update(table, plan, stats, 1.0, 1.0, -1, gn)
     shp.refresh_group_roots(plan, stats, roots, 0)
-    shp.precondition(table, plan, roots, gn, sc)
+    shp.tf32_split(roots, roots_lo)
+    shp.precondition(table, plan, roots, gn, sc, roots_lo=roots_lo)
 
 
 for fn in (plain, delayed):

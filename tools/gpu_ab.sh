@@ -1,5 +1,5 @@
 for i in 1 2; do
-  (cd abtest/old && python tools/profile_stats.py --reps 5) 2>&1 | tail -1 | sed "s/^/old: /"
-  python tools/profile_stats.py --reps 5 2>&1 | tail -1 | sed 's/^/new: /'
+  (cd abtest/old && python tools/profile_root.py --batch 296 --reps 2 && python tools/profile_stats.py --reps 3) 2>&1 | grep -E "roots/s|stats:" | sed "s/^/old: /"
+  (python tools/profile_root.py --batch 296 --reps 2 && python tools/profile_stats.py --reps 3) 2>&1 | grep -E "roots/s|stats:" | sed 's/^/new: /'
 done
-timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "stats" 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
