@@ -216,6 +216,21 @@ int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t
                                             shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
                                             shampoo_stream_t stream);
 
+/* Ozaki precision: every coupled-Newton product on the INT8
+ * tensor cores with fp64-level accuracy -- each fp64 operand is split per row
+ * into 7 int8 slices (2^-49 relative to the row maximum), the 28 slice products
+ * with s + t <= 8 accumulate EXACTLY in int32 TMEM accumulators
+ * (tcgen05.mma.kind::i8), and the epilogue combines them in fp64.  Iterates,
+ * power iteration, ridge, stopping rule and statuses are those of
+ * shampoo_inverse_pth_root_batched (p-th roots, r = 1); the workspace is larger
+ * (shampoo_root_ozaki_workspace_bytes: + 5 x 7 int8 planes per matrix). */
+size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter);
+int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                           int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                           double tol, int32_t max_iter, int32_t power_iters,
+                                           shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
+                                           shampoo_stream_t stream);
+
 /* Independent root check (config 2, north-star invariant):
  *   residual_i = || X_i^p (A_i + eps_rel*lambda_i*I) - I ||_F   in fp64,
  * lambda_i = info[i].lambda_max from the root call.  out: double[batch]. */

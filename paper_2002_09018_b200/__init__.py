@@ -170,8 +170,18 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
                          max_iter: int = 100, power_iters: int = 100, device=None, stream=None, r: int = 1,
                          fp64_iters: int | None = None):
     """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry).
-    fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch)."""
+    fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch);
+    fp64_iters="ozaki": every product on the INT8 tensor cores with fp64-level accuracy."""
     L = _lib.lib()
+    if fp64_iters == "ozaki":
+        if r != 1:
+            raise ValueError("the ozaki root serves r = 1 only")
+        wsb = L.shampoo_root_ozaki_workspace_bytes(batch, n, p, max_iter)
+        ws = workspace(wsb, device if device is not None else info.device, "root")
+        check(L.shampoo_inverse_pth_root_batched_ozaki(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
+                                                       tol, max_iter, power_iters, info.data_ptr(), ws.data_ptr(),
+                                                       ws.numel(), _stream_ptr(stream)))
+        return
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
     ws = workspace(wsb, device if device is not None else info.device, "root")
     if fp64_iters is not None:

@@ -38,7 +38,8 @@ EXPORTED = [
     "shampoo_abi_version", "shampoo_last_error", "shampoo_last_launch_count", "shampoo_plan",
     "shampoo_stats_workspace_bytes", "shampoo_stats_update",
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
-    "shampoo_inverse_pth_root_batched_hybrid",
+    "shampoo_inverse_pth_root_batched_hybrid", "shampoo_root_ozaki_workspace_bytes",
+    "shampoo_inverse_pth_root_batched_ozaki",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition", "shampoo_precondition_split",
     "shampoo_tf32_split",
@@ -90,6 +91,11 @@ def lib():
     L.shampoo_inverse_pth_root_batched_hybrid.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl,
                                                           _dbl, _i32, _i32, _i32, _vp, _vp, _sz, _vp]
     L.shampoo_inverse_pth_root_batched_hybrid.restype = ctypes.c_int
+    L.shampoo_root_ozaki_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
+    L.shampoo_root_ozaki_workspace_bytes.restype = _sz
+    L.shampoo_inverse_pth_root_batched_ozaki.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl,
+                                                         _dbl, _i32, _i32, _vp, _vp, _sz, _vp]
+    L.shampoo_inverse_pth_root_batched_ozaki.restype = ctypes.c_int
     L.shampoo_root_residual_workspace_bytes.argtypes = [_i32, _i32, _i32]
     L.shampoo_root_residual_workspace_bytes.restype = _sz
     L.shampoo_root_residual_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl, _vp, _vp,

@@ -24,7 +24,7 @@ CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLU
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu", "tc_gemm.cu", "momentum.cu", "tensor.cu", "root_tail.cu"]
-HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h", "tc_common.cuh", "tc_gemm.h"]
+HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h", "tc_common.cuh", "tc_gemm.h", "ozaki.cuh"]
 
 
 def _newer(target: str, deps) -> bool:

@@ -47,6 +47,7 @@ struct RootArgs {
   int64_t ldx, stride_x;
   int batch, n, np, p, r, max_iter, power_iters;
   int k_sw;  // hybrid: matrices still iterating at check k_sw are handed to the 3xTF32 tail (> max_iter: off)
+  int handoff_fp64;  // ozaki: hand off at k_sw = 0 with the fp64 buffers left as they are
   double eps_rel, tol;
   shampoo_root_info_t* info;
   double* bufs;  // batch * kBufs * np * np
@@ -549,7 +550,7 @@ SHP_DEV void tail_handoff(const RootArgs& a) {
   const int nw = gridDim.x * (kRT / 32);
   const int64_t rows = (int64_t)a.batch * a.n;
   const int64_t half = (int64_t)np * np;  // floats per hi (or lo) half of a region
-  for (int64_t rid = gw; rid < rows; rid += nw) {
+  for (int64_t rid = gw; rid < rows && !a.handoff_fp64; rid += nw) {
     const int mat = (int)(rid / a.n), i = (int)(rid - (int64_t)mat * a.n);
     if (a.res[mat].x != -3) continue;  // warp-uniform
     const int src[3] = {BX0 + xs, BM0 + xs, tsrc};
@@ -631,12 +632,13 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static int padded(int n) { return (n + kNT - 1) / kNT * kNT; }
 
-size_t root_workspace_bytes(int batch, int n, int max_iter) {
+size_t root_workspace_bytes(int batch, int n, int max_iter, int precision) {
   const size_t np = (size_t)padded(n);
   const int chunk = batch < kMaxBatchPerLaunch ? batch : kMaxBatchPerLaunch;
   return align256((size_t)batch * kBufs * np * np * sizeof(double)) + align256((size_t)batch * sizeof(double)) +
          align256((size_t)batch * (max_iter + 1) * sizeof(double)) + align256((size_t)batch * sizeof(int4)) +
-         align256((size_t)2 * batch * n * sizeof(double)) + root_tail_ws_bytes(chunk);
+         align256((size_t)2 * batch * n * sizeof(double)) + root_tail_ws_bytes(chunk) +
+         (precision == 2 ? align256(root_ozaki_ws_bytes(chunk, n)) : 0);
 }
 
 size_t root_smem_bytes(int n) {
@@ -646,7 +648,7 @@ size_t root_smem_bytes(int n) {
 }
 
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
-                int n, int p, int r, int k_sw, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
+                int n, int p, int r, int k_sw, int precision, double eps_rel, double tol, int max_iter, int power_iters, shampoo_root_info_t* info,
                 void* ws, cudaStream_t stream, int64_t* launches) {
   static size_t configured_smem = 0;
   const size_t smem = root_smem_bytes(n);
@@ -662,8 +664,6 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     return set_error(SHAMPOO_ERR_UNSUPPORTED, "root_kernel cannot be resident (smem %zu)", smem);
   const int np = padded(n);
   char* w = static_cast<char*>(ws);
-  const size_t full = root_workspace_bytes(batch, n, max_iter);
-  (void)full;
   for (int b0 = 0; b0 < batch; b0 += kMaxBatchPerLaunch) {
     const int bc = (batch - b0 < kMaxBatchPerLaunch) ? batch - b0 : kMaxBatchPerLaunch;
     RootArgs a;
@@ -679,7 +679,8 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     a.p = p;
     a.r = r;
     a.max_iter = max_iter;
-    a.k_sw = k_sw;
+    a.k_sw = precision == 2 ? 0 : k_sw;
+    a.handoff_fp64 = precision == 2 ? 1 : 0;
     a.power_iters = power_iters;
     a.eps_rel = eps_rel;
     a.tol = tol;
@@ -698,6 +699,8 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     void* tail_maps = q;
     a.tail_act = reinterpret_cast<int*>(q + align256((size_t)2 * 7 * 128));
     a.tail_nact = a.tail_act + bc;
+    q += root_tail_ws_bytes(bc);
+    void* oz_ws = q;
     void* args[] = {&a};
     const int grid = num_sms() * per_sm;
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);
@@ -708,7 +711,11 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
       if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_power_kernel)", e);
       ++*launches;
     }
-    if (k_sw <= max_iter) {
+    if (precision == 2) {
+      int rc = root_ozaki_launch(a.bufs, bc, n, np, p, max_iter, tol, a.errh, a.res, a.info, a.X, ldx, stride_x,
+                                 a.tail_act, a.tail_nact, oz_ws, stream, launches);
+      if (rc) return rc;
+    } else if (k_sw <= max_iter) {
       int rc = root_tail_launch(a.bufs, bc, n, np, p, max_iter, k_sw, tol, a.errh, a.res, a.info, a.X, ldx, stride_x,
                                 a.tail_act, a.tail_nact, tail_maps, stream, launches);
       if (rc) return rc;

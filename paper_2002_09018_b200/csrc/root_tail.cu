@@ -17,11 +17,13 @@
 // one fp32 TMEM accumulator, TMA (SWIZZLE_128B, 3-D maps over the batch) into a
 // 3-stage ring, warp-specialised like tc_gemm.cu.
 #include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <cstring>
 
 #include "common.cuh"
 #include "internal.h"
+#include "ozaki.cuh"
 #include "tc_common.cuh"
 #include "tc_gemm.h"
 
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
 // the active list shrinks in order.  d[mat] records the decision check.
 enum { TD_CONTINUE = 0, TD_CONVERGED = 1, TD_STAGNATED = 2, TD_MAXITER = 3, TD_NONFINITE = 4 };
 
-TC_DEV int tail_decide(const double* errh, int max_iter, double tol, int mat, int k) {
+TC_DEV int tail_decide(const double* errh, int max_iter, double tol, double stag, int mat, int k) {
   const double* e = errh + (int64_t)mat * (max_iter + 1);
   const double ek = e[k];
   if (!isfinite(ek)) return TD_NONFINITE;
@@ -329,13 +331,13 @@ TC_DEV int tail_decide(const double* errh, int max_iter, double tol, int mat, in
   // reading #20, tail variant: fp32 iterates reach a noise floor where err may
   // keep creeping down; no quadratic progress (err_k >= 0.5 err_{k-1}) below
   // 1e-2 counts as stagnation
-  if (ek >= 0.5 * ep && ep < 1e-2) return TD_STAGNATED;
+  if (ek >= stag * ep && ep < 1e-2) return TD_STAGNATED;
   if (k == max_iter) return TD_MAXITER;
   return TD_CONTINUE;
 }
 
 __global__ void __launch_bounds__(1024) root_tail_decide_kernel(int* act, int* nact, const double* errh, int max_iter,
-                                                                double tol, int k) {
+                                                                double tol, double stag, int k) {
   __shared__ int cnt[1025];
   __shared__ int s_act[kTailMaxBatch];
   const int n = *nact;
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(1024) root_tail_decide_kernel(int* act, int* n
   for (int q = 0; q < per; ++q)
     if (b0 + q < n) {
       const int mat = s_act[b0 + q];
-      if (tail_decide(errh, max_iter, tol, mat, k) == TD_CONTINUE) mine[nm++] = mat;
+      if (tail_decide(errh, max_iter, tol, stag, mat, k) == TD_CONTINUE) mine[nm++] = mat;
     }
   cnt[threadIdx.x] = nm;
   __syncthreads();
@@ -370,18 +372,18 @@ __global__ void __launch_bounds__(1024) root_tail_decide_kernel(int* act, int* n
 __global__ void __launch_bounds__(128) root_tail_finish_kernel(double* bufs, const int4* res, const double* errh,
                                                                shampoo_root_info_t* info, float* X, int64_t ldx,
                                                                int64_t stride_x, int batch, int n, int np,
-                                                               int max_iter, int k_sw, double tol, int reg_x0,
-                                                               int reg_x1) {
+                                                               int max_iter, int k_sw, double tol, double stag,
+                                                               int reg_x0, int reg_x1, int fp64) {
   const int mat = blockIdx.x;
   if (mat >= batch || res[mat].x != -3) return;
   __shared__ int s_buf;
   if (threadIdx.x == 0) {
     int k = k_sw + 1, d = TD_CONTINUE;
     for (; k <= max_iter; ++k) {
-      d = tail_decide(errh, max_iter, tol, mat, k);
+      d = tail_decide(errh, max_iter, tol, stag, mat, k);
       if (d != TD_CONTINUE) break;
     }
-    if (k > max_iter) k = max_iter;  // unreachable: decide returns MAXITER at max_iter
+    if (k > max_iter) k = max_iter;  // k_sw == max_iter: decided at the handoff check
     const double* e = errh + (int64_t)mat * (max_iter + 1);
     int status, iters, kx;
     double err;
@@ -396,11 +398,12 @@ __global__ void __launch_bounds__(128) root_tail_finish_kernel(double* bufs, con
   }
   __syncthreads();
   if (s_buf < 0) return;
-  const float* src = reinterpret_cast<const float*>(bufs + ((int64_t)mat * kTailRegions + s_buf) * (int64_t)np * np);
+  const double* src64 = bufs + ((int64_t)mat * kTailRegions + s_buf) * (int64_t)np * np;
+  const float* src = reinterpret_cast<const float*>(src64);
   float* out = X + (int64_t)mat * stride_x;
   for (int64_t idx = threadIdx.x; idx < (int64_t)n * n; idx += blockDim.x) {
     const int64_t i = idx / n, j = idx - i * n;
-    out[i * ldx + j] = src[i * np + j];
+    out[i * ldx + j] = fp64 ? __double2float_rn(src64[i * np + j]) : src[i * np + j];
   }
 }
 
@@ -500,14 +503,161 @@ int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter
     s3.kcheck = k + 1;
     run(s3);
     tcur = tnext;
-    root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, ttol, k + 1);
+    root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, ttol, 0.5, k + 1);
     ++*launches;
   }
   root_tail_finish_kernel<<<batch, 128, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
-                                                     k_sw, ttol, R(TX0), R(TX1));
+                                                     k_sw, ttol, 0.5, R(TX0), R(TX1), 0);
   ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("root tail kernels", e);
+  return SHAMPOO_OK;
+}
+
+// ======================================================= Ozaki (INT8) root
+// All coupled-Newton iterations on the INT8 tensor cores (ozaki.cuh): fp64
+// iterates in root.cu's regions, every operand sliced into kS int8 planes right
+// before its product.  Slots (planes + row scales) for X_k, T, S0, S1, M_k.
+enum { OZ_SX = 0, OZ_ST = 1, OZ_SS0 = 2, OZ_SS1 = 3, OZ_SM = 4, OZ_SLOTS = 5 };
+
+size_t root_ozaki_ws_bytes(int batch, int n) {
+  const size_t np = (size_t)((n + 63) / 64 * 64);
+  const size_t planes = (size_t)OZ_SLOTS * batch * oz::kS * np * np;
+  const size_t scales = (size_t)OZ_SLOTS * batch * np * sizeof(double);
+  return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap);
+}
+
+int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
+                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
+                      int* nact, void* oz_ws, cudaStream_t stream, int64_t* launches) {
+  static bool configured = false;
+  const size_t smem = oz::gemm_smem_bytes();
+  if (!configured) {
+    if (cudaFuncSetAttribute(oz::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel)");
+    configured = true;
+  }
+  if (batch > kTailMaxBatch) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: batch chunk > %d", kTailMaxBatch);
+  if (np % 64) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: padded n must be a multiple of 64");
+  char* w = static_cast<char*>(oz_ws);
+  const size_t slot_planes = (size_t)batch * oz::kS * np * np;
+  int8_t* planes = reinterpret_cast<int8_t*>(w);
+  const size_t planes_bytes = ((size_t)OZ_SLOTS * slot_planes + 255) / 256 * 256;
+  double* scales = reinterpret_cast<double*>(w + planes_bytes);
+  const size_t scales_bytes = ((size_t)OZ_SLOTS * batch * np * sizeof(double) + 255) / 256 * 256;
+  CUtensorMap* maps_dev = reinterpret_cast<CUtensorMap*>(w + planes_bytes + scales_bytes);
+  auto slot_planes_ptr = [&](int slot) { return planes + (size_t)slot * slot_planes; };
+  auto slot_scale = [&](int slot) { return scales + (size_t)slot * batch * np; };
+  // maps: slot q -> 2q (A use, 128-row box), 2q+1 (B use, 64-row box)
+  CUtensorMap maps[2 * OZ_SLOTS];
+  {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return set_error(SHAMPOO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    for (int q2 = 0; q2 < OZ_SLOTS; ++q2) {
+      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM) != CUDA_SUCCESS ||
+          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN) != CUDA_SUCCESS)
+        return set_error(SHAMPOO_ERR_CUDA, "ozaki: cuTensorMapEncodeTiled failed");
+    }
+  }
+  if (cudaMemcpyAsync(maps_dev, maps, sizeof maps, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return set_cuda_error("cudaMemcpyAsync(ozaki maps)");
+  const int64_t mstride = (int64_t)kTailRegions * np * np;
+  auto region = [&](int r) { return bufs + (int64_t)r * np * np; };
+  const int slice_grid = 8 * num_sms();
+  auto slice = [&](int reg, int slot) {
+    oz::slice_kernel<<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
+                                                    slot_planes_ptr(slot), slot_scale(slot));
+    ++*launches;
+  };
+  oz::OzArgs base;
+  std::memset(&base, 0, sizeof base);
+  base.act = act;
+  base.nact = nact;
+  base.batch = batch;
+  base.n = n;
+  base.np = np;
+  base.tiles_m = (n + oz::kBM - 1) / oz::kBM;
+  base.tiles_n = (n + oz::kBN - 1) / oz::kBN;
+  base.sym = 1;
+  base.p = p;
+  base.errh = errh;
+  base.max_iter = max_iter;
+  auto job = [&](int sa, int sb, int out_reg) {
+    oz::OzJob j;
+    j.a_map = 2 * sa;
+    j.b_map = 2 * sb + 1;
+    j.a_scale = slot_scale(sa);
+    j.b_scale = slot_scale(sb);
+    j.out = region(out_reg);
+    j.out_stride = mstride;
+    return j;
+  };
+  const int grid = num_sms();
+  auto gemm = [&](const oz::OzArgs& a) {
+    oz::gemm_kernel<<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
+    ++*launches;
+  };
+  enum { RX0 = 0, RX1 = 1, RM0 = 2, RM1 = 3, RT = 4, RS0 = 5, RS1 = 6 };  // root.cu regions
+  const int lead = 31 - __builtin_clz((unsigned)p);
+  int treg = RT;  // region of T_k (p = 1 alternates RT / RS0, as root.cu)
+  for (int k = 0; k < max_iter; ++k) {
+    const int xs = k & 1;
+    slice(RX0 + xs, OZ_SX);
+    slice(treg, OZ_ST);
+    slice(RM0 + xs, OZ_SM);
+    // P1: X_{k+1} = X_k T ; S0 = T T (p >= 2)
+    oz::OzArgs a1 = base;
+    a1.jobs = p >= 2 ? 2 : 1;
+    a1.job[0] = job(OZ_SX, OZ_ST, RX0 + (xs ^ 1));
+    a1.job[1] = job(OZ_ST, OZ_ST, RS0);
+    gemm(a1);
+    int rb = RS0, sb = OZ_SS0;
+    if (p >= 2) slice(RS0, OZ_SS0);
+    for (int bit = lead - 1; bit >= 0; --bit) {
+      if (bit != lead - 1) {
+        const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
+        oz::OzArgs q = base;
+        q.jobs = 1;
+        q.job[0] = job(sb, sb, rd);
+        gemm(q);
+        slice(rd, sd);
+        rb = rd;
+        sb = sd;
+      }
+      if ((p >> bit) & 1) {
+        const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
+        oz::OzArgs q = base;
+        q.jobs = 1;
+        q.job[0] = job(sb, OZ_ST, rd);
+        gemm(q);
+        slice(rd, sd);
+        rb = rd;
+        sb = sd;
+      }
+    }
+    // P3: M_{k+1} = T^p M_k ; T_{k+1} ; err_{k+1}
+    const int tnext = (p == 1) ? (treg == RT ? RS0 : RT) : RT;
+    oz::OzArgs a3 = base;
+    a3.jobs = 1;
+    a3.job[0] = job(p == 1 ? OZ_ST : sb, OZ_SM, RM0 + (xs ^ 1));
+    a3.mupdate = 1;
+    a3.t_out = region(tnext);
+    a3.t_stride = mstride;
+    a3.kcheck = k + 1;
+    gemm(a3);
+    treg = tnext;
+    root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, tol, 1.0, k + 1);
+    ++*launches;
+  }
+  root_tail_finish_kernel<<<batch, 128, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
+                                                     0, tol, 1.0, RX0, RX1, 1);
+  ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("ozaki root kernels", e);
   return SHAMPOO_OK;
 }
 
