@@ -1,5 +1,10 @@
 """bench.py -- the hot path of distributed Shampoo on B200, one JSON line.
 
+Roots run in the "ozaki" precision by default (every Newton product on the INT8
+tensor cores with exact int32 accumulation of 7-slice splits, fp64-level
+accuracy); --root-precision fp64 runs them on the FP64 DMMA
+pipe, --root-precision hybrid with a 3xTF32 tail.
+
 Workload (BASELINE.json configs[2], the configuration the metric is quoted on):
 Transformer-Big (99 matrix parameters, 375.1M of P:494's 375.4M), block size
 1024, max_precond_dim 8192 -> 360 blocks, 528 inverse-4th roots + 96
@@ -40,7 +45,13 @@ KAPPA_REFRESH = 500  # root refresh interval of the paper's Transformer runs (P:
 FP64_DMMA_PEAK_TFLOPS = 37.1  # measured: tools/microbench/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)
 # dram__bytes_read.sum + dram__bytes_write.sum of root_kernel per 1024^2 p=4 matrix (20 iterations), from the
 # ncu --set full capture in profiles/r01_ncu_root_kernel.txt (148-matrix launch: 323.6 GB)
-ROOT_TRAFFIC_BYTES_PER_MATRIX = 323.626e9 / 148
+ROOT_TRAFFIC_BYTES_PER_MATRIX = (191.679e9 + 128.690e9) / 148  # profiles/root_r01h_ncu_summary.txt
+INT8_PEAK_TOPS = 2 * 1687.1  # bf16 measured (MEASURED_PEAKS.json) x the nominal int8:bf16 ratio
+# dram read + write of one Ozaki product stage per 1024^2 matrix (ncu --set full, 148-matrix dual stage)
+OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = (2.296e9 + 2.448e9) / 148
+ROOT_MODE = {"fp64": None, "ozaki": "ozaki", "hybrid": -1}
+ROOT_LABEL = {"fp64": "fp64 DMMA", "ozaki": "ozaki: INT8 tcgen05, 7 slices, exact int32 accumulation",
+              "hybrid": "hybrid fp64 DMMA -> 3xTF32 tcgen05 (auto switch)"}
 
 
 def parse():
@@ -55,8 +66,10 @@ def parse():
     ap.add_argument("--block-size", type=int, default=BLOCK,
                     help="config 5 sweep (128..4096); the metric is quoted at 1024")
     ap.add_argument("--max-precond-dim", type=int, default=MAX_PRECOND)
-    ap.add_argument("--hybrid", action="store_true",
-                    help="hybrid roots: FP64 DMMA iterations, then the 3xTF32 tcgen05 tail (DESIGN.md §6.3b)")
+    ap.add_argument("--root-precision", default="ozaki", choices=["fp64", "ozaki", "hybrid"],
+                    help="fp64: FP64 DMMA; ozaki: INT8 tensor cores with fp64-level accuracy (§6.3c); "
+                         "hybrid: FP64 DMMA then a 3xTF32 tcgen05 tail (§6.3b)")
+    ap.add_argument("--hybrid", action="store_true", help="alias of --root-precision hybrid")
     return ap.parse_args()
 
 
@@ -158,6 +171,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.hybrid:
+        args.root_precision = "hybrid"
     if args.impl == "reference":
         run_reference(args)
         return
@@ -215,7 +230,7 @@ def main():
         if ev:
             ev[1].record(stream)
         infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol,
-                                        fp64_iters=-1 if args.hybrid else None)
+                                        fp64_iters=ROOT_MODE[args.root_precision])
         launches[0] += len(infos)
         if ev:
             ev[2].record(stream)
@@ -266,7 +281,46 @@ def main():
     g4 = sorted([g for g in plan.groups_of(rank) if int(g["p"]) == 4], key=lambda g: -int(g["count"]) * int(g["n"]) ** 3)
     roof = None
     iters_mean = None
-    if g4:
+    if g4 and args.root_precision == "ozaki":
+        # the INT8 GEMM dominates: every launch bracketed by CUDA events on its stream
+        g = g4[0]
+        cnt, off, stride = int(g["count"]), int(g["offset"]), int(g["stride"])
+        gn_ = int(g["n"])
+        gld = (gn_ + 3) // 4 * 4
+        info = shp.new_info(cnt, dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        shp.profile_begin()
+        e0.record(stream)
+        shp.inverse_pth_root_ptr(stats.data_ptr() + 4 * off, gld, stride, roots.data_ptr() + 4 * off, gld, stride,
+                                 cnt, gn_, 4, info, tol=args.tol, device=dev, fp64_iters="ozaki")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gemm_ms, gemm_launches = shp.profile_end("ozaki_gemm")
+        rk_ms, _ = shp.profile_end("root_kernel")
+        call_ms = e0.elapsed_time(e1)
+        inf = shp.info_to_numpy(info)
+        iters_mean = float(inf["iters"].sum()) / cnt
+        n = gn_
+        # algorithmic int8 ops: per symmetric product 28 slice products of n^2 (n+1) (upper triangle incl.
+        # diagonal, 2 ops per multiply-add), 4 products per iteration
+        ops = float(inf["iters"].sum()) * 4 * 28 * n * n * (n + 1)
+        achieved = ops / (gemm_ms * 1e-3) / 1e12
+        peak = INT8_PEAK_TOPS
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                "frac": achieved / peak, "traffic": OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE * cnt,
+                "traffic_note": "dram bytes per launch (one symmetric product stage), ncu --set full of a 148-matrix "
+                                "stage scaled per matrix",
+                "kernel": f"oz::gemm_kernel (INT8 tcgen05 Ozaki products, batch {cnt} x {n}^2, p=4)",
+                "kernel_ms": gemm_ms / max(1, gemm_launches), "kernel_launches": gemm_launches,
+                "ops_per_launch": ops / max(1, gemm_launches),
+                "root_call_ms": call_ms, "gemm_share_of_root_call": gemm_ms / call_ms,
+                "root_kernel_ms_power_iteration_and_setup": rk_ms,
+                "fp64_equivalent_tflops": (float(inf["iters"].sum()) * 4 * n * n * (n + 1)
+                                           + cnt * 100 * 2.0 * n * n) / (call_ms * 1e-3) / 1e12,
+                "peak_source": "int8 dense = 2 x the measured bf16 1687 TF/s of MEASURED_PEAKS.json (nominal "
+                               "int8:bf16 ratio 2; NVIDIA nominal 4.5 POPS)"}
+    elif g4:
         g = g4[0]
         cnt, off, stride = int(g["count"]), int(g["offset"]), int(g["stride"])
         info = shp.new_info(cnt, dev)
@@ -345,7 +399,7 @@ def main():
                        "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
                        "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
                        "parallelism": f"root-shard{world}",
-                       "root_precision": "hybrid fp64 DMMA -> 3xTF32 tcgen05 (auto switch)" if args.hybrid else "fp64 DMMA", "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
+                       "root_precision": ROOT_LABEL[args.root_precision], "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
             "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather_and_roots_split": ph[2], "precondition": ph[3]},
             "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,
             "root_phase_roots_per_s": n_p4_total / (ph[1] * 1e-3),

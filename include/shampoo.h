@@ -371,6 +371,15 @@ int shampoo_tensor_precondition(const shampoo_ttensor_t* tensors_host, int32_t n
                                 const double* graft_num, float* graft_scale, double* den, void* workspace,
                                 size_t workspace_bytes, shampoo_stream_t stream);
 
+/* Kernel timing for measurement (bench.py's roofline): between
+ * shampoo_profile_begin() and shampoo_profile_end(), every launch of the
+ * library's dominant kernels ("root_kernel", "ozaki_gemm") on this host thread
+ * is bracketed by CUDA events recorded on its launching stream.  end()
+ * synchronizes those events and returns the summed milliseconds and the launch
+ * count of `kernel` (NULL: all). */
+int shampoo_profile_begin(void);
+int shampoo_profile_end(const char* kernel, double* ms, int64_t* launches);
+
 /* Number of kernel launches the last compute call on this host thread
  * enqueued (bench accounting, "gpu_launches"). */
 int64_t shampoo_last_launch_count(void);

@@ -417,3 +417,17 @@ def tensor_precondition(table: TTensorTable, plan: Plan, roots: torch.Tensor, gr
                                         graft_scale.data_ptr() if graft_scale is not None else None,
                                         den.data_ptr() if den is not None else None, ws.data_ptr(), ws.numel(),
                                         _stream_ptr(stream)))
+
+
+# ----------------------------------------------------------------- profiling
+def profile_begin():
+    """Bracket the library's dominant kernels with CUDA events (bench roofline)."""
+    check(_lib.lib().shampoo_profile_begin())
+
+
+def profile_end(kernel: str | None = None):
+    """-> (summed ms, launches) of `kernel` ("root_kernel", "ozaki_gemm") since profile_begin()."""
+    ms = np.zeros(1, np.float64)
+    n = np.zeros(1, np.int64)
+    check(_lib.lib().shampoo_profile_end(kernel.encode() if kernel else None, ms.ctypes.data, n.ctypes.data))
+    return float(ms[0]), int(n[0])

@@ -39,7 +39,7 @@ EXPORTED = [
     "shampoo_stats_workspace_bytes", "shampoo_stats_update",
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_inverse_pth_root_batched_hybrid", "shampoo_root_ozaki_workspace_bytes",
-    "shampoo_inverse_pth_root_batched_ozaki",
+    "shampoo_inverse_pth_root_batched_ozaki", "shampoo_profile_begin", "shampoo_profile_end",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition", "shampoo_precondition_split",
     "shampoo_tf32_split",
@@ -123,6 +123,9 @@ def lib():
     L.shampoo_tensor_precondition_workspace_bytes.restype = _sz
     L.shampoo_tensor_precondition.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     L.shampoo_tensor_precondition.restype = ctypes.c_int
+    L.shampoo_profile_begin.restype = ctypes.c_int
+    L.shampoo_profile_end.argtypes = [ctypes.c_char_p, _vp, _vp]
+    L.shampoo_profile_end.restype = ctypes.c_int
     if L.shampoo_abi_version() != 2:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "internal.h"
 
@@ -24,6 +25,31 @@ int set_error(int code, const char* fmt, ...) {
 
 int set_cuda_error(const char* what, cudaError_t e) {
   return set_error(SHAMPOO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------- profiling
+// Event pairs around launches of named kernels (bench.py's roofline timing).
+struct ProfRec {
+  const char* name;
+  cudaEvent_t e0, e1;
+};
+static thread_local bool g_prof = false;
+static thread_local std::vector<ProfRec>* g_prof_recs = nullptr;
+
+void prof_begin_launch(const char* name, cudaStream_t stream, void** token) {
+  *token = nullptr;
+  if (!g_prof) return;
+  ProfRec r{name, nullptr, nullptr};
+  cudaEventCreate(&r.e0);
+  cudaEventCreate(&r.e1);
+  cudaEventRecord(r.e0, stream);
+  g_prof_recs->push_back(r);
+  *token = reinterpret_cast<void*>(g_prof_recs->size());
+}
+
+void prof_end_launch(void* token, cudaStream_t stream) {
+  if (!g_prof || !token) return;
+  cudaEventRecord((*g_prof_recs)[reinterpret_cast<size_t>(token) - 1].e1, stream);
 }
 
 int num_sms() {
@@ -97,6 +123,36 @@ using namespace shp;
 extern "C" {
 
 int shampoo_abi_version(void) { return SHAMPOO_ABI_VERSION; }
+
+int shampoo_profile_begin(void) {
+  if (!g_prof_recs) g_prof_recs = new std::vector<ProfRec>();
+  for (auto& r : *g_prof_recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  g_prof_recs->clear();
+  g_prof = true;
+  return SHAMPOO_OK;
+}
+
+int shampoo_profile_end(const char* kernel, double* ms, int64_t* launches) {
+  g_prof = false;
+  double total = 0.0;
+  int64_t count = 0;
+  if (g_prof_recs) {
+    for (auto& r : *g_prof_recs) {
+      if (kernel && std::strcmp(kernel, r.name) != 0) continue;
+      float t = 0.0f;
+      if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&t, r.e0, r.e1) != cudaSuccess)
+        return set_cuda_error("shampoo_profile_end");
+      total += t;
+      ++count;
+    }
+  }
+  if (ms) *ms = total;
+  if (launches) *launches = count;
+  return SHAMPOO_OK;
+}
 
 const char* shampoo_last_error(void) { return g_err; }
 

@@ -64,5 +64,8 @@ int tensor_precondition_launch(const shampoo_ttensor_t* T, const shampoo_tblock_
                                void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
 
 int num_sms();
+// profiling hooks (shampoo_profile_begin/end): bracket a launch with events
+void prof_begin_launch(const char* name, cudaStream_t stream, void** token);
+void prof_end_launch(void* token, cudaStream_t stream);
 
 }  // namespace shp

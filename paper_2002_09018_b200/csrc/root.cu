@@ -703,7 +703,10 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     void* oz_ws = q;
     void* args[] = {&a};
     const int grid = num_sms() * per_sm;
+    void* tok;
+    prof_begin_launch("root_kernel", stream, &tok);
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);
+    prof_end_launch(tok, stream);
     if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_kernel)", e);
     ++*launches;
     if (r >= 2) {

@@ -598,7 +598,10 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   };
   const int grid = num_sms();
   auto gemm = [&](const oz::OzArgs& a) {
+    void* tok;
+    prof_begin_launch("ozaki_gemm", stream, &tok);
     oz::gemm_kernel<<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
+    prof_end_launch(tok, stream);
     ++*launches;
   };
   enum { RX0 = 0, RX1 = 1, RM0 = 2, RM1 = 3, RT = 4, RS0 = 5, RS1 = 6 };  // root.cu regions
