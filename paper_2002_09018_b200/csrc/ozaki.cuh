@@ -3,10 +3,10 @@
 // used by the "ozaki" precision of the coupled-Newton root.
 //
 // Slicing (per operand matrix, per row i): e_i = exponent of max_k |A_ik|
-// (frexp: max < 2^e_i), a = A_ik 2^-e_i in (-1, 1);
-//   r = a 2^6;  d_1 = rint(r);  r = (r - d_1) 2^7;  d_2 = rint(r);  ...  d_S
-// every step exact in fp64, |d_s| <= 64 (int8).  a = sum_s d_s 2^-(6+7(s-1))
-// + O(2^-(7S)).
+// (frexp: max < 2^e_i), a = A_ik 2^-e_i in (-1, 1);  V = rint(a 2^(6+7(S-1)))
+// (the only rounding, |V| < 2^48 for S = 7), then balanced base-128 digits from
+// the bottom: d_S = ((V + 64) mod 128) - 64, V = (V - d_S) / 128, ..., d_1 = V;
+// |d_s| <= 64 (int8), a = sum_s d_s 2^-(6+7(s-1)) + O(2^-(7S)).
 // Product C = A B^T (B by rows): pairs (s, t) with s + t <= S + 1 accumulate,
 // grouped by d = s + t - 2, in one int32 TMEM accumulator per d -- exact:
 // |sum| <= S * K * 64^2 < 2^31 for K <= 4096, S <= 8.  Epilogue, in fp64:
@@ -102,17 +102,25 @@ __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ s
 #pragma unroll
         for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? row[j + q] : 0.0;
       }
+      // one rounding to the 2^-48 grid (|V| < 2^48), then balanced base-128 digits
+      // by integer ops, lowest first: d = ((V + 64) mod 128) - 64, V = (V - d) / 128
+      long long V[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) r[q] = ldexp(r[q], sh);
+      for (int q = 0; q < 8; ++q) V[q] = __double2ll_rn(ldexp(r[q], sh + 7 * (kS - 1)));
+      uint32_t dig[kS][2];
 #pragma unroll
-      for (int s = 0; s < kS; ++s) {
-        uint32_t w[2] = {0u, 0u};
+      for (int s = kS - 1; s >= 0; --s) {
+        dig[s][0] = dig[s][1] = 0u;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const double d = rint(r[q]);
-          r[q] = (r[q] - d) * 128.0;
-          w[q >> 2] |= ((uint32_t)(int)d & 0xFFu) << (8 * (q & 3));
+          const long long d = s ? ((V[q] + 64) & 127) - 64 : V[q];
+          V[q] = (V[q] - d) >> 7;
+          dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
         }
+      }
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        const uint32_t w[2] = {dig[s][0], dig[s][1]};
         int8_t* dst = planes + (((int64_t)mat * kS + s) * np + i) * np + j;
         if (j + 8 <= n) {
           *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
