@@ -231,7 +231,7 @@ def main():
             ev[1].record(stream)
         infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol,
                                         fp64_iters=ROOT_MODE[args.root_precision])
-        launches[0] += len(infos)
+        launches[0] += shp.last_refresh_launch_count()
         if ev:
             ev[2].record(stream)
         sdist.all_gather_roots(plan, roots, rank, world)

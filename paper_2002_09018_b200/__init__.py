@@ -250,11 +250,21 @@ def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.
     return out
 
 
+_refresh_launches = 0
+
+
+def last_refresh_launch_count() -> int:
+    """Kernel launches enqueued by the last refresh_group_roots call (all groups)."""
+    return _refresh_launches
+
+
 def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, owner: int, eps_rel: float = 1e-6,
                         tol: float = 1e-7, max_iter: int = 100, power_iters: int = 100, infos=None, stream=None,
                         fp64_iters: int | None = None):
     """Inverse p-th roots of every statistic owned by `owner` (one batched call per
     (n, p) group); roots land at the statistics' offsets."""
+    global _refresh_launches
+    _refresh_launches = 0
     out = []
     for g in plan.groups_of(owner):
         cnt, n, p, r = int(g["count"]), int(g["n"]), int(g["p"]), int(g["r"])
@@ -264,6 +274,7 @@ def refresh_group_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, ow
         inverse_pth_root_ptr(stats.data_ptr() + 4 * off, ld, stride, roots.data_ptr() + 4 * off, ld, stride, cnt, n,
                              p, info, eps_rel, tol, max_iter, power_iters, stats.device, stream, r,
                              fp64_iters if r == 1 else None)
+        _refresh_launches += last_launch_count()
         out.append((g, info))
     if infos is not None:
         infos.extend(out)
