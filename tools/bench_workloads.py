@@ -33,6 +33,9 @@ import paper_2002_09018_b200 as shp  # noqa: E402
 import synth  # noqa: E402
 
 
+MODE = {"fp64": None, "ozaki": "ozaki", "hybrid": -1}
+
+
 def timed(fn, steps, warmup, stream):
     for _ in range(warmup):
         fn()
@@ -56,7 +59,8 @@ def config2(args, dev, stream):
         A[1::2] = torch.from_numpy(synth.psd_batch(n, 2, synth.BASE_SEED + 2 + n, "spectrum")).to(dev).repeat(64, 1, 1)
         X = torch.empty_like(A)
         info = shp.new_info(256, dev)
-        t_root = timed(lambda: shp.inverse_pth_root_batched(A, 4, X=X, info=info), args.steps, args.warmup, stream)
+        t_root = timed(lambda: shp.inverse_pth_root_batched(A, 4, X=X, info=info, fp64_iters=MODE[args.root_precision]),
+                       args.steps, args.warmup, stream)
         res_box = {}
 
         def resid():
@@ -94,7 +98,7 @@ def config4(args, dev, stream):
         box = {}
 
         def roots_fn():
-            box["i"] = shp.refresh_group_roots(plan, stats, roots, 0)
+            box["i"] = shp.refresh_group_roots(plan, stats, roots, 0, fp64_iters=MODE[args.root_precision])
         t_roots = timed(roots_fn, args.steps, args.warmup, stream)
         t_prec = timed(lambda: shp.precondition(table, plan, roots, gn, sc), args.steps, args.warmup, stream)
         iters = np.concatenate([shp.info_to_numpy(i)["iters"] for _, i in box["i"]])
@@ -126,7 +130,7 @@ def resnet50(args, dev, stream):
     box = {}
 
     def roots_fn():
-        box["i"] = shp.refresh_group_roots(plan, stats, roots, 0)
+        box["i"] = shp.refresh_group_roots(plan, stats, roots, 0, fp64_iters=MODE[args.root_precision])
     t_roots = timed(roots_fn, args.steps, args.warmup, stream)
     t_prec = timed(lambda: shp.tensor_precondition(table, plan, roots, gn, sc), args.steps, args.warmup, stream)
     iters = np.concatenate([shp.info_to_numpy(i)["iters"] for _, i in box["i"]])
@@ -158,13 +162,15 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--block-size", type=int, default=1024)
+    ap.add_argument("--root-precision", default="ozaki", choices=["fp64", "ozaki", "hybrid"])
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     fn = {"config2": config2, "config4": config4, "resnet50": resnet50}[args.workload]
     out = fn(args, dev, stream)
-    out.update({"steps": args.steps, "warmup": args.warmup, "data": "synthetic", "gpu": torch.cuda.get_device_name()})
+    out.update({"steps": args.steps, "warmup": args.warmup, "data": "synthetic", "gpu": torch.cuda.get_device_name(),
+                "root_precision": args.root_precision})
     print(json.dumps(out), flush=True)
 
 
