@@ -33,11 +33,12 @@ from .dist import all_gather_roots
 class DelayedRefresh:
     def __init__(self, plan: Plan, stats: torch.Tensor, roots: torch.Tensor, rank: int = 0, world_size: int = 1,
                  kappa: int = 500, spread: int | None = None, eps_rel: float = 1e-6, tol: float = 1e-7,
-                 max_iter: int = 100, power_iters: int = 100, group=None):
+                 max_iter: int = 100, power_iters: int = 100, group=None, fp64_iters=None):
         self.plan, self.stats, self.rank, self.world = plan, stats, rank, world_size
         self.kappa = int(kappa)
         self.spread = max(1, min(int(spread if spread is not None else kappa), self.kappa))
         self.kw = dict(eps_rel=eps_rel, tol=tol, max_iter=max_iter, power_iters=power_iters)
+        self.fp64_iters = fp64_iters  # root precision: None (FP64 DMMA), "ozaki", or a hybrid switch
         self.group = group
         self.current = roots                       # roots the step uses (stale by <= 2 kappa)
         self.next = torch.zeros_like(roots)        # roots being built from the last snapshot
@@ -87,7 +88,7 @@ class DelayedRefresh:
             src = self.snapshot.data_ptr() + 4 * (off - self.seg0)
             dst = self.next.data_ptr() + 4 * off
             inverse_pth_root_ptr(src, ld, stride, dst, ld, stride, n, nn, p, info, device=self.stats.device,
-                                 stream=stream, r=r, **self.kw)
+                                 stream=stream, r=r, fp64_iters=self.fp64_iters if r == 1 else None, **self.kw)
             self.infos.append((g, i, n, info))
 
     def step(self, t: int, stream=None) -> bool:

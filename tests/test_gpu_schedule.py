@@ -20,14 +20,15 @@ def _setup(shp, shapes, block):
 
 
 @pytest.mark.gpu
-def test_delayed_refresh_matches_synchronous_refresh_of_snapshot():
+@pytest.mark.parametrize("precision", [None, "ozaki"])
+def test_delayed_refresh_matches_synchronous_refresh_of_snapshot(precision):
     import paper_2002_09018_b200 as shp
     from paper_2002_09018_b200.schedule import DelayedRefresh
     shapes = [(256, 384), (128, 128), (300, 200)]
     plan, Gs, table, stats = _setup(shp, shapes, 128)
     roots = torch.zeros_like(stats)
     kappa = 4
-    dr = DelayedRefresh(plan, stats, roots, kappa=kappa, spread=3)
+    dr = DelayedRefresh(plan, stats, roots, kappa=kappa, spread=3, fp64_iters=precision)
     snapshots = {}
     adopted_at = []
     for t in range(0, 3 * kappa + 1):
@@ -39,7 +40,7 @@ def test_delayed_refresh_matches_synchronous_refresh_of_snapshot():
         if dr.step(t):
             adopted_at.append(t)
             ref = torch.zeros_like(stats)
-            shp.refresh_group_roots(plan, snapshots[t - kappa], ref, 0)
+            shp.refresh_group_roots(plan, snapshots[t - kappa], ref, 0, fp64_iters=precision)
             torch.cuda.synchronize()
             assert torch.equal(dr.current[:plan.stats_elems], ref[:plan.stats_elems]), t
     assert adopted_at == [kappa, 2 * kappa, 3 * kappa]
