@@ -104,19 +104,32 @@ __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ s
       }
       // one rounding to the 2^-48 grid (|V| < 2^48), then balanced base-128 digits
       // by integer ops, lowest first: d = ((V + 64) mod 128) - 64, V = (V - d) / 128
-      long long V[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) V[q] = __double2ll_rn(ldexp(r[q], sh + 7 * (kS - 1)));
+      // (32-bit integer work: V = H 2^21 + L, the three low digits from L, the
+      // carry into H, the four high digits from H)
+      static_assert(kS == 7, "the 21 + 27-bit split assumes 7 slices");
       uint32_t dig[kS][2];
 #pragma unroll
-      for (int s = kS - 1; s >= 0; --s) {
-        dig[s][0] = dig[s][1] = 0u;
+      for (int s = 0; s < kS; ++s) dig[s][0] = dig[s][1] = 0u;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const long long d = s ? ((V[q] + 64) & 127) - 64 : V[q];
-          V[q] = (V[q] - d) >> 7;
+      for (int q = 0; q < 8; ++q) {
+        const long long V = __double2ll_rn(ldexp(r[q], sh + 7 * (kS - 1)));
+        int H = (int)(V >> 21);
+        int L = (int)(V & 0x1FFFFF);
+        int d;
+#pragma unroll
+        for (int s = kS - 1; s >= kS - 3; --s) {
+          d = ((L + 64) & 127) - 64;
+          L = (L - d) >> 7;
           dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
         }
+        H += L;
+#pragma unroll
+        for (int s = kS - 4; s >= 1; --s) {
+          d = ((H + 64) & 127) - 64;
+          H = (H - d) >> 7;
+          dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
+        }
+        dig[0][q >> 2] |= ((uint32_t)H & 0xFFu) << (8 * (q & 3));
       }
 #pragma unroll
       for (int s = 0; s < kS; ++s) {
