@@ -1,9 +1,9 @@
 """bench.py -- the hot path of distributed Shampoo on B200, one JSON line.
 
-Roots run in the "ozaki" precision by default (every Newton product on the INT8
-tensor cores with exact int32 accumulation of 7-slice splits, fp64-level
-accuracy); --root-precision fp64 runs them on the FP64 DMMA
-pipe, --root-precision hybrid with a 3xTF32 tail.
+Roots run in the "auto" precision by default: the Ozaki root (every Newton
+product on the INT8 tensor cores with exact int32 accumulation of 7-slice
+splits, fp64-level accuracy) for blocks of n >= 512 (all of
+this workload), FP64 DMMA below; --root-precision fp64 / ozaki / hybrid force one.
 
 Workload (BASELINE.json configs[2], the configuration the metric is quoted on):
 Transformer-Big (99 matrix parameters, 375.1M of P:494's 375.4M), block size
@@ -49,8 +49,9 @@ ROOT_TRAFFIC_BYTES_PER_MATRIX = (191.679e9 + 128.690e9) / 148  # profiles/root_r
 INT8_PEAK_TOPS = 2 * 1687.1  # bf16 measured (MEASURED_PEAKS.json) x the nominal int8:bf16 ratio
 # dram read + write of one Ozaki product stage per 1024^2 matrix (ncu --set full, 148-matrix dual stage)
 OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = (2.296e9 + 2.448e9) / 148
-ROOT_MODE = {"fp64": None, "ozaki": "ozaki", "hybrid": -1}
-ROOT_LABEL = {"fp64": "fp64 DMMA", "ozaki": "ozaki: INT8 tcgen05, 7 slices, exact int32 accumulation",
+ROOT_MODE = {"auto": "auto", "fp64": None, "ozaki": "ozaki", "hybrid": -1}
+ROOT_LABEL = {"auto": "auto: ozaki (INT8 tcgen05, 7 slices, exact int32 accumulation) for n >= 512, fp64 DMMA below",
+              "fp64": "fp64 DMMA", "ozaki": "ozaki: INT8 tcgen05, 7 slices, exact int32 accumulation",
               "hybrid": "hybrid fp64 DMMA -> 3xTF32 tcgen05 (auto switch)"}
 
 
@@ -66,8 +67,9 @@ def parse():
     ap.add_argument("--block-size", type=int, default=BLOCK,
                     help="config 5 sweep (128..4096); the metric is quoted at 1024")
     ap.add_argument("--max-precond-dim", type=int, default=MAX_PRECOND)
-    ap.add_argument("--root-precision", default="ozaki", choices=["fp64", "ozaki", "hybrid"],
-                    help="fp64: FP64 DMMA; ozaki: INT8 tensor cores with fp64-level accuracy (§6.3c); "
+    ap.add_argument("--root-precision", default="auto", choices=["auto", "fp64", "ozaki", "hybrid"],
+                    help="auto: ozaki for n >= 512, fp64 below; fp64: FP64 DMMA; ozaki: INT8 tensor cores "
+                         "with fp64-level accuracy (§6.3c); "
                          "hybrid: FP64 DMMA then a 3xTF32 tcgen05 tail (§6.3b)")
     ap.add_argument("--hybrid", action="store_true", help="alias of --root-precision hybrid")
     return ap.parse_args()
@@ -281,7 +283,7 @@ def main():
     g4 = sorted([g for g in plan.groups_of(rank) if int(g["p"]) == 4], key=lambda g: -int(g["count"]) * int(g["n"]) ** 3)
     roof = None
     iters_mean = None
-    if g4 and args.root_precision == "ozaki":
+    if g4 and (args.root_precision == "ozaki" or (args.root_precision == "auto" and int(g4[0]["n"]) >= shp.OZAKI_MIN_N)):
         # the INT8 GEMM dominates: every launch bracketed by CUDA events on its stream
         g = g4[0]
         cnt, off, stride = int(g["count"]), int(g["offset"]), int(g["stride"])

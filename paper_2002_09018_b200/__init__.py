@@ -171,8 +171,11 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
                          fp64_iters: int | None = None):
     """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry).
     fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch);
-    fp64_iters="ozaki": every product on the INT8 tensor cores with fp64-level accuracy."""
+    fp64_iters="ozaki": every product on the INT8 tensor cores with fp64-level accuracy;
+    fp64_iters="auto": "ozaki" for n >= OZAKI_MIN_N, FP64 DMMA below."""
     L = _lib.lib()
+    if fp64_iters == "auto":  # the INT8 Ozaki loop pays off from n = 512 (per-iteration launches, 128-row tiles)
+        fp64_iters = "ozaki" if (n >= OZAKI_MIN_N and r == 1) else None
     if fp64_iters == "ozaki":
         if r != 1:
             raise ValueError("the ozaki root serves r = 1 only")
@@ -251,6 +254,9 @@ def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.
 
 
 _refresh_launches = 0
+# smallest n for which precision "auto" picks the Ozaki root (measured on B200: n = 128 ozaki 19k roots/s vs
+# FP64 DMMA 72k; n = 512 2.7k vs 2.5k; n = 1024 580 vs 354 -- profiles/r01t_*)
+OZAKI_MIN_N = 512
 
 
 def last_refresh_launch_count() -> int:
