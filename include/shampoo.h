@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SHAMPOO_ABI_VERSION 2
+#define SHAMPOO_ABI_VERSION 3
 
 typedef enum {
   SHAMPOO_OK = 0,
@@ -217,17 +217,24 @@ int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t
                                             shampoo_stream_t stream);
 
 /* Ozaki precision: every coupled-Newton product on the INT8
- * tensor cores with fp64-level accuracy -- each fp64 operand is split per row
- * into 7 int8 slices (2^-49 relative to the row maximum), the 28 slice products
- * with s + t <= 8 accumulate EXACTLY in int32 TMEM accumulators
- * (tcgen05.mma.kind::i8), and the epilogue combines them in fp64.  Iterates,
- * power iteration, ridge, stopping rule and statuses are those of
- * shampoo_inverse_pth_root_batched (p-th roots, r = 1); the workspace is larger
- * (shampoo_root_ozaki_workspace_bytes: + 5 x 7 int8 planes per matrix). */
+ * tensor cores -- each fp64 operand is split per row into `slices` int8 slices
+ * (one rounding, to 2^-(7 slices - 1) relative to the row maximum), the
+ * slices (slices + 1) / 2 slice products with s + t <= slices + 1 accumulate
+ * EXACTLY in int32 TMEM accumulators (tcgen05.mma.kind::i8), and the epilogue
+ * combines them in fp64.  Iterates, power iteration, ridge, stopping rule and
+ * statuses are those of shampoo_inverse_pth_root_batched (p-th roots, r = 1);
+ * the workspace is larger (shampoo_root_ozaki_workspace_bytes: + 5 x 7 int8
+ * planes per matrix, enough for either slice count).
+ * slices = 7 (28 products): fp64-level; measured 2.4e-7 relative Frobenius
+ *   root error at n = 1024, kappa 1e6 (fp32-output-limited).
+ * slices = 6 (21 products): the precision chosen against the north star's
+ *   1e-3 bar -- host emulation (tools/ozaki_precision.py) 3.8e-6 at n = 256;
+ *   measured on B200 in tests/test_gpu_ozaki.py.
+ * Any other value: SHAMPOO_ERR_INVALID_ARG, nothing enqueued. */
 size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter);
 int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
                                            int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
-                                           double tol, int32_t max_iter, int32_t power_iters,
+                                           double tol, int32_t max_iter, int32_t power_iters, int32_t slices,
                                            shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
                                            shampoo_stream_t stream);
 

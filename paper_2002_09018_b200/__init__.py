@@ -171,19 +171,21 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
                          fp64_iters: int | None = None):
     """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry).
     fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch);
-    fp64_iters="ozaki": every product on the INT8 tensor cores with fp64-level accuracy;
-    fp64_iters="auto": "ozaki" for n >= OZAKI_MIN_N, FP64 DMMA below."""
+    fp64_iters="ozaki" (= "ozaki7"): every product on the INT8 tensor cores, 7 slices, fp64-level accuracy;
+    fp64_iters="ozaki6": 6 slices (21 slice products instead of 28; DESIGN.md §6.3c);
+    fp64_iters="auto" / "auto6": "ozaki" / "ozaki6" for n >= OZAKI_MIN_N, FP64 DMMA below."""
     L = _lib.lib()
-    if fp64_iters == "auto":  # the INT8 Ozaki loop pays off from n = 512 (per-iteration launches, 128-row tiles)
-        fp64_iters = "ozaki" if (n >= OZAKI_MIN_N and r == 1) else None
-    if fp64_iters == "ozaki":
+    if fp64_iters in ("auto", "auto6"):  # the INT8 Ozaki loop pays off from n = 512 (per-iteration launches, 128-row tiles)
+        fp64_iters = ("ozaki" + fp64_iters[4:]) if (n >= OZAKI_MIN_N and r == 1) else None
+    if isinstance(fp64_iters, str) and fp64_iters.startswith("ozaki"):
+        slices = int(fp64_iters[5:] or 7)
         if r != 1:
             raise ValueError("the ozaki root serves r = 1 only")
         wsb = L.shampoo_root_ozaki_workspace_bytes(batch, n, p, max_iter)
         ws = workspace(wsb, device if device is not None else info.device, "root")
         check(L.shampoo_inverse_pth_root_batched_ozaki(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
-                                                       tol, max_iter, power_iters, info.data_ptr(), ws.data_ptr(),
-                                                       ws.numel(), _stream_ptr(stream)))
+                                                       tol, max_iter, power_iters, slices, info.data_ptr(),
+                                                       ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
         return
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
     ws = workspace(wsb, device if device is not None else info.device, "root")

@@ -94,7 +94,7 @@ def lib():
     L.shampoo_root_ozaki_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
     L.shampoo_root_ozaki_workspace_bytes.restype = _sz
     L.shampoo_inverse_pth_root_batched_ozaki.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl,
-                                                         _dbl, _i32, _i32, _vp, _vp, _sz, _vp]
+                                                         _dbl, _i32, _i32, _i32, _vp, _vp, _sz, _vp]
     L.shampoo_inverse_pth_root_batched_ozaki.restype = ctypes.c_int
     L.shampoo_root_residual_workspace_bytes.argtypes = [_i32, _i32, _i32]
     L.shampoo_root_residual_workspace_bytes.restype = _sz
@@ -126,7 +126,7 @@ def lib():
     L.shampoo_profile_begin.restype = ctypes.c_int
     L.shampoo_profile_end.argtypes = [ctypes.c_char_p, _vp, _vp]
     L.shampoo_profile_end.restype = ctypes.c_int
-    if L.shampoo_abi_version() != 2:
+    if L.shampoo_abi_version() != 3:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L
     return L

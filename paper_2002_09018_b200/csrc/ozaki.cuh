@@ -12,15 +12,18 @@
 // |sum| <= S * K * 64^2 < 2^31 for K <= 4096, S <= 8.  Epilogue, in fp64:
 //   C_ij = 2^e_i 2^f_j sum_{d = S-1 .. 0} acc_d 2^-(12 + 7d)
 // (products by powers of two are exact; the sum is the only rounding).
-// With S = 7 the product error is ~K 2^-49 max|A_i.| max|B_j.| (numpy
-// emulation of the whole root at n = 256: 3.2e-8 vs the fp64 root, below the
-// fp32 output rounding; S = 6: 3.7e-6).
+// With S = 7 the product error is ~K 2^-49 max|A_i.| max|B_j.| (host
+// emulation of the whole root, tools/ozaki_precision.py, n = 256: 3.2e-8 vs the
+// exact root, below the fp32 output rounding; S = 6: 3.8e-6; S = 5: 4.3e-4).
+// S is a template parameter (6 or 7; the precision choice).
 //
 // GEMM kernel: one CTA per SM, persistent over 128 x 64 output tiles; warp 0 =
 // TMA producer (per 64-byte k-chunk: S A-planes 128 x 64 B and S B-planes 64 x
-// 64 B, SWIZZLE_64B, 2-stage ring), warp 1 = TMEM allocator + MMA issuer (28
-// tcgen05.mma.kind::i8 M=128 N=64 K=32 per k-step for S = 7), warps 2..5 =
-// epilogue (7 tcgen05.ld per 16 columns, fp64 combination, mode-specific store).
+// 64 B, SWIZZLE_64B, 2-stage ring for S = 7, 3 stages for S = 6), warp 1 = TMEM
+// allocator + MMA issuer (the S(S+1)/2 slice pairs of a k-step in 10 (S = 7) /
+// 8 (S = 6) tcgen05.mma.kind::i8 of M = 128, N = 64..256, K = 32), warps 2..5 =
+// epilogue (S tcgen05.ld per 8 columns behind one wait, fp64 combination,
+// mode-specific store).
 #pragma once
 #include <cuda.h>
 #include <stdint.h>
@@ -31,16 +34,19 @@
 namespace shp {
 namespace oz {
 
-constexpr int kS = 7;                       // slices per operand
+constexpr int kSMax = 7;                    // most slices per operand (workspace sizing)
 constexpr int kBM = 128, kBN = 64, kBK = 64;  // tile M, N; k-chunk in bytes (int8 elements): two K=32 MMA steps
 constexpr int kAPlane = kBM * kBK;          // 8 KB
 constexpr int kBPlane = kBN * kBK;          // 4 KB
-constexpr int kStageBytes = kS * (kAPlane + kBPlane);  // 84 KB
-constexpr int kStages = 2;  // (measured: 32-byte k-chunks x 4 stages were 4% slower)
+template <int S>
+struct Cfg {
+  static_assert(S >= 4 && S <= kSMax, "4 <= slices <= 7 (int32 digit split, TMEM columns)");
+  static constexpr int kStageBytes = S * (kAPlane + kBPlane);  // 84 KB (S = 7), 72 KB (S = 6)
+  // S = 7: 2 stages (measured: 32-byte k-chunks x 4 stages were 4% slower); S = 6: 3 fit in 227 KB
+  static constexpr int kStages = S >= 7 ? 2 : 3;
+};
 constexpr int kThreads = 192;
-constexpr uint32_t kTmemCols = 512;         // kS accumulators x 64 columns (448 used)
-// accumulator weights 2^-(12 + 7d)
-__device__ __constant__ const double kW[8] = {0x1p-12, 0x1p-19, 0x1p-26, 0x1p-33, 0x1p-40, 0x1p-47, 0x1p-54, 0x1p-61};
+constexpr uint32_t kTmemCols = 512;         // S accumulators x 64 columns (448 used for S = 7)
 
 // K-major tile of kBK-byte rows, swizzled to match the TMA map (SWIZZLE_32B:
 // layout type 6, 8-row atoms of 256 B; SWIZZLE_64B: type 4, 512 B)
@@ -54,7 +60,7 @@ TC_DEV uint64_t desc_sw(uint32_t smem_addr) {
   return d;
 }
 
-constexpr uint32_t idesc_i8(int M, int N) {
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   // c_format S32 (2) [4,6), a/b format INT8 (1) [7,10) / [10,13), K-major, N>>3 [17,23), M>>4 [24,29)
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
@@ -68,86 +74,322 @@ TC_DEV void umma_i8(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc, u
 }
 
 // --------------------------------------------------------------- slicing
+// Digits of 8 consecutive elements r[0..7] of one row (sh = 6 - e_i): one
+// rounding to the 2^-(7S-1) grid (|V| < 2^(7S-1)), then balanced base-128 digits
+// by integer ops, lowest first: d = ((V + 64) mod 128) - 64, V = (V - d) / 128
+// (32-bit integer work: V = H 2^21 + L, the three low digits from L, the carry
+// into H, the S - 3 high digits from H, |H| < 2^27); dig[s] = 8 packed int8.
+template <int S>
+__device__ __forceinline__ void slice8(const double (&r)[8], int sh, uint32_t (&dig)[S][2]) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) dig[s][0] = dig[s][1] = 0u;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const long long V = __double2ll_rn(ldexp(r[q], sh + 7 * (S - 1)));
+    int H = (int)(V >> 21);
+    int L = (int)(V & 0x1FFFFF);
+    int d;
+#pragma unroll
+    for (int s = S - 1; s >= S - 3; --s) {
+      d = ((L + 64) & 127) - 64;
+      L = (L - d) >> 7;
+      dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
+    }
+    H += L;
+#pragma unroll
+    for (int s = S - 4; s >= 1; --s) {
+      d = ((H + 64) & 127) - 64;
+      H = (H - d) >> 7;
+      dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
+    }
+    dig[0][q >> 2] |= ((uint32_t)H & 0xFFu) << (8 * (q & 3));
+  }
+}
+
+// 8 consecutive elements of a row from column j (two 32-byte loads; the row
+// tail n % 8 element-wise, zero beyond n)
+__device__ __forceinline__ void load8(const double* row, int j, int n, double (&r)[8]) {
+  if (j + 8 <= n) {
+    const double4 u0 = *reinterpret_cast<const double4*>(row + j);
+    const double4 u1 = *reinterpret_cast<const double4*>(row + j + 4);
+    r[0] = u0.x; r[1] = u0.y; r[2] = u0.z; r[3] = u0.w;
+    r[4] = u1.x; r[5] = u1.y; r[6] = u1.z; r[7] = u1.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? row[j + q] : 0.0;
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void store8(int8_t* plane_row, int j, int n, const uint32_t (&w)[2]) {
+  if (j + 8 <= n) {
+    *reinterpret_cast<uint2*>(plane_row + j) = make_uint2(w[0], w[1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (j + q < n) plane_row[j + q] = (int8_t)((w[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+  }
+}
+
+// Row exponent: e with max|row| < 2^e (0 for a zero row)
+__device__ __forceinline__ int row_exponent(double mx) {
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+  return e;
+}
+
+// T_ij = ((p + 1) delta_ij - M_ij) / p, the same expression as the fp64 root's
+// setup (root.cu) -- the coupled-Newton T_k is a function of M_k alone
+__device__ __forceinline__ double t_of(double m, bool diag, double pp1, double inv_p) {
+  return ((diag ? pp1 : 0.0) - m) * inv_p;
+}
+
 // One warp per (matrix, row): scale[mat*np + i] = 2^e_i, planes
-// [(mat*kS + s)*np + i]*np + j = d_s(A_ij) for j < n.
+// [(mat*S + s)*np + i]*np + j = d_s(A_ij) for j < n.  MT: the source is M_k and
+// the same pass also slices T_k = ((p+1)I - M_k)/p into (planes_t, scale_t), so
+// T_k never round-trips through HBM in fp64.  Rows of n <= 1024 are held in
+// registers (32 doubles per lane, 8 KB in flight per warp): ONE pass over HBM
+// for the row maxima and the digits; longer rows take two passes (the second
+// mostly from L1).
+template <int S, bool MT>
 __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ src, int64_t mat_stride, int n, int np,
                                                     int batch, const int* __restrict__ act, const int* nact,
-                                                    int8_t* __restrict__ planes, double* __restrict__ scale) {
+                                                    int8_t* __restrict__ planes, double* __restrict__ scale,
+                                                    int8_t* __restrict__ planes_t, double* __restrict__ scale_t,
+                                                    int p) {
+  constexpr int kRegChunks = 4;  // 4 x 256 columns per warp held in registers
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = act ? *nact : batch;
+  const int64_t plane_pitch = (int64_t)np * np;
+  const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p;
   for (int64_t rid = gw; rid < (int64_t)na * n; rid += nw) {
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
-    double mx = 0.0;
-    for (int j = lane; j < n; j += 32) mx = fmax(mx, fabs(row[j]));
+    const int64_t prow_off = ((int64_t)mat * S * np + i) * np;
+    if (n <= 256 * kRegChunks) {
+      double r[kRegChunks][8];
+      double mx = 0.0, mt = 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    int e = 0;
-    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
-    if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
-    const int sh = 6 - e;
-    // 8 consecutive columns per lane (two double4 loads in flight, one 8-byte
-    // store per plane); the row tail (n % 8) element-wise
-    for (int j = 8 * lane; j < n; j += 256) {
-      double r[8];
-      if (j + 8 <= n) {
-        const double4 u0 = *reinterpret_cast<const double4*>(row + j);
-        const double4 u1 = *reinterpret_cast<const double4*>(row + j + 4);
-        r[0] = u0.x; r[1] = u0.y; r[2] = u0.z; r[3] = u0.w;
-        r[4] = u1.x; r[5] = u1.y; r[6] = u1.z; r[7] = u1.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? row[j + q] : 0.0;
-      }
-      // one rounding to the 2^-48 grid (|V| < 2^48), then balanced base-128 digits
-      // by integer ops, lowest first: d = ((V + 64) mod 128) - 64, V = (V - d) / 128
-      // (32-bit integer work: V = H 2^21 + L, the three low digits from L, the
-      // carry into H, the four high digits from H)
-      static_assert(kS == 7, "the 21 + 27-bit split assumes 7 slices");
-      uint32_t dig[kS][2];
-#pragma unroll
-      for (int s = 0; s < kS; ++s) dig[s][0] = dig[s][1] = 0u;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const long long V = __double2ll_rn(ldexp(r[q], sh + 7 * (kS - 1)));
-        int H = (int)(V >> 21);
-        int L = (int)(V & 0x1FFFFF);
-        int d;
-#pragma unroll
-        for (int s = kS - 1; s >= kS - 3; --s) {
-          d = ((L + 64) & 127) - 64;
-          L = (L - d) >> 7;
-          dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
-        }
-        H += L;
-#pragma unroll
-        for (int s = kS - 4; s >= 1; --s) {
-          d = ((H + 64) & 127) - 64;
-          H = (H - d) >> 7;
-          dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
-        }
-        dig[0][q >> 2] |= ((uint32_t)H & 0xFFu) << (8 * (q & 3));
-      }
-#pragma unroll
-      for (int s = 0; s < kS; ++s) {
-        const uint32_t w[2] = {dig[s][0], dig[s][1]};
-        int8_t* dst = planes + (((int64_t)mat * kS + s) * np + i) * np + j;
-        if (j + 8 <= n) {
-          *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+      for (int c = 0; c < kRegChunks; ++c) {
+        const int j = 256 * c + 8 * lane;
+        if (j < n) {
+          load8(row, j, n, r[c]);
         } else {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (j + q < n) dst[q] = (int8_t)((w[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+          for (int q = 0; q < 8; ++q) r[c][q] = 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          mx = fmax(mx, fabs(r[c][q]));
+          if (MT) mt = fmax(mt, fabs(t_of(r[c][q], j + q == i, pp1, inv_p)));
+        }
+      }
+      const int e = row_exponent(mx);
+      const int et = MT ? row_exponent(mt) : 0;
+      if (lane == 0) {
+        scale[(int64_t)mat * np + i] = ldexp(1.0, e);
+        if (MT) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
+      }
+#pragma unroll
+      for (int c = 0; c < kRegChunks; ++c) {
+        const int j = 256 * c + 8 * lane;
+        if (j < n) {
+          uint32_t dig[S][2];
+          slice8<S>(r[c], 6 - e, dig);
+#pragma unroll
+          for (int s = 0; s < S; ++s) store8<S>(planes + prow_off + s * plane_pitch, j, n, dig[s]);
+          if (MT) {
+            double t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = t_of(r[c][q], j + q == i, pp1, inv_p);
+            slice8<S>(t, 6 - et, dig);
+#pragma unroll
+            for (int s = 0; s < S; ++s) store8<S>(planes_t + prow_off + s * plane_pitch, j, n, dig[s]);
+          }
+        }
+      }
+    } else {
+      double mx = 0.0, mt = 0.0;
+      for (int j = lane; j < n; j += 32) {
+        mx = fmax(mx, fabs(row[j]));
+        if (MT) mt = fmax(mt, fabs(t_of(row[j], j == i, pp1, inv_p)));
+      }
+      const int e = row_exponent(mx);
+      const int et = MT ? row_exponent(mt) : 0;
+      if (lane == 0) {
+        scale[(int64_t)mat * np + i] = ldexp(1.0, e);
+        if (MT) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
+      }
+      for (int j = 8 * lane; j < n; j += 256) {
+        double r[8];
+        load8(row, j, n, r);
+        uint32_t dig[S][2];
+        slice8<S>(r, 6 - e, dig);
+#pragma unroll
+        for (int s = 0; s < S; ++s) store8<S>(planes + prow_off + s * plane_pitch, j, n, dig[s]);
+        if (MT) {
+          double t[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) t[q] = t_of(r[q], j + q == i, pp1, inv_p);
+          slice8<S>(t, 6 - et, dig);
+#pragma unroll
+          for (int s = 0; s < S; ++s) store8<S>(planes_t + prow_off + s * plane_pitch, j, n, dig[s]);
         }
       }
     }
   }
 }
 
+// Rows of n <= 1024 (every Ozaki root of the Transformer-Big plan): each warp
+// streams its rows through a ring of kSliceRing shared-memory buffers with
+// cp.async (16-byte copies, nothing held in registers while in flight: 16-24
+// rows = 128-192 KB in flight per SM, enough to cover HBM latency), then takes
+// the row maxima and the digits from shared memory.  Same outputs as
+// slice_kernel.  Buffer layout: 16-byte segment s at s + s/8 (one pad segment
+// per 128 B), so the per-lane 64-byte column groups read conflict-free.
+constexpr int kSliceWarps = 8, kSliceRing = 3, kSliceRowMax = 1024;
+constexpr int kSliceRowSegs = kSliceRowMax / 2 + kSliceRowMax / 16;  // 16-byte segments incl. padding
+constexpr size_t kSliceSmem = (size_t)kSliceWarps * kSliceRing * kSliceRowSegs * 16;  // 216 KB
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// 8 consecutive columns j = 8 lane + 256 c of a staged row (4 conflict-free 16-byte reads)
+__device__ __forceinline__ void smem_load8(const double2* rb, int c, int lane, double (&r)[8]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int sg = 128 * c + 4 * lane + k;
+    const double2 u = rb[sg + (sg >> 3)];
+    r[2 * k] = u.x;
+    r[2 * k + 1] = u.y;
+  }
+}
+
+template <int S, bool MT>
+__global__ void __launch_bounds__(kSliceWarps * 32, 1) slice_smem_kernel(
+    const double* __restrict__ src, int64_t mat_stride, int n, int np, int batch, const int* __restrict__ act,
+    const int* nact, int8_t* __restrict__ planes, double* __restrict__ scale, int8_t* __restrict__ planes_t,
+    double* __restrict__ scale_t, int p) {
+  extern __shared__ __align__(16) uint8_t slice_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* ring = reinterpret_cast<double2*>(slice_smem) + (size_t)warp * kSliceRing * kSliceRowSegs;
+  const int64_t gw = (int64_t)blockIdx.x * kSliceWarps + warp, nw = (int64_t)gridDim.x * kSliceWarps;
+  const int na = act ? *nact : batch;
+  const int64_t rows = (int64_t)na * n;
+  const int segs = (n + 7) / 8 * 4;  // 16-byte segments copied per row (columns rounded up to 8 <= np)
+  const int64_t plane_pitch = (int64_t)np * np;
+  const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p;
+  auto row_ptr = [&](int64_t rid, int& mat, int& i) {
+    const int pos = (int)(rid / n);
+    i = (int)(rid - (int64_t)pos * n);
+    mat = act ? act[pos] : pos;
+    return src + mat * mat_stride + (int64_t)i * np;
+  };
+  auto issue = [&](int64_t rid, int buf) {
+    if (rid < rows) {
+      int mat, i;
+      const double* row = row_ptr(rid, mat, i);
+      double2* dst = ring + buf * kSliceRowSegs;
+      for (int sg = lane; sg < segs; sg += 32) cp_async16(dst + sg + (sg >> 3), row + 2 * sg);
+    }
+    cp_async_commit();  // empty groups keep the group count uniform
+  };
+#pragma unroll
+  for (int q = 0; q < kSliceRing - 1; ++q) issue(gw + q * nw, q);
+  int it = 0;
+  for (int64_t rid = gw; rid < rows; rid += nw, ++it) {
+    issue(rid + (int64_t)(kSliceRing - 1) * nw, (it + kSliceRing - 1) % kSliceRing);
+    cp_async_wait<kSliceRing - 1>();
+    __syncwarp();
+    const double2* rb = ring + (it % kSliceRing) * kSliceRowSegs;
+    int mat, i;
+    row_ptr(rid, mat, i);
+    double mx = 0.0, mt = 0.0;
+#pragma unroll
+    for (int c = 0; c < kSliceRowMax / 256; ++c) {
+      const int j = 256 * c + 8 * lane;
+      if (j < n) {
+        double r[8];
+        smem_load8(rb, c, lane, r);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double v = (j + q < n) ? r[q] : 0.0;
+          mx = fmax(mx, fabs(v));
+          if (MT) mt = fmax(mt, fabs(t_of(v, j + q == i, pp1, inv_p)));
+        }
+      }
+    }
+    const int e = row_exponent(mx);
+    const int et = MT ? row_exponent(mt) : 0;
+    if (lane == 0) {
+      scale[(int64_t)mat * np + i] = ldexp(1.0, e);
+      if (MT) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
+    }
+    const int64_t prow_off = ((int64_t)mat * S * np + i) * np;
+#pragma unroll 1
+    for (int c = 0; c < kSliceRowMax / 256; ++c) {
+      const int j = 256 * c + 8 * lane;
+      if (j < n) {
+        double r[8];
+        smem_load8(rb, c, lane, r);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? r[q] : 0.0;
+        uint32_t dig[S][2];
+        slice8<S>(r, 6 - e, dig);
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) store8<S>(planes + prow_off + s2 * plane_pitch, j, n, dig[s2]);
+        if (MT) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) r[q] = t_of(r[q], j + q == i, pp1, inv_p);
+          slice8<S>(r, 6 - et, dig);
+#pragma unroll
+          for (int s2 = 0; s2 < S; ++s2) store8<S>(planes_t + prow_off + s2 * plane_pitch, j, n, dig[s2]);
+        }
+      }
+    }
+    __syncwarp();  // every lane done with this buffer before it is refilled
+  }
+  cp_async_wait<0>();
+}
+
 // --------------------------------------------------------------- GEMM
+// Integer-pipe helpers for the epilogue (no fp64 instruction while the tensor
+// pipe runs; see the phase-2 note in gemm_kernel).
+// e such that x = 2^e for the power-of-two row scales (exponent field - 1023)
+__device__ __forceinline__ int exp2_of(double x) {
+  return (int)((__double_as_longlong(x) >> 52) & 0x7FF) - 1023;
+}
+// x 2^k exactly by exponent arithmetic; zero, inf and NaN pass through; results
+// that would leave the normal range take the fp64 multiply (never on the
+// Newton iterates' magnitudes)
+__device__ __forceinline__ double scale2(double x, int k) {
+  const long long b = __double_as_longlong(x);
+  const int ex = (int)((b >> 52) & 0x7FF);
+  const int ne = ex + k;
+  if (ex != 0 && ex != 0x7FF && ne >= 1 && ne <= 2046) return __longlong_as_double(b + ((long long)k << 52));
+  if (ex == 0x7FF || x == 0.0) return x;
+  const int k1 = k / 2;  // two exact power-of-two factors (|k| < 2000)
+  return x * __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k - k1 + 1023) << 52);
+}
+// |x| as an unsigned bit pattern: ordered like |x| for non-NaN, NaN above +inf
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7FFFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+
 struct OzJob {
   int a_map, b_map;         // TMA maps of the A-use (128-row box) / B-use (64-row box) planes
   const double* a_scale;    // [mat * np + row] = 2^e
@@ -163,9 +405,7 @@ struct OzArgs {
   int sym;                  // upper tiles only (tj >= 2 ti), each stored twice (j >= i, mirrored)
   int jobs;
   OzJob job[2];
-  int mupdate;              // job 0's epilogue: M-update (T_{k+1} and max|M - I|)
-  double* t_out;
-  int64_t t_stride;
+  int mupdate;              // job 0's epilogue: max|M_{k+1} - I| into errh[mat][kcheck]
   int p;
   double* errh;
   int max_iter, kcheck;
@@ -199,8 +439,10 @@ TC_DEV void oz_decode(const OzArgs& a, int per_mat, int64_t tile, int& mat, int&
   mat = a.act ? a.act[pos] : pos;
 }
 
+template <int S>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
+  constexpr int kS = S, kStages = Cfg<S>::kStages, kStageBytes = Cfg<S>::kStageBytes;
   const int na = a.act ? *a.nact : a.batch;
   if (na == 0) return;
   const int per_mat = oz_tiles_per_mat(a);
@@ -309,7 +551,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const int quad = warp & 3;
     const int row_in_tile = quad * 32 + lane;
     uint32_t acc_phase = 0;
-    const double inv_p = 1.0 / (double)a.p, pp1 = (double)(a.p + 1);
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int mat, job, ti, tj;
       oz_decode(a, per_mat, tile, mat, job, ti, tj);
@@ -320,39 +561,53 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const OzJob& J = a.job[job];
       const bool mup = a.mupdate && job == 0;
       double* out = J.out + mat * J.out_stride;
-      double* tout = mup ? a.t_out + mat * a.t_stride : nullptr;
       const double sa = row_ok ? J.a_scale[(int64_t)mat * a.np + i] : 0.0;
-      // phase 1: drain the 7 accumulators of all 64 columns into fp64 registers
-      // (sum over d, smallest weights first), then release TMEM so the next
-      // tile's MMAs overlap this tile's scaling and stores
+      // phase 1: drain the S accumulators of all 64 columns, then release TMEM so
+      // the next tile's MMAs overlap this tile's scaling and stores.  Per
+      // 8-column chunk the S loads are issued back to back behind ONE wait.
+      // Per element the exact value V = sum_d acc_d 2^(7(S-1-d)) (|V| < 2^68) is
+      // rounded ONCE to fp64: H = sum_{d<4} acc_d 2^(7(3-d)) and L = sum_{d>=4}
+      // acc_d 2^(7(S-1-d)) exactly in int64, both to fp64 exactly by the
+      // 1.5 2^52 bit trick, x = fma(H, 2^(7(S-4)), L).  The FP64 work sits here,
+      // where the tensor pipe is idle (the MMA warp waits for TMEM): measured
+      // on B200, fp64 instructions issued while tcgen05 MMAs run stall ~100x
+      // ("math pipe throttle"), so phase 2 below uses integer arithmetic only.
       double v[kBN];
 #pragma unroll
-      for (int c0 = 0; c0 < kBN; c0 += 16) {
+      for (int c0 = 0; c0 < kBN; c0 += 8) {
+        uint32_t r[kS][8];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[c0 + e] = 0.0;
+        for (int d = 0; d < kS; ++d)
+          tc::tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(d * kBN + c0), r[d]);
+        tc::tmem_wait_ld();
 #pragma unroll
-        for (int d = kS - 1; d >= 0; --d) {
-          uint32_t r[16];
-          tc::tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(d * kBN + c0), r);
-          tc::tmem_wait_ld();
+        for (int e = 0; e < 8; ++e) {
+          long long hi = 0, lo = 0;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[c0 + e] = v[c0 + e] + (double)(int)r[e] * kW[d];
+          for (int d = 0; d < 4; ++d) hi += (long long)(int)r[d][e] << (7 * (3 - d));
+#pragma unroll
+          for (int d = 4; d < kS; ++d) lo += (long long)(int)r[d][e] << (7 * (kS - 1 - d));
+          const double hd = __longlong_as_double(hi + 0x4338000000000000LL) - 0x1.8p52;  // exact, |hi| < 2^51
+          const double ld = __longlong_as_double(lo + 0x4338000000000000LL) - 0x1.8p52;
+          v[c0 + e] = fma(hd, (double)(1LL << (7 * (kS - 4))), ld);
         }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(tmem_empty);
-      // phase 2: scale by 2^e_i 2^f_j, store row-major (16-byte vectors) and mirrored
-      double emax = 0.0;
+      // phase 2: scale by 2^(e_i + f_j - 12 - 7(S-1)) (exponent arithmetic), store
+      // row-major (16-byte vectors) and mirrored; M-update: max|M - I| on the
+      // bit patterns (T_{k+1} is sliced from M_{k+1} by slice_kernel<S, true>)
+      unsigned long long emax_bits = 0ull;
       if (row_ok) {
         const int j0 = tj * kBN;
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
         double* orow = out + (int64_t)i * a.np + j0;
-        double* trow = mup ? tout + (int64_t)i * a.np + j0 : nullptr;
         const bool full_row = j0 + kBN <= a.n && (!a.sym || j0 >= i);
+        const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
 #pragma unroll
         for (int e = 0; e < kBN; e += 2) {
           const double2 b2 = *reinterpret_cast<const double2*>(bs + e);
-          const double c0 = v[e] * sa * b2.x, c1 = v[e + 1] * sa * b2.y;
+          const double c0 = scale2(v[e], ka + exp2_of(b2.x)), c1 = scale2(v[e + 1], ka + exp2_of(b2.y));
           v[e] = c0;
           v[e + 1] = c1;
           if (full_row) {
@@ -364,15 +619,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               if (j < a.n && (!a.sym || j >= i)) orow[e + q] = q ? c1 : c0;
             }
           }
-          if (mup) {
+          if (mup) {  // max|M_{k+1} - I| (integer max of |c| off the diagonal)
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               const int j = j0 + e + q;
               if (j < a.n && (!a.sym || j >= i)) {
                 const double c = q ? c1 : c0;
-                const double dl = (i == j) ? 1.0 : 0.0;
-                trow[e + q] = (pp1 * dl - c) * inv_p;
-                emax = fmax_nan(emax, fabs(c - dl));
+                emax_bits = umax64(emax_bits, i != j ? abs_bits(c) : abs_bits(c - 1.0));
               }
             }
           }
@@ -383,13 +636,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const int j = j0 + e;
             if (j >= a.n || j <= i) continue;
             out[(int64_t)j * a.np + i] = v[e];
-            if (mup) tout[(int64_t)j * a.np + i] = (pp1 * 0.0 - v[e]) * inv_p;
           }
         }
       }
       if (mup) {
-        emax = warp_max(emax);
-        if (lane == 0) atomic_max_nonneg(a.errh + (int64_t)mat * (a.max_iter + 1) + a.kcheck, emax);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) emax_bits = umax64(emax_bits, __shfl_xor_sync(0xffffffffu, emax_bits, o));
+        if (lane == 0)
+          atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + a.kcheck),
+                    emax_bits);
       }
       acc_phase ^= 1;
     }
@@ -401,14 +656,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 }
 
-inline size_t gemm_smem_bytes() { return 1024 + (size_t)kStages * kStageBytes + 256; }
+template <int S>
+inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S>::kStages * Cfg<S>::kStageBytes + 256; }
 
-// 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * kS),
+// 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * S),
 // row pitch np bytes, plane pitch np*np bytes, box (64 B, box_rows, 1), SWIZZLE_64B
 template <class Encode>
 inline CUresult make_plane_map(Encode enc, CUtensorMap* out, const int8_t* base, int n, int np, int batch,
-                               int box_rows) {
-  cuuint64_t gdim[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch * kS};
+                               int box_rows, int S) {
+  cuuint64_t gdim[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch * S};
   cuuint64_t gstride[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
   cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
   cuuint32_t estride[3] = {1, 1, 1};

@@ -516,31 +516,34 @@ int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter
 
 // ======================================================= Ozaki (INT8) root
 // All coupled-Newton iterations on the INT8 tensor cores (ozaki.cuh): fp64
-// iterates in root.cu's regions, every operand sliced into kS int8 planes right
-// before its product.  Slots (planes + row scales) for X_k, T, S0, S1, M_k.
+// iterates in root.cu's regions, every operand sliced into S int8 planes right
+// before its product (S = 6 or 7).  Slots (planes + row scales) for X_k, T, S0, S1, M_k.
 enum { OZ_SX = 0, OZ_ST = 1, OZ_SS0 = 2, OZ_SS1 = 3, OZ_SM = 4, OZ_SLOTS = 5 };
 
 size_t root_ozaki_ws_bytes(int batch, int n) {
   const size_t np = (size_t)((n + 63) / 64 * 64);
-  const size_t planes = (size_t)OZ_SLOTS * batch * oz::kS * np * np;
+  const size_t planes = (size_t)OZ_SLOTS * batch * oz::kSMax * np * np;
   const size_t scales = (size_t)OZ_SLOTS * batch * np * sizeof(double);
   return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap);
 }
 
-int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
-                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
-                      int* nact, void* oz_ws, cudaStream_t stream, int64_t* launches) {
+template <int S>
+static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
+                               const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x,
+                               int* act, int* nact, void* oz_ws, cudaStream_t stream, int64_t* launches) {
+  constexpr int kS = S;
   static bool configured = false;
-  const size_t smem = oz::gemm_smem_bytes();
+  const size_t smem = oz::gemm_smem_bytes<S>();
   if (!configured) {
-    if (cudaFuncSetAttribute(oz::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(oz::gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
       return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel)");
     configured = true;
   }
   if (batch > kTailMaxBatch) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: batch chunk > %d", kTailMaxBatch);
   if (np % 64) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: padded n must be a multiple of 64");
   char* w = static_cast<char*>(oz_ws);
-  const size_t slot_planes = (size_t)batch * oz::kS * np * np;
+  const size_t slot_planes = (size_t)batch * oz::kSMax * np * np;  // slots keep the S = 7 pitch
   int8_t* planes = reinterpret_cast<int8_t*>(w);
   const size_t planes_bytes = ((size_t)OZ_SLOTS * slot_planes + 255) / 256 * 256;
   double* scales = reinterpret_cast<double*>(w + planes_bytes);
@@ -558,8 +561,9 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
       return set_error(SHAMPOO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     for (int q2 = 0; q2 < OZ_SLOTS; ++q2) {
-      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM) != CUDA_SUCCESS ||
-          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN) != CUDA_SUCCESS)
+      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM, kS) != CUDA_SUCCESS ||
+          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN, kS) !=
+              CUDA_SUCCESS)
         return set_error(SHAMPOO_ERR_CUDA, "ozaki: cuTensorMapEncodeTiled failed");
     }
   }
@@ -568,11 +572,37 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   const int64_t mstride = (int64_t)kTailRegions * np * np;
   auto region = [&](int r) { return bufs + (int64_t)r * np * np; };
   const int slice_grid = 8 * num_sms();
-  auto slice = [&](int reg, int slot) {
-    oz::slice_kernel<<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
-                                                    slot_planes_ptr(slot), slot_scale(slot));
+  static bool slice_configured = false;
+  if (!slice_configured) {
+    if (cudaFuncSetAttribute(oz::slice_smem_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)oz::kSliceSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(oz::slice_smem_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)oz::kSliceSmem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(ozaki slice_smem_kernel)");
+    slice_configured = true;
+  }
+  // MT: M_k and T_k = ((p+1)I - M_k)/p in one pass over M_k (T_k never stored in fp64)
+  auto slice_any = [&](int reg, int slot, bool mt) {
+    int8_t* pt = mt ? slot_planes_ptr(OZ_ST) : nullptr;
+    double* st = mt ? slot_scale(OZ_ST) : nullptr;
+    if (n <= oz::kSliceRowMax) {  // rows staged through shared memory (one CTA per SM)
+      if (mt)
+        oz::slice_smem_kernel<S, true><<<num_sms(), oz::kSliceWarps * 32, oz::kSliceSmem, stream>>>(
+            region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
+      else
+        oz::slice_smem_kernel<S, false><<<num_sms(), oz::kSliceWarps * 32, oz::kSliceSmem, stream>>>(
+            region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
+    } else if (mt) {
+      oz::slice_kernel<S, true><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
+                                                               slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
+    } else {
+      oz::slice_kernel<S, false><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
+                                                                slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
+    }
     ++*launches;
   };
+  auto slice = [&](int reg, int slot) { slice_any(reg, slot, false); };
+  auto slice_mt = [&](int reg) { slice_any(reg, OZ_SM, true); };
   oz::OzArgs base;
   std::memset(&base, 0, sizeof base);
   base.act = act;
@@ -600,18 +630,16 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   auto gemm = [&](const oz::OzArgs& a) {
     void* tok;
     prof_begin_launch("ozaki_gemm", stream, &tok);
-    oz::gemm_kernel<<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
+    oz::gemm_kernel<S><<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
     prof_end_launch(tok, stream);
     ++*launches;
   };
   enum { RX0 = 0, RX1 = 1, RM0 = 2, RM1 = 3, RT = 4, RS0 = 5, RS1 = 6 };  // root.cu regions
   const int lead = 31 - __builtin_clz((unsigned)p);
-  int treg = RT;  // region of T_k (p = 1 alternates RT / RS0, as root.cu)
   for (int k = 0; k < max_iter; ++k) {
     const int xs = k & 1;
     slice(RX0 + xs, OZ_SX);
-    slice(treg, OZ_ST);
-    slice(RM0 + xs, OZ_SM);
+    slice_mt(RM0 + xs);
     // P1: X_{k+1} = X_k T ; S0 = T T (p >= 2)
     oz::OzArgs a1 = base;
     a1.jobs = p >= 2 ? 2 : 1;
@@ -642,17 +670,13 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
         sb = sd;
       }
     }
-    // P3: M_{k+1} = T^p M_k ; T_{k+1} ; err_{k+1}
-    const int tnext = (p == 1) ? (treg == RT ? RS0 : RT) : RT;
+    // P3: M_{k+1} = T^p M_k ; err_{k+1} = max|M_{k+1} - I|
     oz::OzArgs a3 = base;
     a3.jobs = 1;
     a3.job[0] = job(p == 1 ? OZ_ST : sb, OZ_SM, RM0 + (xs ^ 1));
     a3.mupdate = 1;
-    a3.t_out = region(tnext);
-    a3.t_stride = mstride;
     a3.kcheck = k + 1;
     gemm(a3);
-    treg = tnext;
     root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, tol, 1.0, k + 1);
     ++*launches;
   }
@@ -662,6 +686,21 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("ozaki root kernels", e);
   return SHAMPOO_OK;
+}
+
+int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
+                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
+                      int* nact, void* oz_ws, int slices, cudaStream_t stream, int64_t* launches) {
+  switch (slices) {
+    case 6:
+      return root_ozaki_launch_s<6>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
+                                    nact, oz_ws, stream, launches);
+    case 7:
+      return root_ozaki_launch_s<7>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
+                                    nact, oz_ws, stream, launches);
+    default:
+      return set_error(SHAMPOO_ERR_INVALID_ARG, "ozaki root: slices must be 6 or 7 (got %d)", slices);
+  }
 }
 
 }  // namespace shp

@@ -1,8 +1,10 @@
 """GPU parity of the Ozaki root (every coupled-Newton product on the INT8
-tensor cores, exact int32 accumulation of 7-slice splits)
-against the fp64 oracle.  Bars: roots <= 1e-3 (north star), held to 1e-6
-(fp64-level products: measured 2e-7 at n = 1024, kappa 1e6); iterations +-1;
-statuses equal; lambda_hat 1e-12 (the power iteration is the FP64 kernel's)."""
+tensor cores, exact int32 accumulation of S-slice splits)
+against the fp64 oracle.  Bars: roots <= 1e-3 (north star), held to 1e-6 for
+S = 7 (fp64-level products: measured 2e-7 at n = 1024, kappa 1e6) and to 1e-4
+for S = 6 (host emulation tools/ozaki_precision.py: 3.8e-6 at n = 256);
+iterations +-1; statuses equal; lambda_hat 1e-12 (the power iteration is the
+FP64 kernel's)."""
 
 import numpy as np
 import pytest
@@ -26,43 +28,52 @@ def rel(a, b):
     return np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b)
 
 
-def _both(shp, As, p, tol=1e-7, max_iter=100, eps=1e-6):
+# (precision mode, root bar)
+MODES = [("ozaki", 1e-6), ("ozaki6", 1e-4)]
+
+
+def _both(shp, As, p, tol=1e-7, max_iter=100, eps=1e-6, mode="ozaki"):
     A = torch.from_numpy(np.ascontiguousarray(As)).to(DEV)
-    X, info = shp.inverse_pth_root_batched(A, p, fp64_iters="ozaki", tol=tol, max_iter=max_iter, eps_rel=eps)
+    X, info = shp.inverse_pth_root_batched(A, p, fp64_iters=mode, tol=tol, max_iter=max_iter, eps_rel=eps)
     torch.cuda.synchronize()
     outs = [oroot.inverse_pth_root(a.astype(np.float64), p, eps, tol, max_iter) for a in As]
     return X.cpu().numpy(), shp.info_to_numpy(info), outs
 
 
+@pytest.mark.parametrize("mode,bar", MODES)
 @pytest.mark.parametrize("n", [64, 130, 200, 512])
-def test_ozaki_p4_mixed(shp, n):
+def test_ozaki_p4_mixed(shp, n, mode, bar):
     As = synth.psd_batch(n, 4, synth.BASE_SEED + 170 + n, "mixed")
-    Xg, inf, outs = _both(shp, As, 4)
+    Xg, inf, outs = _both(shp, As, 4, mode=mode)
     for i, (Xo, io) in enumerate(outs):
-        assert rel(Xg[i], Xo) < 1e-6, (i, rel(Xg[i], Xo))
+        assert rel(Xg[i], Xo) < bar, (i, rel(Xg[i], Xo))
         assert inf[i]["status"] == io.status == 0
         assert abs(int(inf[i]["iters"]) - io.iters) <= 1
         assert abs(inf[i]["lambda_max"] - io.lambda_max) <= 1e-12 * io.lambda_max
 
 
-def test_ozaki_1024(shp):
+@pytest.mark.parametrize("mode,bar", MODES)
+def test_ozaki_1024(shp, mode, bar):
     As = synth.psd_batch(1024, 2, synth.BASE_SEED + 2, "mixed")
-    Xg, inf, outs = _both(shp, As, 4)
+    Xg, inf, outs = _both(shp, As, 4, mode=mode)
     for i, (Xo, io) in enumerate(outs):
-        assert rel(Xg[i], Xo) < 1e-6
+        print(f"{mode} n=1024 matrix {i}: root rel err {rel(Xg[i], Xo):.3e}")
+        assert rel(Xg[i], Xo) < bar
         assert inf[i]["status"] == 0 and abs(int(inf[i]["iters"]) - io.iters) <= 1
 
 
+@pytest.mark.parametrize("mode,bar", MODES)
 @pytest.mark.parametrize("p", [1, 2, 3, 6, 8])
-def test_ozaki_root_orders(shp, p):
+def test_ozaki_root_orders(shp, p, mode, bar):
     As = synth.psd_batch(130, 2, synth.BASE_SEED + 190 + p, "mixed")
-    Xg, inf, outs = _both(shp, As, p)
+    Xg, inf, outs = _both(shp, As, p, mode=mode)
     for i, (Xo, io) in enumerate(outs):
-        assert rel(Xg[i], Xo) < 1e-6 * max(1, 4 // p) * (4 if p == 1 else 1), (p, i, rel(Xg[i], Xo))
+        assert rel(Xg[i], Xo) < bar * max(1, 4 // p) * (4 if p == 1 else 1), (p, i, rel(Xg[i], Xo))
         assert inf[i]["status"] == io.status
 
 
-def test_ozaki_edge_cases(shp):
+@pytest.mark.parametrize("mode,bar", MODES)
+def test_ozaki_edge_cases(shp, mode, bar):
     n = 40
     As = np.zeros((5, n, n), np.float32)
     As[0] = np.eye(n)                                    # converges at k = 0 (never reaches the INT8 loop)
@@ -73,7 +84,7 @@ def test_ozaki_edge_cases(shp):
     As[4] = synth.spectrum(n, 6)
     A = torch.from_numpy(As).to(DEV)
     X = torch.full_like(A, 7.0)
-    X, info = shp.inverse_pth_root_batched(A, 4, X=X, fp64_iters="ozaki")
+    X, info = shp.inverse_pth_root_batched(A, 4, X=X, fp64_iters=mode)
     torch.cuda.synchronize()
     Xg, inf = X.cpu().numpy(), shp.info_to_numpy(info)
     assert inf[0]["status"] == 0 and inf[0]["iters"] == 0
@@ -82,26 +93,29 @@ def test_ozaki_edge_cases(shp):
     assert inf[3]["status"] == 2 and np.all(Xg[3] == 7.0)
     for i in (1, 4):
         Xo, io = oroot.inverse_pth_root(As[i].astype(np.float64), 4)
-        assert rel(Xg[i], Xo) < 1e-6 and inf[i]["status"] == io.status
+        assert rel(Xg[i], Xo) < bar and inf[i]["status"] == io.status
 
 
-def test_ozaki_max_iter_and_stagnation(shp):
+@pytest.mark.parametrize("mode,bar", MODES)
+def test_ozaki_max_iter_and_stagnation(shp, mode, bar):
     As = synth.psd_batch(64, 2, 77, "wishart")
-    Xg, inf, outs = _both(shp, As, 4, max_iter=3)
+    Xg, inf, outs = _both(shp, As, 4, max_iter=3, mode=mode)
     for i, (Xo, io) in enumerate(outs):
         assert inf[i]["status"] == io.status == 1 and inf[i]["iters"] == io.iters == 3
-        assert rel(Xg[i], Xo) < 1e-6
-    Xg, inf, outs = _both(shp, As, 4, tol=0.0, max_iter=200)
+        assert rel(Xg[i], Xo) < bar
+    Xg, inf, outs = _both(shp, As, 4, tol=0.0, max_iter=200, mode=mode)
     for i, (Xo, io) in enumerate(outs):
         assert inf[i]["status"] == 1 and inf[i]["iters"] < 60
-        assert rel(Xg[i], Xo) < 1e-6
+        assert rel(Xg[i], Xo) < bar
 
 
-def test_ozaki_determinism_and_batch_independence(shp):
+@pytest.mark.parametrize("mode", ["ozaki", "ozaki6"])
+def test_ozaki_determinism_and_batch_independence(shp, mode):
     As = synth.psd_batch(128, 40, 31, "mixed")
-    X1, _ = shp.inverse_pth_root_batched(torch.from_numpy(As[:3]).to(DEV), 4, fp64_iters="ozaki")
-    X2, _ = shp.inverse_pth_root_batched(torch.from_numpy(As).to(DEV), 4, fp64_iters="ozaki")
-    X3, _ = shp.inverse_pth_root_batched(torch.from_numpy(As).to(DEV), 4, fp64_iters="ozaki")
+    X1, _ = shp.inverse_pth_root_batched(torch.from_numpy(As[:3]).to(DEV), 4, fp64_iters=mode)
+    X2, _ = shp.inverse_pth_root_batched(torch.from_numpy(As).to(DEV), 4, fp64_iters=mode)
+    X3, _ = shp.inverse_pth_root_batched(torch.from_numpy(As).to(DEV), 4, fp64_iters=mode)
     torch.cuda.synchronize()
     assert torch.equal(X2, X3)
     assert torch.equal(X1, X2[:3])
+

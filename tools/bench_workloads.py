@@ -33,7 +33,7 @@ import paper_2002_09018_b200 as shp  # noqa: E402
 import synth  # noqa: E402
 
 
-MODE = {"auto": "auto", "fp64": None, "ozaki": "ozaki", "hybrid": -1}
+MODE = {"auto": "auto", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki6": "ozaki6", "hybrid": -1}
 
 
 def timed(fn, steps, warmup, stream):
@@ -162,7 +162,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--block-size", type=int, default=1024)
-    ap.add_argument("--root-precision", default="auto", choices=["auto", "fp64", "ozaki", "hybrid"])
+    ap.add_argument("--root-precision", default="auto", choices=sorted(MODE))
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)

@@ -1,6 +1,6 @@
 // Standalone check of the Ozaki INT8 GEMM (paper_2002_09018_b200/csrc/ozaki.cuh):
 // GPU slicing + tcgen05.mma.kind::i8 products vs a host recomputation from the
-// same slices (exact integer sums, same fp64 combination order: bit-exact), and
+// same slices (exact integer sums rounded once to fp64: bit-exact), and
 // vs the plain fp64 product (accuracy).  Also times the 1024^2 product.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_2002_09018_b200/csrc \
 //        tools/microbench/ozaki_test.cu -lcuda -o tools/microbench/bin/ozaki_test
@@ -34,6 +34,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode() {
   return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
 }
 
+template <int kS>
 static int run(int n, int batch, bool sym, int reps) {
   const int np = (n + 63) / 64 * 64;
   const size_t mat = (size_t)np * np;
@@ -64,18 +65,18 @@ static int run(int n, int batch, bool sym, int reps) {
   CK(cudaMalloc(&dC, batch * mat * 8));
   CK(cudaMalloc(&sA, batch * np * 8));
   CK(cudaMalloc(&sB, batch * np * 8));
-  CK(cudaMalloc(&pA, batch * mat * oz::kS));
-  CK(cudaMalloc(&pB, batch * mat * oz::kS));
+  CK(cudaMalloc(&pA, batch * mat * kS));
+  CK(cudaMalloc(&pB, batch * mat * kS));
   CK(cudaMemcpy(dA, hA.data(), batch * mat * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, hB.data(), batch * mat * 8, cudaMemcpyHostToDevice));
   CK(cudaMemset(dC, 0, batch * mat * 8));
-  oz::slice_kernel<<<1184, 256>>>(dA, (int64_t)mat, n, np, batch, nullptr, nullptr, pA, sA);
-  oz::slice_kernel<<<1184, 256>>>(dB, (int64_t)mat, n, np, batch, nullptr, nullptr, pB, sB);
+  oz::slice_kernel<kS, false><<<1184, 256>>>(dA, (int64_t)mat, n, np, batch, nullptr, nullptr, pA, sA, nullptr, nullptr, 4);
+  oz::slice_kernel<kS, false><<<1184, 256>>>(dB, (int64_t)mat, n, np, batch, nullptr, nullptr, pB, sB, nullptr, nullptr, 4);
   CK(cudaGetLastError());
   CUtensorMap maps[2];
   auto enc = encode();
-  if (oz::make_plane_map(enc, &maps[0], pA, n, np, batch, oz::kBM) != CUDA_SUCCESS ||
-      oz::make_plane_map(enc, &maps[1], pB, n, np, batch, oz::kBN) != CUDA_SUCCESS) {
+  if (oz::make_plane_map(enc, &maps[0], pA, n, np, batch, oz::kBM, kS) != CUDA_SUCCESS ||
+      oz::make_plane_map(enc, &maps[1], pB, n, np, batch, oz::kBN, kS) != CUDA_SUCCESS) {
     printf("map encode failed\n");
     return 1;
   }
@@ -92,8 +93,8 @@ static int run(int n, int batch, bool sym, int reps) {
   a.jobs = 1;
   a.job[0] = {0, 1, sA, sB, dC, (int64_t)mat};
   a.p = 4;
-  const size_t smem = oz::gemm_smem_bytes();
-  CK(cudaFuncSetAttribute(oz::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = oz::gemm_smem_bytes<kS>();
+  CK(cudaFuncSetAttribute(oz::gemm_kernel<kS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   cudaEvent_t e0, e1;
@@ -102,19 +103,19 @@ static int run(int n, int batch, bool sym, int reps) {
   float ms = 0;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(e0);
-    oz::gemm_kernel<<<sms, oz::kThreads, smem>>>(a, dmaps);
+    oz::gemm_kernel<kS><<<sms, oz::kThreads, smem>>>(a, dmaps);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
     cudaEventElapsedTime(&ms, e0, e1);
   }
   std::vector<double> hC(batch * mat), hsA(batch * np), hsB(batch * np);
-  std::vector<int8_t> hpA(batch * mat * oz::kS), hpB(batch * mat * oz::kS);
+  std::vector<int8_t> hpA(batch * mat * kS), hpB(batch * mat * kS);
   CK(cudaMemcpy(hC.data(), dC, batch * mat * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(hsA.data(), sA, batch * np * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(hsB.data(), sB, batch * np * 8, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(hpA.data(), pA, batch * mat * oz::kS, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(hpB.data(), pB, batch * mat * oz::kS, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hpA.data(), pA, batch * mat * kS, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hpB.data(), pB, batch * mat * kS, cudaMemcpyDeviceToHost));
   // host: slices reproduce the inputs; exact recomputation; fp64 accuracy
   long mism = 0, checked = 0;
   double maxrel = 0, maxslice = 0;
@@ -123,8 +124,8 @@ static int run(int n, int batch, bool sym, int reps) {
     for (int i = 0; i < ncheck; ++i) {
       for (int j = 0; j < n; ++j) {  // slice reconstruction
         double rec = 0;
-        for (int s = 0; s < oz::kS; ++s)
-          rec += hpA[((size_t)(b * oz::kS + s) * np + i) * np + j] * std::ldexp(1.0, -6 - 7 * s);
+        for (int s = 0; s < kS; ++s)
+          rec += hpA[((size_t)(b * kS + s) * np + i) * np + j] * std::ldexp(1.0, -6 - 7 * s);
         rec *= hsA[b * np + i];
         const double x = hA[b * mat + (size_t)i * np + j];
         maxslice = std::max(maxslice, std::fabs(rec - x) / hsA[b * np + i]);
@@ -133,18 +134,20 @@ static int run(int n, int batch, bool sym, int reps) {
     for (int i = 0; i < ncheck; ++i)
       for (int j = 0; j < n; ++j) {
         if (sym && j < i) continue;
-        long long acc[oz::kS] = {0};
-        for (int d = 0; d < oz::kS; ++d)
+        long long acc[kS] = {0};
+        for (int d = 0; d < kS; ++d)
           for (int sa = 0; sa <= d; ++sa) {
             const int sb = d - sa;
             long long t = 0;
             for (int k = 0; k < n; ++k)
-              t += (long long)hpA[((size_t)(b * oz::kS + sa) * np + i) * np + k] *
-                   hpB[((size_t)(b * oz::kS + sb) * np + j) * np + k];
+              t += (long long)hpA[((size_t)(b * kS + sa) * np + i) * np + k] *
+                   hpB[((size_t)(b * kS + sb) * np + j) * np + k];
             acc[d] += t;
           }
-        double v = 0;
-        for (int d = oz::kS - 1; d >= 0; --d) v = v + (double)acc[d] * std::exp2(-12.0 - 7.0 * d);
+        // the exact sum rounded once (the kernel's int64 halves + one fma)
+        __int128 V = 0;
+        for (int d = 0; d < kS; ++d) V += (__int128)acc[d] << (7 * (kS - 1 - d));
+        const double v = std::ldexp((double)V, -12 - 7 * (kS - 1));
         const double c = v * hsA[b * np + i] * hsB[b * np + j];
         const double g = hC[b * mat + (size_t)i * np + j];
         ++checked;
@@ -167,20 +170,24 @@ static int run(int n, int batch, bool sym, int reps) {
         }
       }
   }
-  const double ops = 2.0 * oz::kS * (oz::kS + 1) / 2 * (double)n * n * n * batch * (sym ? 0.5625 : 1.0);
-  printf("n %d batch %d sym %d: %ld/%ld mismatches vs exact host, slice err %.2e (x 2^e), max |C - AB^T| / sum|ab| %.2e, "
+  const double ops = 2.0 * kS * (kS + 1) / 2 * (double)n * n * n * batch * (sym ? 0.5625 : 1.0);
+  printf("S %d n %d batch %d sym %d: %ld/%ld mismatches vs exact host, slice err %.2e (x 2^e), max |C - AB^T| / sum|ab| %.2e, "
          "%.3f ms, %.1f TOPS int8 (executed)\n",
-         n, batch, (int)sym, mism, checked, maxslice, maxrel, ms, ops / (ms * 1e-3) / 1e12);
+         kS, n, batch, (int)sym, mism, checked, maxslice, maxrel, ms, ops / (ms * 1e-3) / 1e12);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(sA); cudaFree(sB); cudaFree(pA); cudaFree(pB); cudaFree(dmaps);
   return mism != 0;
 }
 
 int main() {
   int bad = 0;
-  bad |= run(256, 2, false, 2);
-  bad |= run(200, 2, false, 2);
-  bad |= run(256, 2, true, 2);
-  bad |= run(1024, 148, true, 3);
+  bad |= run<7>(256, 2, false, 2);
+  bad |= run<7>(200, 2, false, 2);
+  bad |= run<7>(256, 2, true, 2);
+  bad |= run<7>(1024, 148, true, 3);
+  bad |= run<6>(256, 2, false, 2);
+  bad |= run<6>(200, 2, false, 2);
+  bad |= run<6>(256, 2, true, 2);
+  bad |= run<6>(1024, 148, true, 3);
   printf(bad ? "FAIL\n" : "PASS\n");
   return bad;
 }
