@@ -35,21 +35,23 @@ namespace shp {
 namespace oz {
 
 constexpr int kSMax = 7;                    // most slices per operand (workspace sizing)
-constexpr int kBM = 128, kBN = 64, kBK = 64;  // tile M, N; k-chunk in bytes (int8 elements): two K=32 MMA steps
-constexpr int kAPlane = kBM * kBK;          // 8 KB
-constexpr int kBPlane = kBN * kBK;          // 4 KB
-template <int S>
+constexpr int kBM = 128, kBN = 64;  // tile M, N
+// k-chunk BK bytes (int8 elements) per pipeline stage: BK / 32 K=32 MMA steps
+template <int S, int BK>
 struct Cfg {
   static_assert(S >= 4 && S <= kSMax, "4 <= slices <= 7 (int32 digit split, TMEM columns)");
-  static constexpr int kStageBytes = S * (kAPlane + kBPlane);  // 84 KB (S = 7), 72 KB (S = 6)
-  // S = 7: 2 stages (measured: 32-byte k-chunks x 4 stages were 4% slower); S = 6: 3 fit in 227 KB
-  static constexpr int kStages = S >= 7 ? 2 : 3;
+  static_assert(BK == 32 || BK == 64, "SWIZZLE_32B / SWIZZLE_64B k-chunks");
+  static constexpr int kAPlane = kBM * BK;                     // 8 KB (BK = 64)
+  static constexpr int kBPlane = kBN * BK;                     // 4 KB
+  static constexpr int kStageBytes = S * (kAPlane + kBPlane);  // 84 KB (S = 7, BK = 64), 72 KB (S = 6)
+  static constexpr int kStages = (225 * 1024) / kStageBytes;   // as many as fit: 2 / 5 (S = 7), 3 / 6 (S = 6)
 };
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 512;         // S accumulators x 64 columns (448 used for S = 7)
 
-// K-major tile of kBK-byte rows, swizzled to match the TMA map (SWIZZLE_32B:
+// K-major tile of BK-byte rows, swizzled to match the TMA map (SWIZZLE_32B:
 // layout type 6, 8-row atoms of 256 B; SWIZZLE_64B: type 4, 512 B)
+template <int kBK>
 TC_DEV uint64_t desc_sw(uint32_t smem_addr) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
@@ -74,36 +76,48 @@ TC_DEV void umma_i8(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc, u
 }
 
 // --------------------------------------------------------------- slicing
-// Digits of 8 consecutive elements r[0..7] of one row (sh = 6 - e_i): one
-// rounding to the 2^-(7S-1) grid (|V| < 2^(7S-1)), then balanced base-128 digits
-// by integer ops, lowest first: d = ((V + 64) mod 128) - 64, V = (V - d) / 128
-// (32-bit integer work: V = H 2^21 + L, the three low digits from L, the carry
-// into H, the S - 3 high digits from H, |H| < 2^27); dig[s] = 8 packed int8.
+// Digits of 8 consecutive elements r[0..7] of one row; scl = 2^(6 + 7(S-1) - e_i).
+// One rounding to the integer grid, V = rint(r scl) (|V| < 2^(7S-1)), then the
+// balanced base-128 digits d_s in [-64, 63] (top digit in [-64, 64]): with
+// C = 64 sum_s 128^s, W = V + C >= 0 has unsigned base-128 digits u_s = d_s + 64
+// (the carries of the balanced form are the carries of the addition).  Both
+// steps in one fma: r scl + (1.5 2^52 + C) lands in [2^52, 2^53), where the
+// fp64 grid is the integers, so its bit pattern is 0x4338000000000000 + W
+// (RN ties-to-even, as rint).  Digits by bit-field extracts, packed 4 per word
+// by bit-field inserts, d = u - 64 per byte (__vadd4).  dig[s] = 8 packed int8.
 template <int S>
-__device__ __forceinline__ void slice8(const double (&r)[8], int sh, uint32_t (&dig)[S][2]) {
+__device__ __forceinline__ void slice8(const double (&r)[8], double scl, uint32_t (&dig)[S][2]) {
+  constexpr long long kC = (64LL * ((1LL << (7 * S)) - 1)) / 127;  // 64 sum_{s<S} 128^s
+  constexpr double kMagic = (double)(0x18000000000000LL + kC);     // 1.5 2^52 + C, exact (< 2^53)
 #pragma unroll
   for (int s = 0; s < S; ++s) dig[s][0] = dig[s][1] = 0u;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const long long V = __double2ll_rn(ldexp(r[q], sh + 7 * (S - 1)));
-    int H = (int)(V >> 21);
-    int L = (int)(V & 0x1FFFFF);
-    int d;
+    const long long b = __double_as_longlong(fma(r[q], scl, kMagic));
+    const uint32_t lo = (uint32_t)b;                                    // W mod 2^32
+    const uint32_t hi = (uint32_t)(b >> 32) - 0x43380000u;              // W >> 32 (W < 2^50)
 #pragma unroll
-    for (int s = S - 1; s >= S - 3; --s) {
-      d = ((L + 64) & 127) - 64;
-      L = (L - d) >> 7;
-      dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
+    for (int s = 0; s < S; ++s) {
+      const int pos = 7 * (S - 1 - s), len = s == 0 ? 8 : 7;
+      uint32_t u;
+      if (pos + len <= 32) u = __funnelshift_r(lo, 0u, pos) & ((1u << len) - 1u);
+      else if (pos >= 32) u = (hi >> (pos - 32)) & ((1u << len) - 1u);
+      else u = __funnelshift_r(lo, hi, pos) & ((1u << len) - 1u);
+      dig[s][q >> 2] |= u << (8 * (q & 3));
     }
-    H += L;
-#pragma unroll
-    for (int s = S - 4; s >= 1; --s) {
-      d = ((H + 64) & 127) - 64;
-      H = (H - d) >> 7;
-      dig[s][q >> 2] |= ((uint32_t)d & 0xFFu) << (8 * (q & 3));
-    }
-    dig[0][q >> 2] |= ((uint32_t)H & 0xFFu) << (8 * (q & 3));
   }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    dig[s][0] = __vadd4(dig[s][0], 0xC0C0C0C0u);  // u - 64 in every byte (wrapping)
+    dig[s][1] = __vadd4(dig[s][1], 0xC0C0C0C0u);
+  }
+}
+
+// 2^(6 + 7(S-1) - e): the digit scale of a row with max < 2^e, e in [-960, 1024]
+// (row_exponent), built in the exponent field directly
+template <int S>
+__device__ __forceinline__ double digit_scale(int e) {
+  return __longlong_as_double((long long)(6 + 7 * (S - 1) - e + 1023) << 52);
 }
 
 // 8 consecutive elements of a row from column j (two 32-byte loads; the row
@@ -140,7 +154,7 @@ __device__ __forceinline__ int row_exponent(double mx) {
   mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
-  return e;
+  return max(e, -960);          // keeps digit_scale<S>(e) a normal double (rows below 2^-960: fewer digits)
 }
 
 // T_ij = ((p + 1) delta_ij - M_ij) / p, the same expression as the fp64 root's
@@ -150,18 +164,17 @@ __device__ __forceinline__ double t_of(double m, bool diag, double pp1, double i
 }
 
 // One warp per (matrix, row): scale[mat*np + i] = 2^e_i, planes
-// [(mat*S + s)*np + i]*np + j = d_s(A_ij) for j < n.  MT: the source is M_k and
-// the same pass also slices T_k = ((p+1)I - M_k)/p into (planes_t, scale_t), so
-// T_k never round-trips through HBM in fp64.  Rows of n <= 1024 are held in
-// registers (32 doubles per lane, 8 KB in flight per warp): ONE pass over HBM
-// for the row maxima and the digits; longer rows take two passes (the second
-// mostly from L1).
-template <int S, bool MT>
-__global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ src, int64_t mat_stride, int n, int np,
-                                                    int batch, const int* __restrict__ act, const int* nact,
-                                                    int8_t* __restrict__ planes, double* __restrict__ scale,
-                                                    int8_t* __restrict__ planes_t, double* __restrict__ scale_t,
-                                                    int p) {
+// [(mat*S + s)*np + i]*np + j = d_s(A_ij) for j < n, where A = src, or, with TM,
+// A = T_k = ((p+1)I - M_k)/p computed on the fly from src = M_k (T_k is never
+// stored in fp64).  Rows of n <= 1024 are held in registers (32 doubles per
+// lane, 8 KB in flight per warp, 16 warps per SM): ONE pass over HBM for the
+// row maximum and the digits (measured 6.4 TB/s); longer rows take two passes
+// (the second mostly from L1).
+template <int S, bool TM>
+__global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict__ src, int64_t mat_stride, int n,
+                                                       int np, int batch, const int* __restrict__ act,
+                                                       const int* nact, int8_t* __restrict__ planes,
+                                                       double* __restrict__ scale, int p) {
   constexpr int kRegChunks = 4;  // 4 x 256 columns per warp held in registers
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -173,10 +186,10 @@ __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ s
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
-    const int64_t prow_off = ((int64_t)mat * S * np + i) * np;
+    int8_t* prow = planes + ((int64_t)mat * S * np + i) * np;
     if (n <= 256 * kRegChunks) {
       double r[kRegChunks][8];
-      double mx = 0.0, mt = 0.0;
+      double mx = 0.0;
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
         const int j = 256 * c + 8 * lane;
@@ -186,183 +199,44 @@ __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ s
 #pragma unroll
           for (int q = 0; q < 8; ++q) r[c][q] = 0.0;
         }
+        if (TM) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          mx = fmax(mx, fabs(r[c][q]));
-          if (MT) mt = fmax(mt, fabs(t_of(r[c][q], j + q == i, pp1, inv_p)));
+          for (int q = 0; q < 8; ++q) r[c][q] = (j + q < n) ? t_of(r[c][q], j + q == i, pp1, inv_p) : 0.0;
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx = fmax(mx, fabs(r[c][q]));
       }
       const int e = row_exponent(mx);
-      const int et = MT ? row_exponent(mt) : 0;
-      if (lane == 0) {
-        scale[(int64_t)mat * np + i] = ldexp(1.0, e);
-        if (MT) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
-      }
+      if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
         const int j = 256 * c + 8 * lane;
         if (j < n) {
           uint32_t dig[S][2];
-          slice8<S>(r[c], 6 - e, dig);
+          slice8<S>(r[c], digit_scale<S>(e), dig);
 #pragma unroll
-          for (int s = 0; s < S; ++s) store8<S>(planes + prow_off + s * plane_pitch, j, n, dig[s]);
-          if (MT) {
-            double t[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) t[q] = t_of(r[c][q], j + q == i, pp1, inv_p);
-            slice8<S>(t, 6 - et, dig);
-#pragma unroll
-            for (int s = 0; s < S; ++s) store8<S>(planes_t + prow_off + s * plane_pitch, j, n, dig[s]);
-          }
+          for (int s = 0; s < S; ++s) store8<S>(prow + s * plane_pitch, j, n, dig[s]);
         }
       }
     } else {
-      double mx = 0.0, mt = 0.0;
-      for (int j = lane; j < n; j += 32) {
-        mx = fmax(mx, fabs(row[j]));
-        if (MT) mt = fmax(mt, fabs(t_of(row[j], j == i, pp1, inv_p)));
-      }
+      double mx = 0.0;
+      for (int j = lane; j < n; j += 32) mx = fmax(mx, fabs(TM ? t_of(row[j], j == i, pp1, inv_p) : row[j]));
       const int e = row_exponent(mx);
-      const int et = MT ? row_exponent(mt) : 0;
-      if (lane == 0) {
-        scale[(int64_t)mat * np + i] = ldexp(1.0, e);
-        if (MT) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
-      }
+      if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
       for (int j = 8 * lane; j < n; j += 256) {
         double r[8];
         load8(row, j, n, r);
+        if (TM) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? t_of(r[q], j + q == i, pp1, inv_p) : 0.0;
+        }
         uint32_t dig[S][2];
-        slice8<S>(r, 6 - e, dig);
+        slice8<S>(r, digit_scale<S>(e), dig);
 #pragma unroll
-        for (int s = 0; s < S; ++s) store8<S>(planes + prow_off + s * plane_pitch, j, n, dig[s]);
-        if (MT) {
-          double t[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) t[q] = t_of(r[q], j + q == i, pp1, inv_p);
-          slice8<S>(t, 6 - et, dig);
-#pragma unroll
-          for (int s = 0; s < S; ++s) store8<S>(planes_t + prow_off + s * plane_pitch, j, n, dig[s]);
-        }
+        for (int s = 0; s < S; ++s) store8<S>(prow + s * plane_pitch, j, n, dig[s]);
       }
     }
   }
-}
-
-// Rows of n <= 1024 (every Ozaki root of the Transformer-Big plan): each warp
-// streams its rows through a ring of kSliceRing shared-memory buffers with
-// cp.async (16-byte copies, nothing held in registers while in flight: 16-24
-// rows = 128-192 KB in flight per SM, enough to cover HBM latency), then takes
-// the row maxima and the digits from shared memory.  Same outputs as
-// slice_kernel.  Buffer layout: 16-byte segment s at s + s/8 (one pad segment
-// per 128 B), so the per-lane 64-byte column groups read conflict-free.
-constexpr int kSliceWarps = 8, kSliceRing = 3, kSliceRowMax = 1024;
-constexpr int kSliceRowSegs = kSliceRowMax / 2 + kSliceRowMax / 16;  // 16-byte segments incl. padding
-constexpr size_t kSliceSmem = (size_t)kSliceWarps * kSliceRing * kSliceRowSegs * 16;  // 216 KB
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// 8 consecutive columns j = 8 lane + 256 c of a staged row (4 conflict-free 16-byte reads)
-__device__ __forceinline__ void smem_load8(const double2* rb, int c, int lane, double (&r)[8]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int sg = 128 * c + 4 * lane + k;
-    const double2 u = rb[sg + (sg >> 3)];
-    r[2 * k] = u.x;
-    r[2 * k + 1] = u.y;
-  }
-}
-
-template <int S, bool MT>
-__global__ void __launch_bounds__(kSliceWarps * 32, 1) slice_smem_kernel(
-    const double* __restrict__ src, int64_t mat_stride, int n, int np, int batch, const int* __restrict__ act,
-    const int* nact, int8_t* __restrict__ planes, double* __restrict__ scale, int8_t* __restrict__ planes_t,
-    double* __restrict__ scale_t, int p) {
-  extern __shared__ __align__(16) uint8_t slice_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* ring = reinterpret_cast<double2*>(slice_smem) + (size_t)warp * kSliceRing * kSliceRowSegs;
-  const int64_t gw = (int64_t)blockIdx.x * kSliceWarps + warp, nw = (int64_t)gridDim.x * kSliceWarps;
-  const int na = act ? *nact : batch;
-  const int64_t rows = (int64_t)na * n;
-  const int segs = (n + 7) / 8 * 4;  // 16-byte segments copied per row (columns rounded up to 8 <= np)
-  const int64_t plane_pitch = (int64_t)np * np;
-  const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p;
-  auto row_ptr = [&](int64_t rid, int& mat, int& i) {
-    const int pos = (int)(rid / n);
-    i = (int)(rid - (int64_t)pos * n);
-    mat = act ? act[pos] : pos;
-    return src + mat * mat_stride + (int64_t)i * np;
-  };
-  auto issue = [&](int64_t rid, int buf) {
-    if (rid < rows) {
-      int mat, i;
-      const double* row = row_ptr(rid, mat, i);
-      double2* dst = ring + buf * kSliceRowSegs;
-      for (int sg = lane; sg < segs; sg += 32) cp_async16(dst + sg + (sg >> 3), row + 2 * sg);
-    }
-    cp_async_commit();  // empty groups keep the group count uniform
-  };
-#pragma unroll
-  for (int q = 0; q < kSliceRing - 1; ++q) issue(gw + q * nw, q);
-  int it = 0;
-  for (int64_t rid = gw; rid < rows; rid += nw, ++it) {
-    issue(rid + (int64_t)(kSliceRing - 1) * nw, (it + kSliceRing - 1) % kSliceRing);
-    cp_async_wait<kSliceRing - 1>();
-    __syncwarp();
-    const double2* rb = ring + (it % kSliceRing) * kSliceRowSegs;
-    int mat, i;
-    row_ptr(rid, mat, i);
-    double mx = 0.0, mt = 0.0;
-#pragma unroll
-    for (int c = 0; c < kSliceRowMax / 256; ++c) {
-      const int j = 256 * c + 8 * lane;
-      if (j < n) {
-        double r[8];
-        smem_load8(rb, c, lane, r);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double v = (j + q < n) ? r[q] : 0.0;
-          mx = fmax(mx, fabs(v));
-          if (MT) mt = fmax(mt, fabs(t_of(v, j + q == i, pp1, inv_p)));
-        }
-      }
-    }
-    const int e = row_exponent(mx);
-    const int et = MT ? row_exponent(mt) : 0;
-    if (lane == 0) {
-      scale[(int64_t)mat * np + i] = ldexp(1.0, e);
-      if (MT) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
-    }
-    const int64_t prow_off = ((int64_t)mat * S * np + i) * np;
-#pragma unroll 1
-    for (int c = 0; c < kSliceRowMax / 256; ++c) {
-      const int j = 256 * c + 8 * lane;
-      if (j < n) {
-        double r[8];
-        smem_load8(rb, c, lane, r);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? r[q] : 0.0;
-        uint32_t dig[S][2];
-        slice8<S>(r, 6 - e, dig);
-#pragma unroll
-        for (int s2 = 0; s2 < S; ++s2) store8<S>(planes + prow_off + s2 * plane_pitch, j, n, dig[s2]);
-        if (MT) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) r[q] = t_of(r[q], j + q == i, pp1, inv_p);
-          slice8<S>(r, 6 - et, dig);
-#pragma unroll
-          for (int s2 = 0; s2 < S; ++s2) store8<S>(planes_t + prow_off + s2 * plane_pitch, j, n, dig[s2]);
-        }
-      }
-    }
-    __syncwarp();  // every lane done with this buffer before it is refilled
-  }
-  cp_async_wait<0>();
 }
 
 // --------------------------------------------------------------- GEMM
@@ -372,21 +246,29 @@ __global__ void __launch_bounds__(kSliceWarps * 32, 1) slice_smem_kernel(
 __device__ __forceinline__ int exp2_of(double x) {
   return (int)((__double_as_longlong(x) >> 52) & 0x7FF) - 1023;
 }
-// x 2^k exactly by exponent arithmetic; zero, inf and NaN pass through; results
-// that would leave the normal range take the fp64 multiply (never on the
-// Newton iterates' magnitudes)
+// x 2^k by two fp64 multiplies with exact power-of-two factors (|k| < 2000);
+// out of line so the compiler cannot if-convert it into the common path
+__device__ __noinline__ double scale2_slow(double x, int k) {
+  if (x == 0.0 || !isfinite(x)) return x;
+  const int k1 = k / 2;
+  return x * __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k - k1 + 1023) << 52);
+}
+// x 2^k exactly by exponent arithmetic (integer pipe); zero, subnormal, inf,
+// NaN or a result outside the normal range take scale2_slow (never on the
+// Newton iterates' magnitudes, except exact zeros)
 __device__ __forceinline__ double scale2(double x, int k) {
   const long long b = __double_as_longlong(x);
   const int ex = (int)((b >> 52) & 0x7FF);
   const int ne = ex + k;
   if (ex != 0 && ex != 0x7FF && ne >= 1 && ne <= 2046) return __longlong_as_double(b + ((long long)k << 52));
-  if (ex == 0x7FF || x == 0.0) return x;
-  const int k1 = k / 2;  // two exact power-of-two factors (|k| < 2000)
-  return x * __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k - k1 + 1023) << 52);
+  return scale2_slow(x, k);
 }
-// |x| as an unsigned bit pattern: ordered like |x| for non-NaN, NaN above +inf
+// |x| as an unsigned bit pattern: ordered like |x| for non-NaN, NaN above +inf.
+// In PTX so the front end cannot turn it back into an fp64 fabs (DADD |x|).
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
-  return (unsigned long long)__double_as_longlong(x) & 0x7FFFFFFFFFFFFFFFull;
+  unsigned long long r;
+  asm("and.b64 %0, %1, 0x7FFFFFFFFFFFFFFF;" : "=l"(r) : "l"(__double_as_longlong(x)));
+  return r;
 }
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
 
@@ -439,10 +321,12 @@ TC_DEV void oz_decode(const OzArgs& a, int per_mat, int64_t tile, int& mat, int&
   mat = a.act ? a.act[pos] : pos;
 }
 
-template <int S>
+template <int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
-  constexpr int kS = S, kStages = Cfg<S>::kStages, kStageBytes = Cfg<S>::kStageBytes;
+  using C = Cfg<S, BK>;
+  constexpr int kS = S, kBK = BK, kStages = C::kStages, kStageBytes = C::kStageBytes;
+  constexpr int kAPlane = C::kAPlane, kBPlane = C::kBPlane;
   const int na = a.act ? *a.nact : a.batch;
   if (na == 0) return;
   const int per_mat = oz_tiles_per_mat(a);
@@ -512,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (tc::elect_one()) {
           const uint32_t s0 = tc::smem_u32(smem + stage * kStageBytes);
           // plane and k-step offsets are added to the 14-bit (addr >> 4) field
-          const uint64_t dA0 = desc_sw(s0), dB0 = desc_sw(s0 + kS * kAPlane);
+          const uint64_t dA0 = desc_sw<kBK>(s0), dB0 = desc_sw<kBK>(s0 + kS * kAPlane);
 #pragma unroll
           for (int k = 0; k < kBK / 32; ++k) {
             const uint64_t adv = (uint64_t)((k * 32) >> 4);  // 32 bytes per K=32 step
@@ -592,12 +476,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           v[c0 + e] = fma(hd, (double)(1LL << (7 * (kS - 4))), ld);
         }
       }
+      // pin the fp64 conversions before the release: the arrive's address depends
+      // on every v (an OR of the high words; the offset is 0 at run time since
+      // n > 0) -- otherwise ptxas sinks some of them past the arrive, into the
+      // next tile's MMAs, where fp64 instructions crawl
+      uint32_t dep = 0u;
+#pragma unroll
+      for (int e = 0; e < kBN; ++e) dep |= (uint32_t)(__double_as_longlong(v[e]) >> 32);
       tc::tc_fence_before();
-      tc::mbar_arrive(tmem_empty);
+      tc::mbar_arrive(tmem_empty + ((dep == 0xFFFFFFFFu && a.n < 0) ? 1 : 0));
       // phase 2: scale by 2^(e_i + f_j - 12 - 7(S-1)) (exponent arithmetic), store
-      // row-major (16-byte vectors) and mirrored; M-update: max|M - I| on the
+      // row-major (16-byte vectors) and mirrored, evict-first (st.global.cs: the
+      // outputs must not push the operand planes other tiles still read out of L2); M-update: max|M - I| on the
       // bit patterns (T_{k+1} is sliced from M_{k+1} by slice_kernel<S, true>)
-      unsigned long long emax_bits = 0ull;
+      unsigned long long emax_bits = 0ull, diag_bits = 0ull;
       if (row_ok) {
         const int j0 = tj * kBN;
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
@@ -611,31 +503,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           v[e] = c0;
           v[e + 1] = c1;
           if (full_row) {
-            *reinterpret_cast<double2*>(orow + e) = make_double2(c0, c1);
+            __stcs(reinterpret_cast<double2*>(orow + e), make_double2(c0, c1));
           } else {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               const int j = j0 + e + q;
-              if (j < a.n && (!a.sym || j >= i)) orow[e + q] = q ? c1 : c0;
+              if (j < a.n && (!a.sym || j >= i)) __stcs(orow + e + q, q ? c1 : c0);
             }
           }
-          if (mup) {  // max|M_{k+1} - I| (integer max of |c| off the diagonal)
+          if (mup) {  // max|M_{k+1} - I|: integer max of |c| off the diagonal; the diagonal element kept
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               const int j = j0 + e + q;
               if (j < a.n && (!a.sym || j >= i)) {
                 const double c = q ? c1 : c0;
-                emax_bits = umax64(emax_bits, i != j ? abs_bits(c) : abs_bits(c - 1.0));
+                emax_bits = umax64(emax_bits, j == i ? 0ull : abs_bits(c));
+                diag_bits = j == i ? (unsigned long long)__double_as_longlong(c) : diag_bits;
               }
             }
           }
         }
+        // the one fp64 subtraction of the M-update, once per row of a diagonal tile
+        if (mup && i >= j0 && i < j0 + kBN) emax_bits = umax64(emax_bits, abs_bits(__longlong_as_double((long long)diag_bits) - 1.0));
         if (a.sym) {  // mirror: lanes are consecutive rows -> coalesced
 #pragma unroll
           for (int e = 0; e < kBN; ++e) {
             const int j = j0 + e;
             if (j >= a.n || j <= i) continue;
-            out[(int64_t)j * a.np + i] = v[e];
+            __stcs(out + (int64_t)j * a.np + i, v[e]);
           }
         }
       }
@@ -656,14 +551,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
 }
 
-template <int S>
-inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S>::kStages * Cfg<S>::kStageBytes + 256; }
+template <int S, int BK>
+inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S, BK>::kStages * Cfg<S, BK>::kStageBytes + 256; }
 
 // 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * S),
 // row pitch np bytes, plane pitch np*np bytes, box (64 B, box_rows, 1), SWIZZLE_64B
 template <class Encode>
 inline CUresult make_plane_map(Encode enc, CUtensorMap* out, const int8_t* base, int n, int np, int batch,
-                               int box_rows, int S) {
+                               int box_rows, int S, int kBK) {
   cuuint64_t gdim[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch * S};
   cuuint64_t gstride[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
   cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};

@@ -24,6 +24,8 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ozaki.cuh"
+
+#include <cstdlib>
 #include "tc_common.cuh"
 #include "tc_gemm.h"
 
@@ -527,15 +529,15 @@ size_t root_ozaki_ws_bytes(int batch, int n) {
   return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap);
 }
 
-template <int S>
+template <int S, int BK>
 static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
                                const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x,
                                int* act, int* nact, void* oz_ws, cudaStream_t stream, int64_t* launches) {
   constexpr int kS = S;
   static bool configured = false;
-  const size_t smem = oz::gemm_smem_bytes<S>();
+  const size_t smem = oz::gemm_smem_bytes<S, BK>();
   if (!configured) {
-    if (cudaFuncSetAttribute(oz::gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(oz::gemm_kernel<S, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel)");
     configured = true;
@@ -561,8 +563,9 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
       return set_error(SHAMPOO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     for (int q2 = 0; q2 < OZ_SLOTS; ++q2) {
-      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM, kS) != CUDA_SUCCESS ||
-          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN, kS) !=
+      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM, kS, BK) !=
+              CUDA_SUCCESS ||
+          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN, kS, BK) !=
               CUDA_SUCCESS)
         return set_error(SHAMPOO_ERR_CUDA, "ozaki: cuTensorMapEncodeTiled failed");
     }
@@ -572,37 +575,17 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   const int64_t mstride = (int64_t)kTailRegions * np * np;
   auto region = [&](int r) { return bufs + (int64_t)r * np * np; };
   const int slice_grid = 8 * num_sms();
-  static bool slice_configured = false;
-  if (!slice_configured) {
-    if (cudaFuncSetAttribute(oz::slice_smem_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)oz::kSliceSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(oz::slice_smem_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)oz::kSliceSmem) != cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(ozaki slice_smem_kernel)");
-    slice_configured = true;
-  }
-  // MT: M_k and T_k = ((p+1)I - M_k)/p in one pass over M_k (T_k never stored in fp64)
-  auto slice_any = [&](int reg, int slot, bool mt) {
-    int8_t* pt = mt ? slot_planes_ptr(OZ_ST) : nullptr;
-    double* st = mt ? slot_scale(OZ_ST) : nullptr;
-    if (n <= oz::kSliceRowMax) {  // rows staged through shared memory (one CTA per SM)
-      if (mt)
-        oz::slice_smem_kernel<S, true><<<num_sms(), oz::kSliceWarps * 32, oz::kSliceSmem, stream>>>(
-            region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
-      else
-        oz::slice_smem_kernel<S, false><<<num_sms(), oz::kSliceWarps * 32, oz::kSliceSmem, stream>>>(
-            region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
-    } else if (mt) {
+  // tm: slice T_k = ((p+1)I - M_k)/p computed from M_k on the fly (T_k never stored in fp64)
+  auto slice_any = [&](int reg, int slot, bool tm) {
+    if (tm)
       oz::slice_kernel<S, true><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
-                                                               slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
-    } else {
+                                                               slot_planes_ptr(slot), slot_scale(slot), p);
+    else
       oz::slice_kernel<S, false><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
-                                                                slot_planes_ptr(slot), slot_scale(slot), pt, st, p);
-    }
+                                                                slot_planes_ptr(slot), slot_scale(slot), p);
     ++*launches;
   };
   auto slice = [&](int reg, int slot) { slice_any(reg, slot, false); };
-  auto slice_mt = [&](int reg) { slice_any(reg, OZ_SM, true); };
   oz::OzArgs base;
   std::memset(&base, 0, sizeof base);
   base.act = act;
@@ -630,7 +613,7 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   auto gemm = [&](const oz::OzArgs& a) {
     void* tok;
     prof_begin_launch("ozaki_gemm", stream, &tok);
-    oz::gemm_kernel<S><<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
+    oz::gemm_kernel<S, BK><<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
     prof_end_launch(tok, stream);
     ++*launches;
   };
@@ -639,7 +622,8 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   for (int k = 0; k < max_iter; ++k) {
     const int xs = k & 1;
     slice(RX0 + xs, OZ_SX);
-    slice_mt(RM0 + xs);
+    slice(RM0 + xs, OZ_SM);
+    slice_any(RM0 + xs, OZ_ST, true);  // T_k from M_k
     // P1: X_{k+1} = X_k T ; S0 = T T (p >= 2)
     oz::OzArgs a1 = base;
     a1.jobs = p >= 2 ? 2 : 1;
@@ -691,13 +675,21 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
 int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
                       const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
                       int* nact, void* oz_ws, int slices, cudaStream_t stream, int64_t* launches) {
-  switch (slices) {
-    case 6:
-      return root_ozaki_launch_s<6>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
-                                    nact, oz_ws, stream, launches);
-    case 7:
-      return root_ozaki_launch_s<7>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
-                                    nact, oz_ws, stream, launches);
+  // k-chunk of the GEMM pipeline (A/B knob while tuning: SHAMPOO_OZ_BK=32 -> 32-byte chunks, deeper ring)
+  static const int bk = (getenv("SHAMPOO_OZ_BK") && atoi(getenv("SHAMPOO_OZ_BK")) == 32) ? 32 : 64;
+  switch (slices * 100 + bk) {
+    case 664:
+      return root_ozaki_launch_s<6, 64>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
+                                        nact, oz_ws, stream, launches);
+    case 632:
+      return root_ozaki_launch_s<6, 32>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
+                                        nact, oz_ws, stream, launches);
+    case 764:
+      return root_ozaki_launch_s<7, 64>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
+                                        nact, oz_ws, stream, launches);
+    case 732:
+      return root_ozaki_launch_s<7, 32>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
+                                        nact, oz_ws, stream, launches);
     default:
       return set_error(SHAMPOO_ERR_INVALID_ARG, "ozaki root: slices must be 6 or 7 (got %d)", slices);
   }

@@ -34,7 +34,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode() {
   return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
 }
 
-template <int kS>
+template <int kS, int BK = 64>
 static int run(int n, int batch, bool sym, int reps) {
   const int np = (n + 63) / 64 * 64;
   const size_t mat = (size_t)np * np;
@@ -70,13 +70,13 @@ static int run(int n, int batch, bool sym, int reps) {
   CK(cudaMemcpy(dA, hA.data(), batch * mat * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, hB.data(), batch * mat * 8, cudaMemcpyHostToDevice));
   CK(cudaMemset(dC, 0, batch * mat * 8));
-  oz::slice_kernel<kS, false><<<1184, 256>>>(dA, (int64_t)mat, n, np, batch, nullptr, nullptr, pA, sA, nullptr, nullptr, 4);
-  oz::slice_kernel<kS, false><<<1184, 256>>>(dB, (int64_t)mat, n, np, batch, nullptr, nullptr, pB, sB, nullptr, nullptr, 4);
+  oz::slice_kernel<kS, false><<<1184, 256>>>(dA, (int64_t)mat, n, np, batch, nullptr, nullptr, pA, sA, 4);
+  oz::slice_kernel<kS, false><<<1184, 256>>>(dB, (int64_t)mat, n, np, batch, nullptr, nullptr, pB, sB, 4);
   CK(cudaGetLastError());
   CUtensorMap maps[2];
   auto enc = encode();
-  if (oz::make_plane_map(enc, &maps[0], pA, n, np, batch, oz::kBM, kS) != CUDA_SUCCESS ||
-      oz::make_plane_map(enc, &maps[1], pB, n, np, batch, oz::kBN, kS) != CUDA_SUCCESS) {
+  if (oz::make_plane_map(enc, &maps[0], pA, n, np, batch, oz::kBM, kS, BK) != CUDA_SUCCESS ||
+      oz::make_plane_map(enc, &maps[1], pB, n, np, batch, oz::kBN, kS, BK) != CUDA_SUCCESS) {
     printf("map encode failed\n");
     return 1;
   }
@@ -93,8 +93,8 @@ static int run(int n, int batch, bool sym, int reps) {
   a.jobs = 1;
   a.job[0] = {0, 1, sA, sB, dC, (int64_t)mat};
   a.p = 4;
-  const size_t smem = oz::gemm_smem_bytes<kS>();
-  CK(cudaFuncSetAttribute(oz::gemm_kernel<kS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = oz::gemm_smem_bytes<kS, BK>();
+  CK(cudaFuncSetAttribute(oz::gemm_kernel<kS, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   cudaEvent_t e0, e1;
@@ -103,7 +103,7 @@ static int run(int n, int batch, bool sym, int reps) {
   float ms = 0;
   for (int r = 0; r < reps; ++r) {
     cudaEventRecord(e0);
-    oz::gemm_kernel<kS><<<sms, oz::kThreads, smem>>>(a, dmaps);
+    oz::gemm_kernel<kS, BK><<<sms, oz::kThreads, smem>>>(a, dmaps);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
@@ -171,9 +171,9 @@ static int run(int n, int batch, bool sym, int reps) {
       }
   }
   const double ops = 2.0 * kS * (kS + 1) / 2 * (double)n * n * n * batch * (sym ? 0.5625 : 1.0);
-  printf("S %d n %d batch %d sym %d: %ld/%ld mismatches vs exact host, slice err %.2e (x 2^e), max |C - AB^T| / sum|ab| %.2e, "
+  printf("S %d BK %d n %d batch %d sym %d: %ld/%ld mismatches vs exact host, slice err %.2e (x 2^e), max |C - AB^T| / sum|ab| %.2e, "
          "%.3f ms, %.1f TOPS int8 (executed)\n",
-         kS, n, batch, (int)sym, mism, checked, maxslice, maxrel, ms, ops / (ms * 1e-3) / 1e12);
+         kS, BK, n, batch, (int)sym, mism, checked, maxslice, maxrel, ms, ops / (ms * 1e-3) / 1e12);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(sA); cudaFree(sB); cudaFree(pA); cudaFree(pB); cudaFree(dmaps);
   return mism != 0;
 }
@@ -188,6 +188,9 @@ int main() {
   bad |= run<6>(200, 2, false, 2);
   bad |= run<6>(256, 2, true, 2);
   bad |= run<6>(1024, 148, true, 3);
+  bad |= run<7, 32>(200, 2, false, 2);
+  bad |= run<7, 32>(1024, 148, true, 3);
+  bad |= run<6, 32>(1024, 148, true, 3);
   printf(bad ? "FAIL\n" : "PASS\n");
   return bad;
 }
