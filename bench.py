@@ -61,8 +61,10 @@ def _int8_peak():
     except (OSError, ValueError):
         pass
     return 2 * 1687.1, "burst (earlier measurement; MEASURED_PEAKS.json absent)"
-# dram read + write of one Ozaki product stage per 1024^2 matrix (ncu --set full, 148-matrix dual stage)
-OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = (2.296e9 + 2.448e9) / 148
+# dram read + write per Ozaki GEMM launch per 1024^2 matrix: the mean over the three product stages of one
+# iteration ({X T, T T} 20.2 GB, T^2 T^2 8.5 GB, T^4 M 12.2 GB for 528 matrices), ncu launch list
+# profiles/r01v_launches_root528_summary.txt
+OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = ((11.35 + 8.84) + (4.12 + 4.39) + (7.76 + 4.39)) / 3 * 1e9 / 528
 ROOT_MODE = {"auto": "auto", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki6": "ozaki6", "hybrid": -1}
 ROOT_SLICES = {"auto": 7, "auto6": 6, "ozaki": 7, "ozaki6": 6}
 ROOT_LABEL = {"auto": "auto: ozaki (INT8 tcgen05, 7 slices, exact int32 accumulation) for n >= 512, fp64 DMMA below",
@@ -329,8 +331,8 @@ def main():
         peak, peak_kind = _int8_peak()
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
                 "frac": achieved / peak, "traffic": OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE * cnt,
-                "traffic_note": "dram bytes per launch (one symmetric product stage), ncu --set full of a 148-matrix "
-                                "stage scaled per matrix",
+                "traffic_note": "dram read+write bytes per GEMM launch (mean of the 3 product stages of an "
+                                "iteration), ncu launch list of a 528-matrix root call scaled per matrix",
                 "kernel": f"oz::gemm_kernel (INT8 tcgen05 Ozaki products, batch {cnt} x {n}^2, p=4)",
                 "kernel_ms": gemm_ms / max(1, gemm_launches), "kernel_launches": gemm_launches,
                 "ops_per_launch": ops / max(1, gemm_launches),

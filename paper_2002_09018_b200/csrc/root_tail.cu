@@ -24,8 +24,6 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ozaki.cuh"
-
-#include <cstdlib>
 #include "tc_common.cuh"
 #include "tc_gemm.h"
 
@@ -675,20 +673,14 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
 int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
                       const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
                       int* nact, void* oz_ws, int slices, cudaStream_t stream, int64_t* launches) {
-  // k-chunk of the GEMM pipeline (A/B knob while tuning: SHAMPOO_OZ_BK=32 -> 32-byte chunks, deeper ring)
-  static const int bk = (getenv("SHAMPOO_OZ_BK") && atoi(getenv("SHAMPOO_OZ_BK")) == 32) ? 32 : 64;
-  switch (slices * 100 + bk) {
-    case 664:
+  // 64-byte k-chunks (measured on B200: 32-byte chunks with a 5-deep ring are 13% slower on the
+  // 528-root call -- 585 vs 673 roots/s; SWIZZLE_32B TMA rows are short requests)
+  switch (slices) {
+    case 6:
       return root_ozaki_launch_s<6, 64>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
                                         nact, oz_ws, stream, launches);
-    case 632:
-      return root_ozaki_launch_s<6, 32>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
-                                        nact, oz_ws, stream, launches);
-    case 764:
+    case 7:
       return root_ozaki_launch_s<7, 64>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
-                                        nact, oz_ws, stream, launches);
-    case 732:
-      return root_ozaki_launch_s<7, 32>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
                                         nact, oz_ws, stream, launches);
     default:
       return set_error(SHAMPOO_ERR_INVALID_ARG, "ozaki root: slices must be 6 or 7 (got %d)", slices);
