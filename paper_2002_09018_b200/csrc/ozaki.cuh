@@ -321,11 +321,31 @@ TC_DEV void oz_decode(const OzArgs& a, int per_mat, int64_t tile, int& mat, int&
   mat = a.act ? a.act[pos] : pos;
 }
 
+// Each stage's planes arrive in 4 groups with their own full barriers, in the
+// order the MMAs consume them, so the first MMAs of a stage start while the
+// rest of its 84 KB is in flight: A plane sa in group gA(sa), B planes 0-3 in
+// group 0, 4+ in group 1; MMA (sa, tb) needs group max(gA(sa), gB(tb)), which
+// is nondecreasing in issue order (S = 7: 24 / 20 / 16 / 24 KB).
+constexpr int kGroups = 4;
+__host__ __device__ constexpr int grp_a(int sa) { return sa == 0 ? 0 : sa == 1 ? 1 : sa <= 3 ? 2 : 3; }
+__host__ __device__ constexpr int grp_b(int tb) { return tb < 4 ? 0 : 1; }
+template <int S, int BK>
+__host__ __device__ constexpr int grp_bytes(int g) {
+  int b = 0;
+  for (int s = 0; s < S; ++s) {
+    if (grp_a(s) == g) b += Cfg<S, BK>::kAPlane;
+    if (grp_b(s) == g) b += Cfg<S, BK>::kBPlane;
+  }
+  return b;
+}
+
 template <int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
   using C = Cfg<S, BK>;
   constexpr int kS = S, kBK = BK, kStages = C::kStages, kStageBytes = C::kStageBytes;
+  static_assert(grp_bytes<S, BK>(0) + grp_bytes<S, BK>(1) + grp_bytes<S, BK>(2) + grp_bytes<S, BK>(3) == kStageBytes,
+                "plane groups cover the stage");
   constexpr int kAPlane = C::kAPlane, kBPlane = C::kBPlane;
   const int na = a.act ? *a.nact : a.batch;
   if (na == 0) return;
@@ -333,15 +353,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int64_t total = (int64_t)na * per_mat * a.jobs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);  // [stage][group]
+  uint64_t* empty = full + kStages * kGroups;
   uint64_t* tmem_full = empty + kStages;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(full + s, 1);
+      for (int g = 0; g < kGroups; ++g) tc::mbar_init(full + s * kGroups + g, 1);
       tc::mbar_init(empty + s, 1);
     }
     tc::mbar_init(tmem_full, 1);
@@ -369,11 +389,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         for (int kc = 0; kc < k_chunks; ++kc) {
           tc::mbar_wait(empty + stage, phase ^ 1);
           uint8_t* st = smem + stage * kStageBytes;
-          tc::mbar_arrive_expect_tx(full + stage, kStageBytes);
 #pragma unroll
-          for (int s = 0; s < kS; ++s) {
-            tc::tma_load_3d(st + s * kAPlane, am, full + stage, kc * kBK, ti * kBM, mat * kS + s);
-            tc::tma_load_3d(st + kS * kAPlane + s * kBPlane, bm, full + stage, kc * kBK, tj * kBN, mat * kS + s);
+          for (int g = 0; g < kGroups; ++g) {
+            uint64_t* fb = full + stage * kGroups + g;
+            tc::mbar_arrive_expect_tx(fb, grp_bytes<S, BK>(g));
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+              if (grp_a(s) == g) tc::tma_load_3d(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kS + s);
+              if (grp_b(s) == g)
+                tc::tma_load_3d(st + kS * kAPlane + s * kBPlane, bm, fb, kc * kBK, tj * kBN, mat * kS + s);
+            }
           }
           if (++stage == kStages) {
             stage = 0;
@@ -391,35 +416,38 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       tc::mbar_wait(tmem_empty, acc_phase ^ 1);
       tc::tc_fence_after();
       for (int kc = 0; kc < k_chunks; ++kc) {
-        tc::mbar_wait(full + stage, phase);
-        tc::tc_fence_after();
-        if (tc::elect_one()) {
-          const uint32_t s0 = tc::smem_u32(smem + stage * kStageBytes);
-          // plane and k-step offsets are added to the 14-bit (addr >> 4) field
-          const uint64_t dA0 = desc_sw<kBK>(s0), dB0 = desc_sw<kBK>(s0 + kS * kAPlane);
+        const uint32_t s0 = tc::smem_u32(smem + stage * kStageBytes);
+        // plane and k-step offsets are added to the 14-bit (addr >> 4) field
+        const uint64_t dA0 = desc_sw<kBK>(s0), dB0 = desc_sw<kBK>(s0 + kS * kAPlane);
+        int ready = -1;  // plane groups of this stage known to have landed (compile-time after unrolling)
 #pragma unroll
-          for (int k = 0; k < kBK / 32; ++k) {
-            const uint64_t adv = (uint64_t)((k * 32) >> 4);  // 32 bytes per K=32 step
-            // A plane sa against up to 4 consecutive B planes at once: the B planes
-            // are consecutive 64-row blocks of one K-major tile, and pairs (sa, tb..tb+3)
-            // land in the consecutive accumulators d = sa + tb .. sa + tb + 3 (64
-            // TMEM columns each) -- one MMA of N = 64 * count reads A once for all
-            // of them (10 MMAs per k-step instead of 28: a third of the A traffic)
+        for (int k = 0; k < kBK / 32; ++k) {
+          const uint64_t adv = (uint64_t)((k * 32) >> 4);  // 32 bytes per K=32 step
+          // A plane sa against up to 4 consecutive B planes at once: the B planes
+          // are consecutive 64-row blocks of one K-major tile, and pairs (sa, tb..tb+3)
+          // land in the consecutive accumulators d = sa + tb .. sa + tb + 3 (64
+          // TMEM columns each) -- one MMA of N = 64 * count reads A once for all
+          // of them (10 MMAs per k-step instead of 28: a third of the A traffic)
 #pragma unroll
-            for (int sa = 0; sa < kS; ++sa) {
+          for (int sa = 0; sa < kS; ++sa) {
 #pragma unroll
-              for (int tb = 0; tb < kS - sa; tb += 4) {
-                const int cnt = (kS - sa - tb) < 4 ? (kS - sa - tb) : 4;
-                const uint64_t da = dA0 + (uint64_t)((sa * kAPlane) >> 4) + adv;
-                const uint64_t db = dB0 + (uint64_t)((tb * kBPlane) >> 4) + adv;
-                // sa == 0 initialises every diagonal at the first k-step (it spans d = 0..6)
-                const uint32_t acc = (kc == 0 && k == 0 && sa == 0) ? 0u : 1u;
-                umma_i8(tmem_base + (uint32_t)((sa + tb) * kBN), da, db, idesc_i8(kBM, kBN * cnt), acc);
+            for (int tb = 0; tb < kS - sa; tb += 4) {
+              const int need = grp_a(sa) > grp_b(tb) ? grp_a(sa) : grp_b(tb);
+              while (ready < need) {
+                ++ready;
+                tc::mbar_wait(full + stage * kGroups + ready, phase);
+                tc::tc_fence_after();
               }
+              const int cnt = (kS - sa - tb) < 4 ? (kS - sa - tb) : 4;
+              const uint64_t da = dA0 + (uint64_t)((sa * kAPlane) >> 4) + adv;
+              const uint64_t db = dB0 + (uint64_t)((tb * kBPlane) >> 4) + adv;
+              // sa == 0 initialises every diagonal at the first k-step (it spans d = 0..6)
+              const uint32_t acc = (kc == 0 && k == 0 && sa == 0) ? 0u : 1u;
+              if (lane == 0) umma_i8(tmem_base + (uint32_t)((sa + tb) * kBN), da, db, idesc_i8(kBM, kBN * cnt), acc);
             }
           }
-          tc::umma_commit(empty + stage);
         }
+        if (lane == 0) tc::umma_commit(empty + stage);
         __syncwarp();
         if (++stage == kStages) {
           stage = 0;
@@ -552,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 }
 
 template <int S, int BK>
-inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S, BK>::kStages * Cfg<S, BK>::kStageBytes + 256; }
+inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S, BK>::kStages * Cfg<S, BK>::kStageBytes + 512; }
 
 // 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * S),
 // row pitch np bytes, plane pitch np*np bytes, box (64 B, box_rows, 1), SWIZZLE_64B

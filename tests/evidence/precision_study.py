@@ -13,7 +13,7 @@ same coupled Newton iteration as the oracle on fp32 Wishart statistics
               lo = trunc(x - hi), fp32 accumulation
   hybN      : first N iterations fp64, then 3xtf32 (hybNt: then 3xtf32t)
 
-    python tools/precision_study.py [--n 256] [--seeds 2] > profiles/r01_precision_study.txt
+    python tests/evidence/precision_study.py [--n 256] [--seeds 2] > profiles/r01_precision_study.txt
 """
 
 import argparse
@@ -22,7 +22,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import synth  # noqa: E402
 from oracle import root as oroot  # noqa: E402
