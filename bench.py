@@ -3,7 +3,8 @@
 Roots run in the "auto" precision by default: the Ozaki root (every Newton
 product on the INT8 tensor cores with exact int32 accumulation of 7-slice
 splits, fp64-level accuracy) for blocks of n >= 512 (all of
-this workload), FP64 DMMA below; --root-precision fp64 / ozaki / hybrid force one.
+this workload), FP64 DMMA below; --root-precision fp64 / ozaki / ozaki6 / hybrid force one
+(auto6: 6 slices for n >= 512).
 
 Workload (BASELINE.json configs[2], the configuration the metric is quoted on):
 Transformer-Big (99 matrix parameters, 375.1M of P:494's 375.4M), block size
@@ -88,7 +89,8 @@ def parse():
     ap.add_argument("--max-precond-dim", type=int, default=MAX_PRECOND)
     ap.add_argument("--root-precision", default="auto", choices=sorted(ROOT_MODE),
                     help="auto: ozaki for n >= 512, fp64 below; fp64: FP64 DMMA; ozaki: INT8 tensor cores "
-                         "with fp64-level accuracy (§6.3c); "
+                         "with fp64-level accuracy (7 slices, §6.3c); ozaki6 / auto6: 6 slices (21 slice "
+                         "products, roots ~3e-5 from the fp64 oracle, reading #27); "
                          "hybrid: FP64 DMMA then a 3xTF32 tcgen05 tail (§6.3b)")
     ap.add_argument("--hybrid", action="store_true", help="alias of --root-precision hybrid")
     return ap.parse_args()

@@ -62,6 +62,16 @@ def test_ozaki_1024(shp, mode, bar):
         assert inf[i]["status"] == 0 and abs(int(inf[i]["iters"]) - io.iters) <= 1
 
 
+def test_ozaki_2048(shp):
+    """n > 1024: the two-pass slicing path and 32 k-chunks per tile (config 5's b = 2048 blocks)."""
+    As = synth.psd_batch(2048, 1, synth.BASE_SEED + 5, "wishart")
+    Xg, inf, outs = _both(shp, As, 4)
+    Xo, io = outs[0]
+    print(f"ozaki n=2048: root rel err {rel(Xg[0], Xo):.3e}, iters {inf[0]['iters']} vs {io.iters}")
+    assert rel(Xg[0], Xo) < 1e-6
+    assert inf[0]["status"] == 0 and abs(int(inf[0]["iters"]) - io.iters) <= 1
+
+
 @pytest.mark.parametrize("mode,bar", MODES)
 @pytest.mark.parametrize("p", [1, 2, 3, 6, 8])
 def test_ozaki_root_orders(shp, p, mode, bar):
