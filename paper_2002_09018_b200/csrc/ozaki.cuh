@@ -240,6 +240,36 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
 }
 
 // --------------------------------------------------------------- GEMM
+// W = V + C for an exact fp64 value c and a row scale 2^e_out, integer arithmetic
+// only (the epilogue runs while the tensor pipe is busy): V = rint(c 2^(6 + 7(S-1)
+// - e_out)) from the mantissa by a rounded shift (RN ties-to-even, as rint), so
+// the base-128 digits of W are those slice8 produces for the same scale.
+// ovf: |c| >= 2^e_out (the a-priori bound failed).
+template <int S>
+__device__ __forceinline__ unsigned long long int_w(double c, int e_out, bool& ovf) {
+  constexpr long long kC = (64LL * ((1LL << (7 * S)) - 1)) / 127;
+  const unsigned long long b = (unsigned long long)__double_as_longlong(c);
+  const int ex = (int)((b >> 52) & 0x7FF);
+  ovf |= (ex != 0) && (ex - 1023 >= e_out);
+  const int sh = 1075 - (6 + 7 * (S - 1)) + e_out - ex;  // >= 5 when |c| < 2^e_out
+  const int shc = min(max(sh, 1), 63);
+  const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+  unsigned long long q = m >> shc;
+  const unsigned long long rem = m & ((1ull << shc) - 1ull), half = 1ull << (shc - 1);
+  q += (rem > half || (rem == half && (q & 1ull))) ? 1ull : 0ull;
+  q = (ex == 0 || sh >= 64 || sh < 1) ? 0ull : q;  // zero / subnormal / below the grid; overflow (flagged)
+  const long long V = (b >> 63) ? -(long long)q : (long long)q;
+  return (unsigned long long)(V + kC);
+}
+
+// byte of plane s (digit u_s - 64) from W; plane 0 takes 8 bits (top digit in [-64, 64])
+template <int S>
+__device__ __forceinline__ uint32_t w_byte(unsigned long long W, int s) {
+  const int pos = 7 * (S - 1 - s);
+  const uint32_t mask = s == 0 ? 0xFFu : 0x7Fu;
+  return ((((uint32_t)(W >> pos)) & mask) + 192u) & 0xFFu;
+}
+
 // Integer-pipe helpers for the epilogue (no fp64 instruction while the tensor
 // pipe runs; see the phase-2 note in gemm_kernel).
 // e such that x = 2^e for the power-of-two row scales (exponent field - 1023)
@@ -278,6 +308,12 @@ struct OzJob {
   const double* b_scale;
   double* out;              // fp64 output of matrix 0; matrix m at out + m * out_stride
   int64_t out_stride;
+  // sliced output (out == nullptr, symmetric products only): the product's S int8 planes at
+  // planes[(mat S + s) np^2], every row scaled by the a-priori bound 2^out_e (|C_ij| < 2^out_e),
+  // 2^out_e written to out_scale[mat np + row]
+  int8_t* planes;
+  double* out_scale;
+  int out_e;
 };
 
 struct OzArgs {
@@ -518,7 +554,78 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // outputs must not push the operand planes other tiles still read out of L2); M-update: max|M - I| on the
       // bit patterns (T_{k+1} is sliced from M_{k+1} by slice_kernel<S, true>)
       unsigned long long emax_bits = 0ull, diag_bits = 0ull;
-      if (row_ok) {
+      if (J.planes) {
+        // sliced output (symmetric products T^m): W of every element by integer arithmetic, then per plane
+        // the row-major 64-byte segment (four 16-byte stores: whole sectors) and the mirror -- for tiles
+        // strictly above the diagonal a warp-level 4 x 32 byte transpose (shuffles) turns it into 4-byte
+        // stores of whole sectors; diagonal-band and ragged tiles store bytes
+        const int j0 = tj * kBN;
+        const int64_t pitch = (int64_t)a.np * a.np;
+        int8_t* pl = J.planes + (int64_t)mat * kS * pitch;
+        // A = B (squarings): C is computed bit-symmetrically (the same exact integer pair sums, the same
+        // scales), so the lower-triangle values a tile computes equal their mirrors and every in-range
+        // tile may store whole rows and the whole transpose; otherwise only tiles above the diagonal
+        const bool same_ab = (J.a_map >> 1) == (J.b_map >> 1);
+        const bool interior = (same_ab || j0 >= ti * kBM + kBM) && (j0 + kBN <= a.n) && (ti * kBM + kBM <= a.n);
+        bool ovf = false;
+        const int i0w = ti * kBM + quad * 32;  // this warp's first row
+        const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
+        const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
+        if (row_ok && tj == 2 * ti)
+          J.out_scale[(int64_t)mat * a.np + i] = __longlong_as_double((long long)(J.out_e + 1023) << 52);
+        // two halves of 32 columns (bounds the live registers: 32 W values)
+#pragma unroll
+        for (int h = 0; h < kBN; h += 32) {
+          unsigned long long w[32];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            if (row_ok) {
+              const double2 b2 = *reinterpret_cast<const double2*>(bs + h + e);
+              w[e] = int_w<kS>(scale2(v[h + e], ka + exp2_of(b2.x)), J.out_e, ovf);
+              w[e + 1] = int_w<kS>(scale2(v[h + e + 1], ka + exp2_of(b2.y)), J.out_e, ovf);
+            } else {
+              w[e] = w[e + 1] = 0ull;
+            }
+          }
+#pragma unroll 1
+          for (int s2 = 0; s2 < kS; ++s2) {
+            int8_t* ps = pl + s2 * pitch;
+            uint32_t wd[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              wd[k] = w_byte<kS>(w[4 * k], s2) | (w_byte<kS>(w[4 * k + 1], s2) << 8) |
+                      (w_byte<kS>(w[4 * k + 2], s2) << 16) | (w_byte<kS>(w[4 * k + 3], s2) << 24);
+            if (interior) {
+              uint4* dst = reinterpret_cast<uint4*>(ps + (int64_t)i * a.np + j0 + h);
+              dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+              dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+              // mirror rows j0 + h + 4k + (lane >> 3), columns i0w + 4 (lane & 7) .. + 3
+              const int src = 4 * (lane & 7), sel = 8 * (lane >> 3);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t x0 = __shfl_sync(0xffffffffu, wd[k], src);
+                const uint32_t x1 = __shfl_sync(0xffffffffu, wd[k], src + 1);
+                const uint32_t x2 = __shfl_sync(0xffffffffu, wd[k], src + 2);
+                const uint32_t x3 = __shfl_sync(0xffffffffu, wd[k], src + 3);
+                const uint32_t o = ((x0 >> sel) & 0xFFu) | (((x1 >> sel) & 0xFFu) << 8) |
+                                   (((x2 >> sel) & 0xFFu) << 16) | (((x3 >> sel) & 0xFFu) << 24);
+                *reinterpret_cast<uint32_t*>(ps + (int64_t)(j0 + h + 4 * k + (lane >> 3)) * a.np + i0w + src) = o;
+              }
+            } else if (row_ok) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const int j = j0 + h + e;
+                const int8_t byte = (int8_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+                if (j < a.n && j >= i) ps[(int64_t)i * a.np + j] = byte;
+                if (j < a.n && j > i) ps[(int64_t)j * a.np + i] = byte;
+              }
+            }
+          }
+        }
+        if (ovf)  // the a-priori bound failed: poison this matrix's next err check (status 2, never silent)
+          atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + a.kcheck),
+                    0x7FF8000000000000ull);
+      } else if (row_ok) {
         const int j0 = tj * kBN;
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
         double* orow = out + (int64_t)i * a.np + j0;

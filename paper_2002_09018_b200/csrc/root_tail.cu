@@ -24,6 +24,8 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ozaki.cuh"
+
+#include <cmath>
 #include "tc_common.cuh"
 #include "tc_gemm.h"
 
@@ -605,6 +607,24 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
     j.b_scale = slot_scale(sb);
     j.out = region(out_reg);
     j.out_stride = mstride;
+    j.planes = nullptr;
+    j.out_scale = nullptr;
+    j.out_e = 0;
+    return j;
+  };
+  // T^m (m >= 2) sliced by the product's own epilogue: every row scaled by 2^e with
+  // 2^e > ((p+1)/p)^m >= rho(T)^m >= |(T^m)_ij| (reading #28; a violated bound is
+  // flagged as a non-finite err, status 2).  S = 7 only (S = 6 keeps 3 pipeline stages).
+  const bool fuse_pow = (kS == 7);
+  auto sliced_job = [&](int sa, int sb, int slot, int m) {
+    oz::OzJob j = job(sa, sb, 0);
+    j.out = nullptr;
+    j.planes = slot_planes_ptr(slot);
+    j.out_scale = slot_scale(slot);
+    const double bound = std::pow((double)(p + 1) / (double)p, m) * (1.0 + 1e-9);
+    int e = 0;
+    while (std::ldexp(1.0, e) <= bound) ++e;
+    j.out_e = e;
     return j;
   };
   const int grid = num_sms();
@@ -622,34 +642,51 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
     slice(RX0 + xs, OZ_SX);
     slice(RM0 + xs, OZ_SM);
     slice_any(RM0 + xs, OZ_ST, true);  // T_k from M_k
-    // P1: X_{k+1} = X_k T ; S0 = T T (p >= 2)
+    // P1: X_{k+1} = X_k T (fp64) ; S0 = T T (p >= 2; sliced in the epilogue when fuse_pow)
     oz::OzArgs a1 = base;
-    a1.jobs = p >= 2 ? 2 : 1;
+    a1.kcheck = k + 1;
     a1.job[0] = job(OZ_SX, OZ_ST, RX0 + (xs ^ 1));
-    a1.job[1] = job(OZ_ST, OZ_ST, RS0);
-    gemm(a1);
-    int rb = RS0, sb = OZ_SS0;
-    if (p >= 2) slice(RS0, OZ_SS0);
-    for (int bit = lead - 1; bit >= 0; --bit) {
-      if (bit != lead - 1) {
-        const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
-        oz::OzArgs q = base;
-        q.jobs = 1;
-        q.job[0] = job(sb, sb, rd);
-        gemm(q);
-        slice(rd, sd);
-        rb = rd;
-        sb = sd;
+    if (fuse_pow) {
+      // two launches: a stage whose jobs take different epilogue paths was measured 17-18 ms against
+      // 6 + 6 ms for the two alone (the alternating paths thrash the instruction cache)
+      a1.jobs = 1;
+      gemm(a1);
+      if (p >= 2) {
+        oz::OzArgs a2 = a1;
+        a2.job[0] = sliced_job(OZ_ST, OZ_ST, OZ_SS0, 2);
+        gemm(a2);
       }
-      if ((p >> bit) & 1) {
+    } else {
+      a1.jobs = p >= 2 ? 2 : 1;
+      a1.job[1] = job(OZ_ST, OZ_ST, RS0);
+      gemm(a1);
+    }
+    int rb = RS0, sb = OZ_SS0, m = 2;
+    if (p >= 2 && !fuse_pow) slice(RS0, OZ_SS0);
+    for (int bit = lead - 1; bit >= 0; --bit) {
+      if (bit != lead - 1) {  // square
         const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
         oz::OzArgs q = base;
         q.jobs = 1;
-        q.job[0] = job(sb, OZ_ST, rd);
+        q.kcheck = k + 1;
+        q.job[0] = fuse_pow ? sliced_job(sb, sb, sd, 2 * m) : job(sb, sb, rd);
+        gemm(q);
+        if (!fuse_pow) slice(rd, sd);
+        rb = rd;
+        sb = sd;
+        m *= 2;
+      }
+      if ((p >> bit) & 1) {  // times T
+        const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
+        oz::OzArgs q = base;
+        q.jobs = 1;
+        q.kcheck = k + 1;
+        q.job[0] = job(sb, OZ_ST, rd);  // A != B: fp64 output and the slice kernel
         gemm(q);
         slice(rd, sd);
         rb = rd;
         sb = sd;
+        m += 1;
       }
     }
     // P3: M_{k+1} = T^p M_k ; err_{k+1} = max|M_{k+1} - I|
