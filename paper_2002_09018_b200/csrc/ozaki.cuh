@@ -114,7 +114,7 @@ __device__ __forceinline__ void slice8(const double (&r)[8], double scl, uint32_
 }
 
 // 2^(6 + 7(S-1) - e): the digit scale of a row with max < 2^e, e in [-960, 1024]
-// (row_exponent), built in the exponent field directly
+// (row_exponent_bits), built in the exponent field directly
 template <int S>
 __device__ __forceinline__ double digit_scale(int e) {
   return __longlong_as_double((long long)(6 + 7 * (S - 1) - e + 1023) << 52);
@@ -145,16 +145,23 @@ __device__ __forceinline__ void store8(int8_t* plane_row, int j, int n, const ui
   }
 }
 
-// Row exponent: e with max|row| < 2^e (0 for a zero row)
-__device__ __forceinline__ int row_exponent(double mx) {
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
-  return max(e, -960);          // keeps digit_scale<S>(e) a normal double (rows below 2^-960: fewer digits)
+// |x| as an unsigned bit pattern (PTX, so it stays on the integer pipe): ordered like |x|
+// for non-NaN x, NaN above +inf.  The slicer's row maxima are taken on these patterns --
+// fmax(|x|) is an fp64 compare/select that kept the FP64 pipe busy in the T slicing
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  unsigned long long r;
+  asm("and.b64 %0, %1, 0x7FFFFFFFFFFFFFFF;" : "=l"(r) : "l"(__double_as_longlong(x)));
+  return r;
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+
+// e with max|row| < 2^e (frexp's exponent), from the largest |x| bit pattern of the
+// row (warp max); 0 for a zero row; clamped at -960 so that digit_scale stays a normal double
+__device__ __forceinline__ int row_exponent_bits(unsigned long long mb) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mb = umax64(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+  if (mb == 0ull) return 0;
+  return max((int)(mb >> 52) - 1022, -960);
 }
 
 // T_ij = ((p + 1) delta_ij - M_ij) / p, the same expression as the fp64 root's
@@ -181,15 +188,18 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = act ? *nact : batch;
   const int64_t plane_pitch = (int64_t)np * np;
-  const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p;
+  const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p, ninv_p = -inv_p;
   for (int64_t rid = gw; rid < (int64_t)na * n; rid += nw) {
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
     int8_t* prow = planes + ((int64_t)mat * S * np + i) * np;
+    // TM: off the diagonal T_ij = -M_ij / p (one multiply: the same value as (0 - m) / p up to the sign
+    // of zero); the diagonal element once per row
+    const double tii = TM ? t_of(row[i], true, pp1, inv_p) : 0.0;
     if (n <= 256 * kRegChunks) {
       double r[kRegChunks][8];
-      double mx = 0.0;
+      unsigned long long mb = 0ull;
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
         const int j = 256 * c + 8 * lane;
@@ -201,12 +211,12 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
         }
         if (TM) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) r[c][q] = (j + q < n) ? t_of(r[c][q], j + q == i, pp1, inv_p) : 0.0;
+          for (int q = 0; q < 8; ++q) r[c][q] = (j + q == i) ? tii : r[c][q] * ninv_p;  // beyond n: -0, never stored
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mx = fmax(mx, fabs(r[c][q]));
+        for (int q = 0; q < 8; ++q) mb = umax64(mb, abs_bits(r[c][q]));
       }
-      const int e = row_exponent(mx);
+      const int e = row_exponent_bits(mb);
       if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
@@ -219,16 +229,16 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
         }
       }
     } else {
-      double mx = 0.0;
-      for (int j = lane; j < n; j += 32) mx = fmax(mx, fabs(TM ? t_of(row[j], j == i, pp1, inv_p) : row[j]));
-      const int e = row_exponent(mx);
+      unsigned long long mb = 0ull;
+      for (int j = lane; j < n; j += 32) mb = umax64(mb, abs_bits(TM ? ((j == i) ? tii : row[j] * ninv_p) : row[j]));
+      const int e = row_exponent_bits(mb);
       if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
       for (int j = 8 * lane; j < n; j += 256) {
         double r[8];
         load8(row, j, n, r);
         if (TM) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) r[q] = (j + q < n) ? t_of(r[q], j + q == i, pp1, inv_p) : 0.0;
+          for (int q = 0; q < 8; ++q) r[q] = (j + q == i) ? tii : r[q] * ninv_p;
         }
         uint32_t dig[S][2];
         slice8<S>(r, digit_scale<S>(e), dig);
@@ -293,14 +303,6 @@ __device__ __forceinline__ double scale2(double x, int k) {
   if (ex != 0 && ex != 0x7FF && ne >= 1 && ne <= 2046) return __longlong_as_double(b + ((long long)k << 52));
   return scale2_slow(x, k);
 }
-// |x| as an unsigned bit pattern: ordered like |x| for non-NaN, NaN above +inf.
-// In PTX so the front end cannot turn it back into an fp64 fabs (DADD |x|).
-__device__ __forceinline__ unsigned long long abs_bits(double x) {
-  unsigned long long r;
-  asm("and.b64 %0, %1, 0x7FFFFFFFFFFFFFFF;" : "=l"(r) : "l"(__double_as_longlong(x)));
-  return r;
-}
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
 
 struct OzJob {
   int a_map, b_map;         // TMA maps of the A-use (128-row box) / B-use (64-row box) planes
