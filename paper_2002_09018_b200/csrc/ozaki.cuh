@@ -114,7 +114,7 @@ __device__ __forceinline__ void slice8(const double (&r)[8], double scl, uint32_
 }
 
 // 2^(6 + 7(S-1) - e): the digit scale of a row with max < 2^e, e in [-960, 1024]
-// (row_exponent_bits), built in the exponent field directly
+// (row_exponent), built in the exponent field directly
 template <int S>
 __device__ __forceinline__ double digit_scale(int e) {
   return __longlong_as_double((long long)(6 + 7 * (S - 1) - e + 1023) << 52);
@@ -145,24 +145,26 @@ __device__ __forceinline__ void store8(int8_t* plane_row, int j, int n, const ui
   }
 }
 
+// Row exponent: e with max|row| < 2^e (0 for a zero row)
+__device__ __forceinline__ int row_exponent(double mx) {
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+  return max(e, -960);          // keeps digit_scale<S>(e) a normal double (rows below 2^-960: fewer digits)
+}
+
 // |x| as an unsigned bit pattern (PTX, so it stays on the integer pipe): ordered like |x|
-// for non-NaN x, NaN above +inf.  The slicer's row maxima are taken on these patterns --
-// fmax(|x|) is an fp64 compare/select that kept the FP64 pipe busy in the T slicing
+// for non-NaN x, NaN above +inf (the GEMM epilogue's max|M - I|, which must stay off the FP64 pipe)
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
   unsigned long long r;
   asm("and.b64 %0, %1, 0x7FFFFFFFFFFFFFFF;" : "=l"(r) : "l"(__double_as_longlong(x)));
   return r;
 }
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
-
-// e with max|row| < 2^e (frexp's exponent), from the largest |x| bit pattern of the
-// row (warp max); 0 for a zero row; clamped at -960 so that digit_scale stays a normal double
-__device__ __forceinline__ int row_exponent_bits(unsigned long long mb) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mb = umax64(mb, __shfl_xor_sync(0xffffffffu, mb, o));
-  if (mb == 0ull) return 0;
-  return max((int)(mb >> 52) - 1022, -960);
-}
 
 // T_ij = ((p + 1) delta_ij - M_ij) / p, the same expression as the fp64 root's
 // setup (root.cu) -- the coupled-Newton T_k is a function of M_k alone
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
     const double tii = TM ? t_of(row[i], true, pp1, inv_p) : 0.0;
     if (n <= 256 * kRegChunks) {
       double r[kRegChunks][8];
-      unsigned long long mb = 0ull;
+      double mx = 0.0;
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
         const int j = 256 * c + 8 * lane;
@@ -214,9 +216,9 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
           for (int q = 0; q < 8; ++q) r[c][q] = (j + q == i) ? tii : r[c][q] * ninv_p;  // beyond n: -0, never stored
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mb = umax64(mb, abs_bits(r[c][q]));
+        for (int q = 0; q < 8; ++q) mx = fmax(mx, fabs(r[c][q]));
       }
-      const int e = row_exponent_bits(mb);
+      const int e = row_exponent(mx);
       if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
@@ -229,9 +231,9 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
         }
       }
     } else {
-      unsigned long long mb = 0ull;
-      for (int j = lane; j < n; j += 32) mb = umax64(mb, abs_bits(TM ? ((j == i) ? tii : row[j] * ninv_p) : row[j]));
-      const int e = row_exponent_bits(mb);
+      double mx = 0.0;
+      for (int j = lane; j < n; j += 32) mx = fmax(mx, fabs(TM ? ((j == i) ? tii : row[j] * ninv_p) : row[j]));
+      const int e = row_exponent(mx);
       if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
       for (int j = 8 * lane; j < n; j += 256) {
         double r[8];
