@@ -614,8 +614,8 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   };
   // T^m (m >= 2) sliced by the product's own epilogue: every row scaled by 2^e with
   // 2^e > ((p+1)/p)^m >= rho(T)^m >= |(T^m)_ij| (reading #28; a violated bound is
-  // flagged as a non-finite err, status 2).  S = 7 only (S = 6 keeps 3 pipeline stages).
-  const bool fuse_pow = (kS == 7);
+  // flagged as a non-finite err, status 2).  The sliced epilogue needs no shared memory, so both S.
+  const bool fuse_pow = true;
   auto sliced_job = [&](int sa, int sb, int slot, int m) {
     oz::OzJob j = job(sa, sb, 0);
     j.out = nullptr;
