@@ -586,6 +586,18 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
     ++*launches;
   };
   auto slice = [&](int reg, int slot) { slice_any(reg, slot, false); };
+  // M_k and T_k in one pass over M_k (rows up to 1024 in registers), else two passes
+  auto slice_mt = [&](int reg) {
+    if (n <= 1024) {
+      oz::slice_mt_kernel<S><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
+                                                             slot_planes_ptr(OZ_SM), slot_scale(OZ_SM),
+                                                             slot_planes_ptr(OZ_ST), slot_scale(OZ_ST), p);
+      ++*launches;
+    } else {
+      slice_any(reg, OZ_SM, false);
+      slice_any(reg, OZ_ST, true);
+    }
+  };
   oz::OzArgs base;
   std::memset(&base, 0, sizeof base);
   base.act = act;
@@ -640,8 +652,7 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   for (int k = 0; k < max_iter; ++k) {
     const int xs = k & 1;
     slice(RX0 + xs, OZ_SX);
-    slice(RM0 + xs, OZ_SM);
-    slice_any(RM0 + xs, OZ_ST, true);  // T_k from M_k
+    slice_mt(RM0 + xs);  // M_k and T_k = ((p+1)I - M_k)/p
     // P1: X_{k+1} = X_k T (fp64) ; S0 = T T (p >= 2; sliced in the epilogue when fuse_pow)
     oz::OzArgs a1 = base;
     a1.kcheck = k + 1;
