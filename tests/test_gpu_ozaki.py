@@ -129,3 +129,26 @@ def test_ozaki_determinism_and_batch_independence(shp, mode):
     assert torch.equal(X2, X3)
     assert torch.equal(X1, X2[:3])
 
+
+
+@pytest.mark.parametrize("mode", ["ozaki", "ozaki6"])
+def test_ozaki_power_bound_violation_is_flagged(shp, mode):
+    """Reading #28: the squarings' a-priori row scale assumes eig(M_0) <= 2(p+1), i.e. a power-iteration
+    lambda_hat within (p+1)x of lambda_max.  One power step on a matrix with one dominant eigenvalue gives
+    lambda_hat ~ lambda_max / n, so T_0 has eigenvalues far below -1 and T^2 exceeds the bound: the root must
+    report status 2 and leave X untouched (never a silently wrong root); a well-estimated batch mate is
+    unaffected."""
+    n = 256
+    As = np.zeros((2, n, n), np.float32)
+    As[0] = np.eye(n, dtype=np.float32)
+    As[0][7, 7] = 1e6
+    As[1] = synth.wishart(n, 11)
+    A = torch.from_numpy(As).to(DEV)
+    X = torch.full_like(A, 7.0)
+    X, info = shp.inverse_pth_root_batched(A, 4, X=X, fp64_iters=mode, power_iters=1)
+    torch.cuda.synchronize()
+    inf = shp.info_to_numpy(info)
+    assert inf[0]["lambda_max"] < 1e6 / 20  # the premise: lambda_max / lambda_hat > 2(p + 1)
+    assert inf[0]["status"] == 2 and np.all(X[0].cpu().numpy() == 7.0)
+    Xo, io = oroot.inverse_pth_root(As[1].astype(np.float64), 4, power_iters=1)
+    assert inf[1]["status"] == io.status and rel(X[1].cpu().numpy(), Xo) < 1e-4
