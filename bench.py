@@ -93,6 +93,9 @@ def parse():
                          "products, roots ~3e-5 from the fp64 oracle, reading #27); "
                          "hybrid: FP64 DMMA then a 3xTF32 tcgen05 tail (§6.3b)")
     ap.add_argument("--hybrid", action="store_true", help="alias of --root-precision hybrid")
+    ap.add_argument("--gather", default="allgather", choices=["overlapped", "allgather"],
+                    help="N > 1: one all_gather_into_tensor after all roots (default), or per-group owner broadcasts "
+                         "overlapping the next group's roots (measured equal at N = 2, 4: DESIGN §8)")
     return ap.parse_args()
 
 
@@ -257,12 +260,20 @@ def main():
         launches[0] += shp.last_launch_count()
         if ev:
             ev[1].record(stream)
-        infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol,
-                                        fp64_iters=ROOT_MODE[args.root_precision])
-        launches[0] += shp.last_refresh_launch_count()
-        if ev:
-            ev[2].record(stream)
-        sdist.all_gather_roots(plan, roots, rank, world)
+        if world > 1 and args.gather == "overlapped":
+            # each group's roots go out (NCCL broadcasts from their owners) while the next group computes
+            infos, nl = sdist.refresh_gather_overlapped(plan, stats, roots, rank, world, tol=args.tol,
+                                                        fp64_iters=ROOT_MODE[args.root_precision])
+            launches[0] += nl
+            if ev:
+                ev[2].record(stream)
+        else:
+            infos = shp.refresh_group_roots(plan, stats, roots, rank, tol=args.tol,
+                                            fp64_iters=ROOT_MODE[args.root_precision])
+            launches[0] += shp.last_refresh_launch_count()
+            if ev:
+                ev[2].record(stream)
+            sdist.all_gather_roots(plan, roots, rank, world)
         shp.tf32_split(roots, roots_lo)  # once per refresh: the roots' TF32 remainder for the tensor cores
         launches[0] += 1
         if ev:
@@ -466,6 +477,9 @@ def main():
                        "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
                        "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
                        "parallelism": f"root-shard{world}",
+                       "root_exchange": (("per-group owner broadcasts overlapping the next group's roots "
+                                          "(phase 'roots' includes them)") if args.gather == "overlapped"
+                                         else "one all_gather_into_tensor") if world > 1 else None,
                        "root_precision": ROOT_LABEL[args.root_precision], "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
             "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather_and_roots_split": ph[2], "precondition": ph[3]},
             "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,

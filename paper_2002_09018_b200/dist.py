@@ -10,7 +10,11 @@ that are part of the training system".  One process per GPU:
     graft numerator are updated everywhere (every rank preconditions all blocks);
   * each rank computes the roots of its segment, then ONE
     ``all_gather_into_tensor`` (NCCL over NVLink/NVSwitch) of the equal-size
-    segments rebuilds the full roots buffer on every rank (in place for NCCL).
+    segments rebuilds the full roots buffer on every rank (in place for NCCL);
+  * or (``refresh_gather_overlapped``) per root group: once the owners have
+    computed a group, its region of every segment is broadcast from its owner on
+    NCCL's stream while the next group computes -- the same bytes, but only the
+    last group's transfer stays on the critical path.
 """
 
 from __future__ import annotations
@@ -18,7 +22,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import Plan, refresh_group_roots
+from . import Plan, inverse_pth_root_ptr, last_launch_count, new_info, refresh_group_roots
 
 
 def segment(plan: Plan, buf: torch.Tensor, rank: int) -> torch.Tensor:
@@ -47,3 +51,55 @@ def refresh_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, rank: in
     infos = refresh_group_roots(plan, stats, roots, rank, eps_rel, tol, max_iter, power_iters, stream=stream)
     all_gather_roots(plan, roots, rank, world_size, group)
     return infos
+
+
+def _group_keys(plan: Plan):
+    """(n, p, r) root groups in the plan's order: every rank walks the same sequence."""
+    keys = []
+    for g in plan.groups:
+        k = (int(g["n"]), int(g["p"]), int(g["r"]))
+        if k not in keys:
+            keys.append(k)
+    return keys
+
+
+def _region(g):
+    off, cnt, stride = int(g["offset"]), int(g["count"]), int(g["stride"])
+    return off, cnt * stride
+
+
+def refresh_gather_overlapped(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, rank: int, world_size: int,
+                              group=None, eps_rel: float = 1e-6, tol: float = 1e-7, max_iter: int = 100,
+                              power_iters: int = 100, fp64_iters=None, compute_group=None):
+    """Owner-sharded refresh with the root exchange overlapped (rows a5-a7): for every (n, p, r) group in the
+    plan's order this rank computes its own roots of the group (``compute_group(g)``, default: the batched root
+    call), then the group's region of EVERY rank's segment is broadcast from its owner (async, NCCL's stream
+    waits for the launches enqueued so far) -- so group k's transfer runs under group k+1's roots.  On return
+    the current stream waits for all transfers: the full roots buffer, as after ``all_gather_roots``.
+    Returns ([(group, info)], kernel launches)."""
+    out, launches, works = [], 0, []
+    for key in _group_keys(plan):
+        mine = [g for g in plan.groups_of(rank) if (int(g["n"]), int(g["p"]), int(g["r"])) == key]
+        for g in mine:
+            if compute_group is not None:
+                compute_group(g)
+                continue
+            cnt, n, p, r = int(g["count"]), int(g["n"]), int(g["p"]), int(g["r"])
+            off, stride = int(g["offset"]), int(g["stride"])
+            ld = (n + 3) // 4 * 4
+            info = new_info(cnt, stats.device)
+            inverse_pth_root_ptr(stats.data_ptr() + 4 * off, ld, stride, roots.data_ptr() + 4 * off, ld, stride,
+                                 cnt, n, p, info, eps_rel, tol, max_iter, power_iters, stats.device, None, r,
+                                 fp64_iters if r == 1 else None)
+            launches += last_launch_count()
+            out.append((g, info))
+        if world_size > 1:
+            for src in range(world_size):
+                for g in plan.groups_of(src):
+                    if (int(g["n"]), int(g["p"]), int(g["r"])) != key:
+                        continue
+                    off, length = _region(g)
+                    works.append(dist.broadcast(roots[off:off + length], src=src, group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return out, launches

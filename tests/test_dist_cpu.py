@@ -89,3 +89,47 @@ def test_owner_shards_cover_each_root_once():
             o = int(g["owner"])
             assert o * plan.segment_elems <= int(g["offset"])
             assert int(g["offset"]) + int(g["count"]) * int(g["stride"]) <= (o + 1) * plan.segment_elems
+
+
+def _worker_overlapped(rank, world, port, shapes, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2002_09018_b200 as shp
+        from paper_2002_09018_b200 import dist as sdist
+        plan = shp.make_plan(shapes, 1024, 8192, world)
+
+        def fill(buf, g):  # the owner's "computed" roots of group g: a distinct value per element
+            off, cnt, stride = int(g["offset"]), int(g["count"]), int(g["stride"])
+            buf[off:off + cnt * stride] = torch.arange(cnt * stride, dtype=torch.float32) + 1e6 * (1 + int(g["owner"]))
+
+        ref = torch.full((plan.stats_elems,), float("nan"))
+        for g in plan.groups_of(rank):
+            fill(ref, g)
+        sdist.all_gather_roots(plan, ref, rank, world)
+        roots = torch.full((plan.stats_elems,), float("nan"))
+        sdist.refresh_gather_overlapped(plan, None, roots, rank, world, compute_group=lambda g: fill(roots, g))
+        q.put((rank, ref.numpy().copy(), roots.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_overlapped_group_broadcasts_equal_the_all_gather(world):
+    """refresh_gather_overlapped (per-group broadcasts from the owners, overlapping the next group's roots)
+    rebuilds exactly the buffer all_gather_roots rebuilds, on every rank."""
+    shapes = [s for _, s in transformer_big_shapes()][:12] + [(32000, 1024)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_overlapped, args=(r, world, port, shapes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ref, got in out:
+        assert np.array_equal(np.nan_to_num(ref, nan=-1), np.nan_to_num(got, nan=-1)), rank
+    assert np.array_equal(np.nan_to_num(out[0][2], nan=-1), np.nan_to_num(out[-1][2], nan=-1))
