@@ -362,7 +362,11 @@ SHP_DEV void write_output(const RootArgs& a, int pbuf);
 SHP_DEV void tail_handoff(const RootArgs& a);
 
 // ---------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
+// kOz: the Ozaki root's prologue (power iteration, setup, the k = 0 decision and
+// handoff) without the FP64-DMMA iteration code, so it needs far fewer registers
+// and no GEMM shared memory: more CTAs per SM for the latency-bound power sweeps.
+template <bool kOz>
+__global__ void __launch_bounds__(kRT, kOz ? 4 : 2) root_kernel(RootArgs a) {
   extern __shared__ __align__(16) double smem[];
   cg::grid_group grid = cg::this_grid();
   const int np = a.np, T = np / kNT, tiles = T * (T + 1) / 2;
@@ -420,6 +424,7 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
   grid.sync();
 
   // ---- iterations
+  if constexpr (!kOz) {
   int* act = reinterpret_cast<int*>(smem + kAsyncSmemDoubles);
   int* cnt = act + kMaxBatchPerLaunch;  // 257 ints scratch
   __shared__ int s_nact;
@@ -491,6 +496,7 @@ __global__ void __launch_bounds__(kRT, 2) root_kernel(RootArgs a) {
     // next active list (ordered compaction; identical in every CTA)
     nact = compact(a, act, nact, k + 1, cnt, false);
   }
+  }  // !kOz
 
   // ---- finalize: per-matrix decision, then fp32 output
   for (int mat = blockIdx.x; mat < a.batch; mat += gridDim.x) {
@@ -651,16 +657,28 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
                 int n, int p, int r, int k_sw, int precision, int slices, double eps_rel, double tol, int max_iter,
                 int power_iters, shampoo_root_info_t* info, void* ws, cudaStream_t stream, int64_t* launches) {
   static size_t configured_smem = 0;
-  const size_t smem = root_smem_bytes(n);
-  if (smem > configured_smem) {
-    if (cudaFuncSetAttribute(root_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+  const bool oz = (precision == 2);
+  const size_t smem = oz ? (2 * (size_t)n + 8) * sizeof(double) : root_smem_bytes(n);
+  if (oz) {
+    static size_t configured_oz = 0;
+    if (smem > configured_oz) {
+      if (cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return set_cuda_error("cudaFuncSetAttribute(root_kernel<ozaki>)");
+      configured_oz = smem;
+    }
+  } else if (smem > configured_smem) {
+    if (cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
         cudaFuncSetAttribute(root_power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
       return set_cuda_error("cudaFuncSetAttribute(root_kernel)");
     configured_smem = smem;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, root_kernel, kRT, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oz ? root_kernel<true> : root_kernel<false>, kRT, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
     return set_error(SHAMPOO_ERR_UNSUPPORTED, "root_kernel cannot be resident (smem %zu)", smem);
   const int np = padded(n);
   char* w = static_cast<char*>(ws);
@@ -705,7 +723,8 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     const int grid = num_sms() * per_sm;
     void* tok;
     prof_begin_launch("root_kernel", stream, &tok);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)root_kernel, dim3(grid), dim3(kRT), args, smem, stream);
+    cudaError_t e = cudaLaunchCooperativeKernel(oz ? (const void*)root_kernel<true> : (const void*)root_kernel<false>,
+                                                dim3(grid), dim3(kRT), args, smem, stream);
     prof_end_launch(tok, stream);
     if (e != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(root_kernel)", e);
     ++*launches;
