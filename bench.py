@@ -66,6 +66,13 @@ def _int8_peak():
 # iteration (X T 14.1 GB, T T sliced 8.5 GB, T^2 T^2 sliced 8.6 GB, T^4 M 12.8 GB for 528 matrices), ncu launch
 # list profiles/r01za_launches_root528_summary.txt
 OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = ((9.71 + 4.39) + (4.67 + 3.85) + (4.71 + 3.85) + (8.37 + 4.39)) / 4 * 1e9 / 528
+# the arithmetic of the dominant phase (the roots): fp64 iterates, products per the root precision
+DTYPE = {"auto": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
+         "auto6": "f64 iterates, int8 Ozaki S=6 products (exact int32 accumulation)",
+         "ozaki": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
+         "ozaki6": "f64 iterates, int8 Ozaki S=6 products (exact int32 accumulation)",
+         "fp64": "f64 (FP64 DMMA)", "hybrid": "f64 DMMA, then 3xTF32 (tf32 tcgen05) tail"}
+EMPTY_LAUNCH_MS = 0.05  # an Ozaki GEMM launch with no active matrix returns in a few microseconds
 ROOT_MODE = {"auto": "auto", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki6": "ozaki6", "hybrid": -1}
 ROOT_SLICES = {"auto": 7, "auto6": 6, "ozaki": 7, "ozaki6": 6}
 ROOT_LABEL = {"auto": "auto: ozaki (INT8 tcgen05, 7 slices, exact int32 accumulation) for n >= 512, fp64 DMMA below",
@@ -342,6 +349,10 @@ def main():
         torch.cuda.synchronize()
         gemm_ms, gemm_launches = shp.profile_end("ozaki_gemm")
         rk_ms, _ = shp.profile_end("root_kernel")
+        per_launch = shp.profile_launch_ms("ozaki_gemm")
+        # launches after every matrix of the batch converged return at once (a few us): the per-launch figure
+        # is taken over the launches that did work
+        working = per_launch[per_launch > EMPTY_LAUNCH_MS]
         call_ms = e0.elapsed_time(e1)
         inf = shp.info_to_numpy(info)
         iters_mean = float(inf["iters"].sum()) / cnt
@@ -356,8 +367,10 @@ def main():
                 "traffic_note": "dram read+write bytes per GEMM launch (mean of the 4 product launches of an "
                                 "iteration), ncu launch list of a 528-matrix root call scaled per matrix",
                 "kernel": f"oz::gemm_kernel (INT8 tcgen05 Ozaki products, batch {cnt} x {n}^2, p=4)",
-                "kernel_ms": gemm_ms / max(1, gemm_launches), "kernel_launches": gemm_launches,
-                "ops_per_launch": ops / max(1, gemm_launches),
+                "kernel_ms": float(working.mean()) if working.size else None,
+                "kernel_launches": int(working.size), "kernel_launches_total": gemm_launches,
+                "kernel_ms_empty_launches_total": float(per_launch[per_launch <= EMPTY_LAUNCH_MS].sum()),
+                "ops_per_launch": ops / max(1, int(working.size)),
                 "root_call_ms": call_ms, "gemm_share_of_root_call": gemm_ms / call_ms,
                 "root_kernel_ms_power_iteration_and_setup": rk_ms,
                 "fp64_equivalent_tflops": (float(inf["iters"].sum()) * 4 * n * n * (n + 1)
@@ -399,6 +412,16 @@ def main():
                 "peak_source": "FP64 DMMA.8x8x4 peak measured on this pool's B200 by tools/microbench/fp64_pipes.cu "
                                "(MEASURED_PEAKS.json has no FP64 entry)"}
 
+    # every root of every timed step: status / iteration histograms (a status-2 root leaves X untouched and
+    # status 1 did not reach tol -- the line says how many of the counted roots are which)
+    st_hist, it_hist = {}, {}
+    for infos in all_infos:
+        for _, info in infos:
+            a = shp.info_to_numpy(info)
+            for v in a["status"]:
+                st_hist[int(v)] = st_hist.get(int(v), 0) + 1
+            for v in a["iters"]:
+                it_hist[int(v)] = it_hist.get(int(v), 0) + 1
     n_p4_total = n_p4  # every p=4 root of the plan is computed once per step (owner-sharded)
     value = n_p4_total / (ms_per_step * 1e-3)
 
@@ -471,7 +494,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": DTYPE[args.root_precision], "data": "synthetic",
             "config": {"workload": f"transformer_big_b{B}_full_step", "model": "Transformer-Big (P:494) shapes",
                        "block_size": B, "max_precond_dim": args.max_precond_dim, "blocks": nb,
                        "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
@@ -485,6 +508,9 @@ def main():
             "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,
             "root_phase_roots_per_s": n_p4_total / (ph[1] * 1e-3),
             "newton_iters_mean": iters_mean,
+            "root_status_hist": {str(k): v for k, v in sorted(st_hist.items())},
+            "root_iters_hist": {str(k): v for k, v in sorted(it_hist.items())},
+            "roots_failed": st_hist.get(2, 0) + st_hist.get(3, 0),
             "gpu_launches": launches[0],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
         }

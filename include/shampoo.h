@@ -386,6 +386,12 @@ int shampoo_tensor_precondition(const shampoo_ttensor_t* tensors_host, int32_t n
  * count of `kernel` (NULL: all). */
 int shampoo_profile_begin(void);
 int shampoo_profile_end(const char* kernel, double* ms, int64_t* launches);
+/* After shampoo_profile_end(): the duration (ms, host array `out` of
+ * `capacity` floats) of each recorded launch of `kernel` (NULL: all) in launch
+ * order; *n receives the number of such launches (may exceed capacity: only
+ * the first `capacity` are written).  Lets the caller separate launches that
+ * did work from the early-exit launches of converged batches. */
+int shampoo_profile_launch_ms(const char* kernel, float* out, int64_t capacity, int64_t* n);
 
 /* Number of kernel launches the last compute call on this host thread
  * enqueued (bench accounting, "gpu_launches"). */

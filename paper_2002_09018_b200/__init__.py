@@ -168,12 +168,13 @@ def root_workspace_bytes(batch: int, n: int, p: int, max_iter: int = 100) -> int
 def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: int, stride_x: int, batch: int,
                          n: int, p: int, info: torch.Tensor, eps_rel: float = 1e-6, tol: float = 1e-7,
                          max_iter: int = 100, power_iters: int = 100, device=None, stream=None, r: int = 1,
-                         fp64_iters: int | None = None):
+                         fp64_iters: int | None = None, ws_tag: str = "root"):
     """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry).
     fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch);
     fp64_iters="ozaki" (= "ozaki7"): every product on the INT8 tensor cores, 7 slices, fp64-level accuracy;
     fp64_iters="ozaki6": 6 slices (21 slice products instead of 28; DESIGN.md §6.3c);
-    fp64_iters="auto" / "auto6": "ozaki" / "ozaki6" for n >= OZAKI_MIN_N, FP64 DMMA below."""
+    fp64_iters="auto" / "auto6": "ozaki" / "ozaki6" for n >= OZAKI_MIN_N, FP64 DMMA below.
+    ws_tag: workspace cache key -- calls that may run concurrently on different streams need different tags."""
     L = _lib.lib()
     if fp64_iters in ("auto", "auto6"):  # the INT8 Ozaki loop pays off from n = 512 (per-iteration launches, 128-row tiles)
         fp64_iters = ("ozaki" + fp64_iters[4:]) if (n >= OZAKI_MIN_N and r == 1) else None
@@ -182,13 +183,13 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
         if r != 1:
             raise ValueError("the ozaki root serves r = 1 only")
         wsb = L.shampoo_root_ozaki_workspace_bytes(batch, n, p, max_iter)
-        ws = workspace(wsb, device if device is not None else info.device, "root")
+        ws = workspace(wsb, device if device is not None else info.device, ws_tag)
         check(L.shampoo_inverse_pth_root_batched_ozaki(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
                                                        tol, max_iter, power_iters, slices, info.data_ptr(),
                                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
         return
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
-    ws = workspace(wsb, device if device is not None else info.device, "root")
+    ws = workspace(wsb, device if device is not None else info.device, ws_tag)
     if fp64_iters is not None:
         if r != 1:
             raise ValueError("the hybrid root serves r = 1 only")
@@ -450,3 +451,14 @@ def profile_end(kernel: str | None = None):
     n = np.zeros(1, np.int64)
     check(_lib.lib().shampoo_profile_end(kernel.encode() if kernel else None, ms.ctypes.data, n.ctypes.data))
     return float(ms[0]), int(n[0])
+
+
+def profile_launch_ms(kernel: str | None = None) -> np.ndarray:
+    """After profile_end(): per-launch milliseconds of `kernel`, in launch order."""
+    L = _lib.lib()
+    n = np.zeros(1, np.int64)
+    key = kernel.encode() if kernel else None
+    check(L.shampoo_profile_launch_ms(key, None, 0, n.ctypes.data))
+    out = np.zeros(max(1, int(n[0])), np.float32)
+    check(L.shampoo_profile_launch_ms(key, out.ctypes.data, out.shape[0], n.ctypes.data))
+    return out[:int(n[0])]

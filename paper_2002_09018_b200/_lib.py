@@ -40,6 +40,7 @@ EXPORTED = [
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_inverse_pth_root_batched_hybrid", "shampoo_root_ozaki_workspace_bytes",
     "shampoo_inverse_pth_root_batched_ozaki", "shampoo_profile_begin", "shampoo_profile_end",
+    "shampoo_profile_launch_ms",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition", "shampoo_precondition_split",
     "shampoo_tf32_split",
@@ -126,6 +127,8 @@ def lib():
     L.shampoo_profile_begin.restype = ctypes.c_int
     L.shampoo_profile_end.argtypes = [ctypes.c_char_p, _vp, _vp]
     L.shampoo_profile_end.restype = ctypes.c_int
+    L.shampoo_profile_launch_ms.argtypes = [ctypes.c_char_p, _vp, ctypes.c_int64, _vp]
+    L.shampoo_profile_launch_ms.restype = ctypes.c_int
     if L.shampoo_abi_version() != 3:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L

@@ -1,5 +1,8 @@
 // abi.cpp -- the extern "C" entry points of libshampoo (include/shampoo.h):
 // host-side validation, error reporting and dispatch to the CUDA launchers.
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -52,15 +55,36 @@ void prof_end_launch(void* token, cudaStream_t stream) {
   cudaEventRecord((*g_prof_recs)[reinterpret_cast<size_t>(token) - 1].e1, stream);
 }
 
+// Per-device caches (a process may drive several GPUs, e.g. tests on cuda:1 after cuda:0): the SM count and the
+// dynamic shared-memory opt-in are properties of the current device's context, not of the process.
+static constexpr int kMaxDevices = 64;
+
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::atomic<int> n[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    n[dev].store(v, std::memory_order_relaxed);
   }
-  return n;
+  return v;
+}
+
+cudaError_t ensure_smem(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(dev, func);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done[key] = smem;
+  return e;
 }
 
 int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
@@ -151,6 +175,24 @@ int shampoo_profile_end(const char* kernel, double* ms, int64_t* launches) {
   }
   if (ms) *ms = total;
   if (launches) *launches = count;
+  return SHAMPOO_OK;
+}
+
+int shampoo_profile_launch_ms(const char* kernel, float* out, int64_t capacity, int64_t* n) {
+  int64_t count = 0;
+  if (g_prof_recs) {
+    for (auto& r : *g_prof_recs) {
+      if (kernel && std::strcmp(kernel, r.name) != 0) continue;
+      if (out && count < capacity) {
+        float t = 0.0f;
+        if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&t, r.e0, r.e1) != cudaSuccess)
+          return set_cuda_error("shampoo_profile_launch_ms");
+        out[count] = t;
+      }
+      ++count;
+    }
+  }
+  if (n) *n = count;
   return SHAMPOO_OK;
 }
 

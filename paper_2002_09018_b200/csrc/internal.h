@@ -64,7 +64,9 @@ int tensor_precondition_launch(const shampoo_ttensor_t* T, const shampoo_tblock_
                                const float* roots, const double* graft_num, float* graft_scale, double* den,
                                void* ws, size_t ws_bytes, cudaStream_t stream, int64_t* launches);
 
-int num_sms();
+int num_sms();  // of the current device (cached per device)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (current device, kernel, larger size); thread-safe
+cudaError_t ensure_smem(const void* func, size_t smem);
 // profiling hooks (shampoo_profile_begin/end): bracket a launch with events
 void prof_begin_launch(const char* name, cudaStream_t stream, void** token);
 void prof_end_launch(void* token, cudaStream_t stream);

@@ -488,15 +488,11 @@ int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, con
   // DMMA path for the remaining blocks (left-only, unaligned)
   if (L.any_dmma) {
     const size_t smem = (size_t)kGemmSmemDoubles * sizeof(double);
-    static bool configured = false;
-    if (!configured) {
-      if (cudaFuncSetAttribute(prec_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-              cudaSuccess ||
-          cudaFuncSetAttribute(prec_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-              cudaSuccess)
-        return set_cuda_error("cudaFuncSetAttribute(prec_gemm_kernel)");
-      configured = true;
-    }
+    if (ensure_smem((const void*)prec_gemm_kernel<1>, smem) !=
+            cudaSuccess ||
+        ensure_smem((const void*)prec_gemm_kernel<2>, smem) !=
+            cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(prec_gemm_kernel)");
     prec_prep_kernel<<<1, 1024, 0, stream>>>(blocks, flags, n_blocks, pre1, pre2, yoff);
     prec_gemm_kernel<1><<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, roots, pre1, yoff, Y);
     prec_gemm_kernel<2><<<num_sms(), kThreads, smem, stream>>>(tensors, blocks, n_blocks, roots, pre2, yoff, Y);

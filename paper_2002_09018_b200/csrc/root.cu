@@ -656,24 +656,14 @@ size_t root_smem_bytes(int n) {
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
                 int n, int p, int r, int k_sw, int precision, int slices, double eps_rel, double tol, int max_iter,
                 int power_iters, shampoo_root_info_t* info, void* ws, cudaStream_t stream, int64_t* launches) {
-  static size_t configured_smem = 0;
   const bool oz = (precision == 2);
   const size_t smem = oz ? (2 * (size_t)n + 8) * sizeof(double) : root_smem_bytes(n);
   if (oz) {
-    static size_t configured_oz = 0;
-    if (smem > configured_oz) {
-      if (cudaFuncSetAttribute(root_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
-        return set_cuda_error("cudaFuncSetAttribute(root_kernel<ozaki>)");
-      configured_oz = smem;
-    }
-  } else if (smem > configured_smem) {
-    if (cudaFuncSetAttribute(root_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(root_power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(root_kernel)");
-    configured_smem = smem;
+    if (ensure_smem((const void*)root_kernel<true>, smem) != cudaSuccess)
+      return set_cuda_error("cudaFuncSetAttribute(root_kernel<ozaki>)");
+  } else if (ensure_smem((const void*)root_kernel<false>, smem) != cudaSuccess ||
+             ensure_smem((const void*)root_power_kernel, smem) != cudaSuccess) {
+    return set_cuda_error("cudaFuncSetAttribute(root_kernel)");
   }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oz ? root_kernel<true> : root_kernel<false>, kRT, smem) !=
@@ -875,12 +865,8 @@ int residual_launch(const float* A, int64_t lda, int64_t stride_a, const float* 
                     int batch, int n, int p, double eps_rel, const shampoo_root_info_t* info, double* residual,
                     void* ws, cudaStream_t stream, int64_t* launches) {
   const size_t smem = (size_t)kAsyncSmemDoubles * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(residual_kernel)");
-    configured = true;
-  }
+  if (ensure_smem((const void*)residual_kernel, smem) != cudaSuccess)
+    return set_cuda_error("cudaFuncSetAttribute(residual_kernel)");
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, residual_kernel, kRT, smem) != cudaSuccess || per_sm < 1)
     return set_error(SHAMPOO_ERR_UNSUPPORTED, "residual_kernel cannot be resident");

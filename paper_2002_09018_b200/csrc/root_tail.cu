@@ -419,14 +419,10 @@ size_t root_tail_ws_bytes(int batch) {
 int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter, int k_sw, double tol, double* errh,
                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
                      int* nact, void* maps_ws, cudaStream_t stream, int64_t* launches) {
-  static bool configured = false;
   const size_t smem = root_tail_smem_bytes();
-  if (!configured) {
-    if (cudaFuncSetAttribute(root_tail_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(root_tail_gemm_kernel)");
-    configured = true;
-  }
+  if (ensure_smem((const void*)root_tail_gemm_kernel, smem) !=
+      cudaSuccess)
+    return set_cuda_error("cudaFuncSetAttribute(root_tail_gemm_kernel)");
   if (batch > kTailMaxBatch) return set_error(SHAMPOO_ERR_UNSUPPORTED, "hybrid root: batch chunk > %d", kTailMaxBatch);
   // 3-D TMA maps (hi, lo) of every region over the batch: (n cols, n rows, batch), OOB -> 0
   CUtensorMap maps[2 * kTailRegions];
@@ -534,14 +530,9 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
                                const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x,
                                int* act, int* nact, void* oz_ws, cudaStream_t stream, int64_t* launches) {
   constexpr int kS = S;
-  static bool configured = false;
   const size_t smem = oz::gemm_smem_bytes<S, BK>();
-  if (!configured) {
-    if (cudaFuncSetAttribute(oz::gemm_kernel<S, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel)");
-    configured = true;
-  }
+  if (ensure_smem((const void*)oz::gemm_kernel<S, BK>, smem) != cudaSuccess)
+    return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel)");
   if (batch > kTailMaxBatch) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: batch chunk > %d", kTailMaxBatch);
   if (np % 64) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: padded n must be a multiple of 64");
   char* w = static_cast<char*>(oz_ws);

@@ -344,15 +344,11 @@ int stats_launch(const shampoo_tensor_t* tensors, int n_tensors, const shampoo_b
   (void)n_tensors;
   if (n_blocks == 0) return SHAMPOO_OK;
   StatsWs w = carve(ws, n_blocks);
-  static bool configured = false;
   const size_t smem_max = (size_t)kAsyncSmemDoubles * sizeof(double) + (size_t)kPrefixSmem * sizeof(int64_t);
   const size_t smem =
       (size_t)kAsyncSmemDoubles * sizeof(double) + (size_t)std::min(n_blocks + 1, kPrefixSmem) * sizeof(int64_t);
-  if (!configured) {
-    if (cudaFuncSetAttribute(stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max) != cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(stats_kernel)");
-    configured = true;
-  }
+  if (ensure_smem((const void*)stats_kernel, smem_max) != cudaSuccess)
+    return set_cuda_error("cudaFuncSetAttribute(stats_kernel)");
   if (cudaMemsetAsync(w.flag, 0, (size_t)n_blocks * sizeof(int), stream) != cudaSuccess)
     return set_cuda_error("cudaMemsetAsync");
   const unsigned eg = (unsigned)n_blocks * kChunks;

@@ -307,14 +307,10 @@ int make_map_f32(CUtensorMap* out, const void* base, int dims, const uint64_t* s
 int tc_gemm_launch(const TcJob* jobs_dev, int n_jobs, int64_t total_tiles, const CUtensorMap* maps_dev,
                    cudaStream_t stream, int64_t* launches) {
   if (total_tiles == 0) return SHAMPOO_OK;
-  static bool configured = false;
   const size_t smem = tc_gemm_smem_bytes();
-  if (!configured) {
-    if (cudaFuncSetAttribute(tc_gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(tc_gemm_3xtf32_kernel)");
-    configured = true;
-  }
+  if (ensure_smem((const void*)tc_gemm_3xtf32_kernel, smem) !=
+      cudaSuccess)
+    return set_cuda_error("cudaFuncSetAttribute(tc_gemm_3xtf32_kernel)");
   const int64_t g = total_tiles < num_sms() ? total_tiles : num_sms();
   tc_gemm_3xtf32_kernel<<<(unsigned)g, kTcThreads, smem, stream>>>(jobs_dev, n_jobs, total_tiles, maps_dev);
   ++*launches;

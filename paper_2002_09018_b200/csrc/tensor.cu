@@ -580,13 +580,9 @@ int tensor_stats_launch(const shampoo_ttensor_t* T, const shampoo_tblock_t* B, i
     ++*launches;
     if (L.n_tiles) {
       const size_t smem = (size_t)kAsyncSmemDoubles * sizeof(double);
-      static bool configured = false;
-      if (!configured) {
-        if (cudaFuncSetAttribute(t_stats_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-          return set_cuda_error("cudaFuncSetAttribute(t_stats_tile_kernel)");
-        configured = true;
-      }
+      if (ensure_smem((const void*)t_stats_tile_kernel, smem) !=
+          cudaSuccess)
+        return set_cuda_error("cudaFuncSetAttribute(t_stats_tile_kernel)");
       const int grid = std::min(L.n_tiles, 2 * num_sms());
       t_stats_tile_kernel<<<grid, kNThreads, smem, stream>>>(
           jobs, reinterpret_cast<const TItem*>(w + L.off_tiles), L.n_tiles, flag, wide, part);
@@ -715,13 +711,9 @@ int tensor_precondition_launch(const shampoo_ttensor_t* T, const shampoo_tblock_
   t_gather_kernel<<<eg, 256, 0, stream>>>(blks, Y);
   ++*launches;
   const size_t smem = (size_t)2 * 2 * kAsyncTile * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(t_mode_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return set_cuda_error("cudaFuncSetAttribute(t_mode_tile_kernel)");
-    configured = true;
-  }
+  if (ensure_smem((const void*)t_mode_tile_kernel, smem) !=
+      cudaSuccess)
+    return set_cuda_error("cudaFuncSetAttribute(t_mode_tile_kernel)");
   for (int i = 0; i < KO; ++i) {
     const TModeJob* jobs = reinterpret_cast<const TModeJob*>(w + L.off_jobs[i]);
     if (L.n_small[i]) {

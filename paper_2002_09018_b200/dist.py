@@ -46,9 +46,12 @@ def all_gather_roots(plan: Plan, roots: torch.Tensor, rank: int, world_size: int
 
 def refresh_roots(plan: Plan, stats: torch.Tensor, roots: torch.Tensor, rank: int = 0, world_size: int = 1,
                   group=None, eps_rel: float = 1e-6, tol: float = 1e-7, max_iter: int = 100,
-                  power_iters: int = 100, stream=None):
-    """Owner-sharded inverse p-th roots + all-gather.  Returns [(group, info)]."""
-    infos = refresh_group_roots(plan, stats, roots, rank, eps_rel, tol, max_iter, power_iters, stream=stream)
+                  power_iters: int = 100, stream=None, fp64_iters="auto"):
+    """Owner-sharded inverse p-th roots + all-gather.  Returns [(group, info)].
+    fp64_iters: root precision as in ``refresh_group_roots`` (default "auto", the bench's path: the INT8 Ozaki
+    root for n >= 512, FP64 DMMA below; None forces FP64 DMMA)."""
+    infos = refresh_group_roots(plan, stats, roots, rank, eps_rel, tol, max_iter, power_iters, stream=stream,
+                                fp64_iters=fp64_iters)
     all_gather_roots(plan, roots, rank, world_size, group)
     return infos
 

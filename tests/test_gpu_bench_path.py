@@ -1,0 +1,164 @@
+"""GPU parity of the bench's exact call (config 3, the metric's workload) against
+the fp64 oracle: the full Transformer-Big plan at b = 1024 (360 blocks, 528
+p=4 + 96 p=2 roots of 1024^2), statistics through ``stats_update``, then
+``refresh_group_roots(..., fp64_iters="auto")`` exactly as ``bench.py`` calls it
+(Ozaki INT8 root, 7 slices, for every group: all 624 statistics are 1024^2),
+then ``tf32_split`` + ``precondition`` with the refreshed roots.
+
+The oracle recomputes sampled blocks one by one from the same seeded gradients
+(``synth``): statistics (Alg. 1), coupled-Newton roots (P:206-214,
+S:131-132) and P = L^{-1/4} G R^{-1/4} / G R^{-1/2}.
+Bars: statistics bit-exact; roots 1e-6 (north star 1e-3); P with
+the GPU's own roots 2e-5 (north star 1e-3); graft scale 1e-5; every one of the
+624 roots status 0 with iterations +-1 of the oracle on the sampled ones."""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import plan as oplan
+from oracle import precondition as opre
+from oracle import root as oroot
+from oracle import stats as ostats
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+# vocab blocks (one-sided R, p = 2; block 31 is the ragged 256-row tail of emb_src), attention / FFN blocks (p = 4)
+SAMPLE = [0, 31, 95, 96, 100, 200, 359]
+STEPS = 2  # statistics accumulated over two identical steps (decay = weight = 1, the bench's setting)
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def bits(x):
+    return np.asarray(x, np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def shp():
+    import paper_2002_09018_b200 as shp
+    return shp
+
+
+@pytest.fixture(scope="module")
+def run(shp):
+    names_shapes = synth.transformer_big_shapes()
+    shapes = [s for _, s in names_shapes]
+    pl = shp.make_plan(shapes, 1024, 8192, 1)
+    Gd = []
+    for i, (m, n) in enumerate(shapes):  # the bench's gradient recipe (bench.py main)
+        seed = synth.BASE_SEED + 3 + i
+        Gd.append(synth.vocab_gradient_device(m, n, seed, DEV) if m == synth.VOCAB
+                  else synth.lowrank_gradient_device(m, n, seed, DEV))
+    Dd = [torch.zeros_like(G) for G in Gd]
+    Pd = [torch.zeros_like(G) for G in Gd]
+    table = shp.TensorTable(Gd, Dd, Pd)
+    stats = torch.zeros(pl.stats_elems, dtype=torch.float32, device=DEV)
+    roots = torch.zeros_like(stats)
+    roots_lo = torch.zeros_like(stats)
+    gn = torch.zeros(pl.n_blocks, dtype=torch.float64, device=DEV)
+    sc = torch.zeros(pl.n_blocks, dtype=torch.float32, device=DEV)
+    for _ in range(STEPS):
+        shp.stats_update(table, pl, stats, 1.0, 1.0, -1, gn)
+    infos = shp.refresh_group_roots(pl, stats, roots, 0, fp64_iters="auto")
+    shp.tf32_split(roots, roots_lo)
+    shp.precondition(table, pl, roots, gn, sc, roots_lo=roots_lo)
+    torch.cuda.synchronize()
+    groups = [(int(g["n"]), int(g["p"]), int(g["count"])) for g, _ in infos]
+    inf = np.concatenate([shp.info_to_numpy(i) for _, i in infos])
+
+    # oracle: the sampled blocks one by one, from the same seeded gradients
+    pl_o = oplan.plan(shapes, 1024, 8192, 1)
+    Gs_np = [None] * len(shapes)
+    for bi in SAMPLE:
+        t = pl_o.blocks[bi].tensor_id
+        if Gs_np[t] is None:
+            Gs_np[t] = Gd[t].cpu().numpy()
+    Ds_o = [np.zeros(s, np.float32) if g is not None else None for s, g in zip(shapes, Gs_np)]
+    stats_o = np.zeros(pl_o.stats_elems, np.float32)
+    for _ in range(STEPS):
+        num_o, _ = ostats.stats_update(Gs_np, Ds_o, pl_o, stats_o, 1.0, 1.0, blocks=SAMPLE)
+    roots_o = np.zeros(pl_o.stats_elems, np.float64)
+    root_info_o = {}
+    for bi in SAMPLE:
+        b = pl_o.blocks[bi]
+        for side, p, n, off, ld in (("L", b.p_left, b.rows, b.left_off, b.left_ld),
+                                    ("R", b.p_right, b.cols, b.right_off, b.right_ld)):
+            if p:
+                A = stats_o[off:off + n * ld].reshape(n, ld)[:, :n].astype(np.float64)
+                X, io = oroot.inverse_pth_root(A, p)
+                roots_o[off:off + n * ld].reshape(n, ld)[:, :n] = X
+                root_info_o[(bi, side)] = (io, off, n, ld, p)
+    Ps_o, sc_o, _ = opre.precondition_plan(Gs_np, Ds_o, pl_o, roots_o, num_o, blocks=SAMPLE)
+    return dict(pl=pl, pl_o=pl_o, stats=stats.cpu().numpy(), stats_o=stats_o, roots=roots.cpu().numpy(),
+                roots_o=roots_o, root_info_o=root_info_o, groups=groups, inf=inf, Pd=Pd, Ps_o=Ps_o, sc=sc.cpu().numpy(), sc_o=sc_o)
+
+
+def test_bench_plan_groups(run):
+    """The refresh issues exactly the bench's two batched calls: 528 p=4 and 96 p=2 roots of 1024^2."""
+    assert sorted(run["groups"]) == [(1024, 2, 96), (1024, 4, 528)]
+
+
+def test_bench_all_roots_converged(run):
+    inf = run["inf"]
+    assert inf.shape[0] == 624
+    assert np.all(inf["status"] == 0), np.unique(inf["status"], return_counts=True)
+    assert np.all(inf["iters"] > 0) and np.all(inf["err"] <= 1e-7)
+
+
+def test_bench_sampled_statistics_bit_exact(run):
+    for (bi, side), (_, off, n, ld, _) in run["root_info_o"].items():
+        seg = slice(off, off + n * ld)
+        assert np.array_equal(bits(run["stats"][seg]), bits(run["stats_o"][seg])), (bi, side)
+
+
+def test_bench_sampled_roots_vs_oracle(run):
+    """Ozaki (S = 7) roots of the bench's 528- and 96-matrix calls within 1e-6 of the fp64 oracle."""
+    pl = run["pl"]
+    p4 = p2 = 0
+    for (bi, side), (io, off, n, ld, p) in run["root_info_o"].items():
+        Xg = run["roots"][off:off + n * ld].reshape(n, ld)[:, :n]
+        Xo = run["roots_o"][off:off + n * ld].reshape(n, ld)[:, :n]
+        err = rel(Xg, Xo)
+        print(f"block {bi} {side} p={p}: root rel err {err:.3e}, oracle iters {io.iters}")
+        assert err < 1e-6, (bi, side, err)
+        gi = _gpu_info(run, pl, bi, side)
+        assert gi["status"] == io.status == 0
+        assert abs(int(gi["iters"]) - io.iters) <= 1
+        assert abs(gi["lambda_max"] - io.lambda_max) <= 1e-12 * io.lambda_max
+        p4 += p == 4
+        p2 += p == 2
+    assert p4 >= 4 and p2 >= 3
+
+
+def test_bench_sampled_precondition_vs_oracle(run):
+    pl_o = run["pl_o"]
+    for bi in SAMPLE:
+        b = pl_o.blocks[bi]
+        Pg = run["Pd"][b.tensor_id][b.row0:b.row0 + b.rows, b.col0:b.col0 + b.cols].cpu().numpy()
+        Po = run["Ps_o"][b.tensor_id][b.row0:b.row0 + b.rows, b.col0:b.col0 + b.cols]
+        err = rel(Pg, Po)
+        print(f"block {bi}: P rel err {err:.3e}")
+        assert err < 2e-5, (bi, err)
+        assert abs(run["sc"][bi] - run["sc_o"][bi]) <= 1e-5 * run["sc_o"][bi], bi
+
+
+# ------------------------------------------------------------------ helpers
+
+def _gpu_info(run, pl, bi, side):
+    """The GPU info record of statistic (bi, side): groups are packed in plan order, so the record's index is
+    the statistic's position inside its group (offset - group offset) / stride, after the earlier groups."""
+    off = int(pl.blocks[bi]["left_off" if side == "L" else "right_off"])
+    base = 0
+    for g in pl.groups_of(0):
+        go, cnt, st = int(g["offset"]), int(g["count"]), int(g["stride"])
+        if go <= off < go + cnt * st:
+            return run["inf"][base + (off - go) // st]
+        base += cnt
+    raise KeyError((bi, side))

@@ -62,6 +62,18 @@ def test_ozaki_1024(shp, mode, bar):
         assert inf[i]["status"] == 0 and abs(int(inf[i]["iters"]) - io.iters) <= 1
 
 
+@pytest.mark.parametrize("mode,bar", MODES)
+def test_ozaki_1024_p2(shp, mode, bar):
+    """The bench's one-sided vocabulary roots: p = 2 at n = 1024 (3 products per iteration, T^2 sliced in the
+    squaring's epilogue with the a-priori scale of reading #28)."""
+    As = synth.psd_batch(1024, 2, synth.BASE_SEED + 12, "mixed")
+    Xg, inf, outs = _both(shp, As, 2, mode=mode)
+    for i, (Xo, io) in enumerate(outs):
+        print(f"{mode} n=1024 p=2 matrix {i}: root rel err {rel(Xg[i], Xo):.3e}")
+        assert rel(Xg[i], Xo) < bar
+        assert inf[i]["status"] == io.status == 0 and abs(int(inf[i]["iters"]) - io.iters) <= 1
+
+
 def test_ozaki_2048(shp):
     """n > 1024: the two-pass slicing path and 32 k-chunks per tile (config 5's b = 2048 blocks)."""
     As = synth.psd_batch(2048, 1, synth.BASE_SEED + 5, "wishart")

@@ -48,22 +48,27 @@ def test_delayed_refresh_matches_synchronous_refresh_of_snapshot(precision):
 
 
 def test_schedule_covers_every_root_once_cpu():
-    """Host-side chunking: every owned root is scheduled exactly once per refresh."""
+    """Host-side chunking: every owned root is scheduled exactly once per refresh, at most `chunk` per step, and
+    the number of chunk steps -- hence the step of the all-gather -- is the same on every rank even when the LPT
+    owners hold unequal counts (a rank-dependent gather step would match collectives out of order)."""
     import paper_2002_09018_b200 as shp
-    from paper_2002_09018_b200.schedule import DelayedRefresh
-    shapes = [s for _, s in synth.transformer_big_shapes()]
-    for world in (1, 3):
-        plan = shp.make_plan(shapes, 1024, 8192, world)
-        for rank in range(world):
-            for spread in (1, 7, 500):
-                dr = DelayedRefresh.__new__(DelayedRefresh)
-                dr.units = [(g, 0, int(g["count"])) for g in plan.groups_of(rank)]
-                total = sum(u[2] for u in dr.units)
-                dr.chunk = max(1, -(-total // spread))
-                steps = dr._schedule()
-                assert len(steps) <= spread
-                seen = []
-                for st in steps:
-                    for g, i, n in st:
-                        seen += [(int(g["offset"]), i + k) for k in range(n)]
-                assert len(seen) == len(set(seen)) == total
+    from paper_2002_09018_b200.schedule import chunking, schedule_units
+    cases = [([s for _, s in synth.transformer_big_shapes()], 1024),
+             ([(256, 384), (128, 128), (300, 200), (1000, 64), (640, 512)], 128)]
+    for shapes, block in cases:
+        for world in (1, 2, 3):
+            plan = shp.make_plan(shapes, block, 8192, world)
+            counts = [sum(int(g["count"]) for g in plan.groups_of(r)) for r in range(world)]
+            for kappa, spread in ((500, None), (500, 7), (20, 1), (4, 3)):
+                chunk, n_steps = chunking(plan, world, kappa, spread)
+                assert n_steps <= min(kappa, spread or kappa)
+                for rank in range(world):
+                    units = [(g, 0, int(g["count"])) for g in plan.groups_of(rank)]
+                    steps = schedule_units(units, chunk, n_steps)
+                    assert len(steps) == n_steps  # identical on every rank
+                    seen = []
+                    for st in steps:
+                        assert sum(n for _, _, n in st) <= chunk
+                        for g, i, n in st:
+                            seen += [(int(g["offset"]), i + k) for k in range(n)]
+                    assert len(seen) == len(set(seen)) == counts[rank]

@@ -2,8 +2,12 @@
 roots + all-gather must give roots bit-identical to a single-GPU computation.
 
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
-        --master-port 29511 tools/check_multi_gpu.py
+        --master-port 29511 tools/check_multi_gpu.py [--root-precision auto|fp64|ozaki|ozaki6]
+
+--root-precision defaults to "auto", the bench's path (INT8 Ozaki root for n >= 512).
 """
+
+import argparse
 
 import os
 import sys
@@ -18,13 +22,23 @@ import synth  # noqa: E402
 from paper_2002_09018_b200 import dist as sdist  # noqa: E402
 
 
+MODES = {"auto": "auto", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki6": "ozaki6"}
+
+
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--root-precision", default="auto", choices=sorted(MODES))
+    ap.add_argument("--full", action="store_true", help="the whole Transformer-Big plan (bench.py's workload)")
+    args = ap.parse_args()
+    mode = MODES[args.root_precision]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    shapes = [s for _, s in synth.transformer_big_shapes()][3:40]  # attention + FFN blocks (no vocab)
+    shapes = [s for _, s in synth.transformer_big_shapes()]
+    if not args.full:
+        shapes = shapes[3:40]  # attention + FFN blocks (no vocab)
     Gs = [synth.lowrank_gradient_device(m, n, synth.BASE_SEED + 3 + i, dev) for i, (m, n) in enumerate(shapes)]
     table = shp.TensorTable(Gs, [torch.zeros_like(G) for G in Gs])
     # sharded
@@ -33,7 +47,7 @@ def main():
     roots = torch.zeros_like(stats)
     for _ in range(2):
         shp.stats_update(table, plan, stats, 1.0, 1.0, rank)
-    sdist.refresh_roots(plan, stats, roots, rank, world)
+    sdist.refresh_roots(plan, stats, roots, rank, world, fp64_iters=mode)
     torch.cuda.synchronize()
     # single-GPU reference on every rank (same kernels, whole plan)
     plan1 = shp.make_plan(shapes, 1024, 8192, 1)
@@ -42,7 +56,7 @@ def main():
     roots1 = torch.zeros_like(stats1)
     for _ in range(2):
         shp.stats_update(table1, plan1, stats1, 1.0, 1.0, -1)
-    shp.refresh_group_roots(plan1, stats1, roots1, 0)
+    shp.refresh_group_roots(plan1, stats1, roots1, 0, fp64_iters=mode)
     torch.cuda.synchronize()
     bad = 0
     for b, b1 in zip(plan.blocks, plan1.blocks):
@@ -57,7 +71,7 @@ def main():
     dist.all_reduce(t)
     if rank == 0:
         n_roots = int((plan.blocks["p_left"] > 0).sum() + (plan.blocks["p_right"] > 0).sum())
-        print(f"world {world}: {n_roots} roots, mismatching (summed over ranks) = {int(t.item())}", flush=True)
+        print(f"world {world}, root precision {args.root_precision} ({mode}), {len(shapes)} tensors: {n_roots} roots, mismatching (summed over ranks) = {int(t.item())}", flush=True)
     dist.destroy_process_group()
     if int(t.item()) != 0:
         raise SystemExit(1)
