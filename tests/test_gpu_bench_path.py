@@ -95,7 +95,17 @@ def run(shp):
                 X, io = oroot.inverse_pth_root(A, p)
                 roots_o[off:off + n * ld].reshape(n, ld)[:, :n] = X
                 root_info_o[(bi, side)] = (io, off, n, ld, p)
-    Ps_o, sc_o, _ = opre.precondition_plan(Gs_np, Ds_o, pl_o, roots_o, num_o, blocks=SAMPLE)
+    # P_b = X_L G_b X_R / G_b X_R and the graft scale, block by block (opre.precondition_block)
+    Ps_o, sc_o = {}, {}
+    for bi in SAMPLE:
+        b = pl_o.blocks[bi]
+        Gb = Gs_np[b.tensor_id][b.row0:b.row0 + b.rows, b.col0:b.col0 + b.cols]
+        XL = roots_o[b.left_off:b.left_off + b.rows * b.left_ld].reshape(b.rows, b.left_ld)[:, :b.rows] \
+            if b.p_left else None
+        XR = roots_o[b.right_off:b.right_off + b.cols * b.right_ld].reshape(b.cols, b.right_ld)[:, :b.cols] \
+            if b.p_right else None
+        Ps_o[bi] = opre.precondition_block(Gb, XL, XR)
+        sc_o[bi] = opre.graft_scale(float(num_o[bi]), float(np.sum(Ps_o[bi] * Ps_o[bi])))
     return dict(pl=pl, pl_o=pl_o, stats=stats.cpu().numpy(), stats_o=stats_o, roots=roots.cpu().numpy(),
                 roots_o=roots_o, root_info_o=root_info_o, groups=groups, inf=inf, Pd=Pd, Ps_o=Ps_o, sc=sc.cpu().numpy(), sc_o=sc_o)
 
@@ -142,7 +152,7 @@ def test_bench_sampled_precondition_vs_oracle(run):
     for bi in SAMPLE:
         b = pl_o.blocks[bi]
         Pg = run["Pd"][b.tensor_id][b.row0:b.row0 + b.rows, b.col0:b.col0 + b.cols].cpu().numpy()
-        Po = run["Ps_o"][b.tensor_id][b.row0:b.row0 + b.rows, b.col0:b.col0 + b.cols]
+        Po = run["Ps_o"][bi]
         err = rel(Pg, Po)
         print(f"block {bi}: P rel err {err:.3e}")
         assert err < 2e-5, (bi, err)
