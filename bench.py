@@ -67,17 +67,25 @@ def _int8_peak():
 # list profiles/r01za_launches_root528_summary.txt
 OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = ((9.71 + 4.39) + (4.67 + 3.85) + (4.71 + 3.85) + (8.37 + 4.39)) / 4 * 1e9 / 528
 # the arithmetic of the dominant phase (the roots): fp64 iterates, products per the root precision
-DTYPE = {"auto": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
+DTYPE = {"auto": "f64 iterates, int8 Ozaki products S=7..5 per iteration (exact int32 accumulation)",
+         "auto7": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
          "auto6": "f64 iterates, int8 Ozaki S=6 products (exact int32 accumulation)",
-         "ozaki": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
+         "ozaki": "f64 iterates, int8 Ozaki products S=7..5 per iteration (exact int32 accumulation)",
+         "ozaki7": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
          "ozaki6": "f64 iterates, int8 Ozaki S=6 products (exact int32 accumulation)",
          "fp64": "f64 (FP64 DMMA)", "hybrid": "f64 DMMA, then 3xTF32 (tf32 tcgen05) tail"}
 EMPTY_LAUNCH_MS = 0.05  # an Ozaki GEMM launch with no active matrix returns in a few microseconds
-ROOT_MODE = {"auto": "auto", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki6": "ozaki6", "hybrid": -1}
-ROOT_SLICES = {"auto": 7, "auto6": 6, "ozaki": 7, "ozaki6": 6}
-ROOT_LABEL = {"auto": "auto: ozaki (INT8 tcgen05, 7 slices, exact int32 accumulation) for n >= 512, fp64 DMMA below",
+ROOT_MODE = {"auto": "auto", "auto7": "auto7", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki7": "ozaki7",
+             "ozaki6": "ozaki6", "hybrid": -1}
+# (max slices, scheduled?) of the Ozaki modes
+ROOT_SLICES = {"auto": (7, True), "auto7": (7, False), "auto6": (6, False), "ozaki": (7, True), "ozaki7": (7, False),
+               "ozaki6": (6, False)}
+ROOT_LABEL = {"auto": "auto: ozaki (INT8 tcgen05, per-iteration slice schedule 7..5 of reading #29, exact int32 "
+                      "accumulation) for n >= 512, fp64 DMMA below",
+              "auto7": "auto7: ozaki (INT8 tcgen05, 7 slices, exact int32 accumulation) for n >= 512, fp64 DMMA below",
               "auto6": "auto6: ozaki (INT8 tcgen05, 6 slices, exact int32 accumulation) for n >= 512, fp64 DMMA below",
-              "fp64": "fp64 DMMA", "ozaki": "ozaki: INT8 tcgen05, 7 slices, exact int32 accumulation",
+              "fp64": "fp64 DMMA", "ozaki": "ozaki: INT8 tcgen05, slice schedule 7..5, exact int32 accumulation",
+              "ozaki7": "ozaki7: INT8 tcgen05, 7 slices, exact int32 accumulation",
               "ozaki6": "ozaki6: INT8 tcgen05, 6 slices, exact int32 accumulation",
               "hybrid": "hybrid fp64 DMMA -> 3xTF32 tcgen05 (auto switch)"}
 
@@ -331,7 +339,7 @@ def main():
     g4 = sorted([g for g in plan.groups_of(rank) if int(g["p"]) == 4], key=lambda g: -int(g["count"]) * int(g["n"]) ** 3)
     roof = None
     iters_mean = None
-    slices = ROOT_SLICES.get(args.root_precision)
+    slices, scheduled = ROOT_SLICES.get(args.root_precision, (None, False))
     if g4 and slices and (args.root_precision.startswith("ozaki") or int(g4[0]["n"]) >= shp.OZAKI_MIN_N):
         # the INT8 GEMM dominates: every launch bracketed by CUDA events on its stream
         g = g4[0]
@@ -344,7 +352,8 @@ def main():
         shp.profile_begin()
         e0.record(stream)
         shp.inverse_pth_root_ptr(stats.data_ptr() + 4 * off, gld, stride, roots.data_ptr() + 4 * off, gld, stride,
-                                 cnt, gn_, 4, info, tol=args.tol, device=dev, fp64_iters=f"ozaki{slices}")
+                                 cnt, gn_, 4, info, tol=args.tol, device=dev,
+                                 fp64_iters="ozaki" if scheduled else f"ozaki{slices}")
         e1.record(stream)
         torch.cuda.synchronize()
         gemm_ms, gemm_launches = shp.profile_end("ozaki_gemm")
@@ -358,8 +367,8 @@ def main():
         iters_mean = float(inf["iters"].sum()) / cnt
         n = gn_
         # algorithmic int8 ops: per symmetric product S(S+1)/2 slice products of n^2 (n+1) (upper triangle incl.
-        # diagonal, 2 ops per multiply-add), 4 products per iteration
-        ops = float(inf["iters"].sum()) * 4 * (slices * (slices + 1) // 2) * n * n * (n + 1)
+        # diagonal, 2 ops per multiply-add), 4 products per iteration, S per iteration from the library's schedule
+        ops = shp.ozaki_int8_ops(inf["iters"], n, 4, 1e-6, None if scheduled else 0.0, slices)
         achieved = ops / (gemm_ms * 1e-3) / 1e12
         peak, peak_kind, peak_burst = _int8_peak()
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
@@ -376,7 +385,8 @@ def main():
                 "fp64_equivalent_tflops": (float(inf["iters"].sum()) * 4 * n * n * (n + 1)
                                            + cnt * 100 * 2.0 * n * n) / (call_ms * 1e-3) / 1e12,
                 "peak_source": f"int8 dense = 2 x the {peak_kind} bf16 TF/s of MEASURED_PEAKS.json (nominal "
-                               f"int8:bf16 ratio 2; NVIDIA nominal 4.5 POPS)", "slices": slices,
+                               f"int8:bf16 ratio 2; NVIDIA nominal 4.5 POPS)", "slices": slices, "slice_schedule": [shp.ozaki_iteration_slices(k, 4, 1e-6, None if scheduled else 0.0, slices)
+                                                        for k in range(int(inf["iters"].max()))],
                 "frac_vs_burst_peak": (achieved / peak_burst) if peak_burst else None,
                 "peak_note": "the sustained bf16 figure was measured at ~1290 MHz under a bf16 GEMM's power draw; "
                              "this int8 kernel runs at ~1550-1650 MHz under the cap, and at b >= 2048 exceeds the "

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SHAMPOO_ABI_VERSION 3
+#define SHAMPOO_ABI_VERSION 4
 
 typedef enum {
   SHAMPOO_OK = 0,
@@ -230,13 +230,27 @@ int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t
  * slices = 6 (21 products): the precision chosen against the north star's
  *   1e-3 bar -- host emulation (tools/ozaki_precision.py) 3.8e-6 at n = 256;
  *   measured on B200 in tests/test_gpu_ozaki.py.
- * Any other value: SHAMPOO_ERR_INVALID_ARG, nothing enqueued. */
+ * Any other value: SHAMPOO_ERR_INVALID_ARG, nothing enqueued.
+ * slice_budget (ABI v4; reading #29): 0 = every product of every
+ *   iteration uses `slices` slices (the fixed-slice root).  > 0 = per-iteration
+ *   schedule: an error in M_k reaches the root amplified by ~1/(p lambda_min(M_k))
+ *   and lambda_min(M_k) >= m_k = min(1, eps_rel g^k), g = ((p+1)/p)^p (the ridge
+ *   and the scalar recurrence), so iteration k uses the smallest S in
+ *   [5, slices] with 2^-(7S-1) / (p m_k) <= slice_budget, and the X-update
+ *   X_k T_k (not amplified) min(S, 5).  eps_rel = 0 keeps `slices` throughout.
+ *   1e-9 (the binding's default): 0.68 of the fixed-7 slice products at
+ *   n = 1024, p = 4, kappa 1e6, root error 2.9e-7 vs 1.2e-7 in host emulation
+ *   (tools/ozaki_schedule.py).  Must be in [0, 1), else SHAMPOO_ERR_INVALID_ARG. */
 size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter);
+/* Host-only: the slice count the Ozaki root uses for the products of iteration
+ * k (the M-chain; the X-update uses min(result, 5) when slice_budget > 0) for
+ * these arguments -- the schedule above, for accounting (bench roofline). */
+int shampoo_ozaki_iteration_slices(int32_t k, int32_t p, double eps_rel, double slice_budget, int32_t slices);
 int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
                                            int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
                                            double tol, int32_t max_iter, int32_t power_iters, int32_t slices,
-                                           shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
-                                           shampoo_stream_t stream);
+                                           double slice_budget, shampoo_root_info_t* info, void* workspace,
+                                           size_t workspace_bytes, shampoo_stream_t stream);
 
 /* Independent root check (config 2, north-star invariant):
  *   residual_i = || X_i^p (A_i + eps_rel*lambda_i*I) - I ||_F   in fp64,

@@ -171,21 +171,23 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
                          fp64_iters: int | None = None, ws_tag: str = "root"):
     """X = A_hat^{-r/p} (r = 1: shampoo_inverse_pth_root_batched, else the rational entry).
     fp64_iters (r = 1 only): hybrid FP64 -> 3xTF32 tensor-core root (-1 = automatic switch);
-    fp64_iters="ozaki" (= "ozaki7"): every product on the INT8 tensor cores, 7 slices, fp64-level accuracy;
-    fp64_iters="ozaki6": 6 slices (21 slice products instead of 28; DESIGN.md §6.3c);
-    fp64_iters="auto" / "auto6": "ozaki" / "ozaki6" for n >= OZAKI_MIN_N, FP64 DMMA below.
+    fp64_iters="ozaki": every product on the INT8 tensor cores with the per-iteration slice schedule
+    (reading #29: 7 slices while the ridge-bounded amplification is large, down to 5; SLICE_BUDGET);
+    fp64_iters="ozaki7" / "ozaki6": 7 / 6 slices for every product (DESIGN.md §6.3c);
+    fp64_iters="auto" / "auto7" / "auto6": "ozaki" / "ozaki7" / "ozaki6" for n >= OZAKI_MIN_N, FP64 DMMA below.
     ws_tag: workspace cache key -- calls that may run concurrently on different streams need different tags."""
     L = _lib.lib()
-    if fp64_iters in ("auto", "auto6"):  # the INT8 Ozaki loop pays off from n = 512 (per-iteration launches, 128-row tiles)
+    if fp64_iters in ("auto", "auto6", "auto7"):  # the INT8 Ozaki loop pays off from n = 512 (launches, 128-row tiles)
         fp64_iters = ("ozaki" + fp64_iters[4:]) if (n >= OZAKI_MIN_N and r == 1) else None
     if isinstance(fp64_iters, str) and fp64_iters.startswith("ozaki"):
         slices = int(fp64_iters[5:] or 7)
+        budget = SLICE_BUDGET if fp64_iters == "ozaki" else 0.0
         if r != 1:
             raise ValueError("the ozaki root serves r = 1 only")
         wsb = L.shampoo_root_ozaki_workspace_bytes(batch, n, p, max_iter)
         ws = workspace(wsb, device if device is not None else info.device, ws_tag)
         check(L.shampoo_inverse_pth_root_batched_ozaki(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
-                                                       tol, max_iter, power_iters, slices, info.data_ptr(),
+                                                       tol, max_iter, power_iters, slices, budget, info.data_ptr(),
                                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
         return
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
@@ -260,6 +262,10 @@ _refresh_launches = 0
 # smallest n for which precision "auto" picks the Ozaki root (measured on B200: n = 128 ozaki 19k roots/s vs
 # FP64 DMMA 72k; n = 512 2.7k vs 2.5k; n = 1024 580 vs 354 -- profiles/r01t_*)
 OZAKI_MIN_N = 512
+# per-iteration slice schedule of the Ozaki root (reading #29, shampoo.h slice_budget): iteration k takes the fewest
+# slices S in [5, 7] with 2^-(7S-1) / (p min(1, eps_rel g^k)) <= SLICE_BUDGET (host emulation at n = 1024, p = 4,
+# kappa 1e6: 0.68 of the fixed-7 slice products, root error 2.9e-7 vs 1.2e-7; tools/ozaki_schedule.py)
+SLICE_BUDGET = 1e-9
 
 
 def last_refresh_launch_count() -> int:
@@ -451,6 +457,29 @@ def profile_end(kernel: str | None = None):
     n = np.zeros(1, np.int64)
     check(_lib.lib().shampoo_profile_end(kernel.encode() if kernel else None, ms.ctypes.data, n.ctypes.data))
     return float(ms[0]), int(n[0])
+
+
+def ozaki_iteration_slices(k: int, p: int, eps_rel: float = 1e-6, budget: float | None = None,
+                           slices: int = 7) -> int:
+    """Slices of the M-chain products of Ozaki iteration k (reading #29; the library's schedule)."""
+    b = SLICE_BUDGET if budget is None else budget
+    return int(_lib.lib().shampoo_ozaki_iteration_slices(k, p, eps_rel, b, slices))
+
+
+def ozaki_int8_ops(iters, n: int, p: int, eps_rel: float = 1e-6, budget: float | None = None,
+                   slices: int = 7) -> float:
+    """Algorithmic int8 ops of an Ozaki root call: per matrix and iteration, each symmetric product takes
+    S(S+1)/2 slice products of n^2 (n+1) ops (upper triangle incl. the diagonal, 2 ops per multiply-add);
+    the X-update at min(S, 5) under a schedule.  `iters`: iterations per matrix (root info)."""
+    b = SLICE_BUDGET if budget is None else budget
+    prods = (p.bit_length() - 1) + bin(p).count("1")  # T^p chain (squarings + multiplications) + T^p M
+    per_k = []
+    for k in range(int(max(iters)) if len(iters) else 0):
+        S = ozaki_iteration_slices(k, p, 1e-6 if eps_rel is None else eps_rel, b, slices)
+        Sx = min(S, 5) if b > 0 else S
+        per_k.append(Sx * (Sx + 1) // 2 + prods * S * (S + 1) // 2)
+    cum = np.concatenate([[0], np.cumsum(per_k)])
+    return float(sum(cum[int(i)] for i in iters)) * n * n * (n + 1)
 
 
 def profile_launch_ms(kernel: str | None = None) -> np.ndarray:

@@ -40,7 +40,7 @@ EXPORTED = [
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_inverse_pth_root_batched_hybrid", "shampoo_root_ozaki_workspace_bytes",
     "shampoo_inverse_pth_root_batched_ozaki", "shampoo_profile_begin", "shampoo_profile_end",
-    "shampoo_profile_launch_ms",
+    "shampoo_profile_launch_ms", "shampoo_ozaki_iteration_slices",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition", "shampoo_precondition_split",
     "shampoo_tf32_split",
@@ -95,7 +95,7 @@ def lib():
     L.shampoo_root_ozaki_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
     L.shampoo_root_ozaki_workspace_bytes.restype = _sz
     L.shampoo_inverse_pth_root_batched_ozaki.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl,
-                                                         _dbl, _i32, _i32, _i32, _vp, _vp, _sz, _vp]
+                                                         _dbl, _i32, _i32, _i32, _dbl, _vp, _vp, _sz, _vp]
     L.shampoo_inverse_pth_root_batched_ozaki.restype = ctypes.c_int
     L.shampoo_root_residual_workspace_bytes.argtypes = [_i32, _i32, _i32]
     L.shampoo_root_residual_workspace_bytes.restype = _sz
@@ -129,7 +129,9 @@ def lib():
     L.shampoo_profile_end.restype = ctypes.c_int
     L.shampoo_profile_launch_ms.argtypes = [ctypes.c_char_p, _vp, ctypes.c_int64, _vp]
     L.shampoo_profile_launch_ms.restype = ctypes.c_int
-    if L.shampoo_abi_version() != 3:
+    L.shampoo_ozaki_iteration_slices.argtypes = [_i32, _i32, _dbl, _dbl, _i32]
+    L.shampoo_ozaki_iteration_slices.restype = ctypes.c_int
+    if L.shampoo_abi_version() != 4:
         raise ImportError("libshampoo ABI version mismatch")
     _lib = L
     return L

@@ -250,7 +250,12 @@ int shampoo_inverse_pth_root_batched(const float* A, int64_t lda, int64_t stride
 static int root_entry(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x,
                       int32_t batch, int32_t n, int32_t p, int32_t r, int32_t k_sw, double eps_rel, double tol,
                       int32_t max_iter, int32_t power_iters, shampoo_root_info_t* info, void* workspace,
-                      size_t workspace_bytes, shampoo_stream_t stream, int precision = 0, int slices = 7);
+                      size_t workspace_bytes, shampoo_stream_t stream, int precision = 0, int slices = 7,
+                      double slice_budget = 0.0);
+
+int shampoo_ozaki_iteration_slices(int32_t k, int32_t p, double eps_rel, double slice_budget, int32_t slices) {
+  return ozaki_iteration_slices(k, p, eps_rel, slice_budget, slices);
+}
 
 size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter) {
   (void)p;
@@ -261,10 +266,10 @@ size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, i
 int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
                                            int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
                                            double tol, int32_t max_iter, int32_t power_iters, int32_t slices,
-                                           shampoo_root_info_t* info, void* workspace, size_t workspace_bytes,
-                                           shampoo_stream_t stream) {
+                                           double slice_budget, shampoo_root_info_t* info, void* workspace,
+                                           size_t workspace_bytes, shampoo_stream_t stream) {
   return root_entry(A, lda, stride_a, X, ldx, stride_x, batch, n, p, 1, 0, eps_rel, tol, max_iter, power_iters, info,
-                    workspace, workspace_bytes, stream, 2, slices);
+                    workspace, workspace_bytes, stream, 2, slices, slice_budget);
 }
 
 int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
@@ -313,7 +318,8 @@ int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t
 static int root_entry(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x,
                       int32_t batch, int32_t n, int32_t p, int32_t r, int32_t k_sw, double eps_rel, double tol,
                       int32_t max_iter, int32_t power_iters, shampoo_root_info_t* info, void* workspace,
-                      size_t workspace_bytes, shampoo_stream_t stream, int precision, int slices) {
+                      size_t workspace_bytes, shampoo_stream_t stream, int precision, int slices,
+                      double slice_budget) {
   g_err[0] = 0;
   g_launches = 0;
   if (batch < 0) return set_error(SHAMPOO_ERR_INVALID_ARG, "batch < 0");
@@ -331,11 +337,14 @@ static int root_entry(const float* A, int64_t lda, int64_t stride_a, float* X, i
     return set_error(SHAMPOO_ERR_INVALID_ARG, "max_iter in [0, 1000], power_iters >= 1");
   if (precision == 2 && slices != 6 && slices != 7)
     return set_error(SHAMPOO_ERR_INVALID_ARG, "slices = %d not in {6, 7}", slices);
+  if (precision == 2 && !(slice_budget >= 0.0 && slice_budget < 1.0))
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "slice_budget must be in [0, 1)");
   if (precision == 2 && max_iter < 1) precision = 0;  // nothing to iterate: the fp64 kernel decides at k = 0
   const int mode = precision ? precision : (k_sw <= max_iter ? 1 : 0);
   int rc = check_ws(workspace, workspace_bytes, root_workspace_bytes(batch, n, max_iter, mode));
   if (rc) return rc;
-  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, r, k_sw, precision, slices, eps_rel, tol,
+  return root_launch(A, lda, stride_a, X, ldx, stride_x, batch, n, p, r, k_sw, precision, slices, slice_budget,
+                     eps_rel, tol,
                      max_iter,
                      power_iters, info,
                      workspace, static_cast<cudaStream_t>(stream), &g_launches);

@@ -15,15 +15,18 @@ int set_cuda_error(const char* what, cudaError_t e = cudaGetLastError());
 // root.cu
 size_t root_workspace_bytes(int batch, int n, int max_iter, int precision);  // 0 fp64, 1 hybrid, 2 ozaki
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
-                int n, int p, int r, int k_sw, int precision, int slices, double eps_rel, double tol, int max_iter,
-                int power_iters,
+                int n, int p, int r, int k_sw, int precision, int slices, double slice_budget, double eps_rel,
+                double tol, int max_iter, int power_iters,
                 shampoo_root_info_t* info, void* ws, cudaStream_t stream, int64_t* launches);
 // root_tail.cu (hybrid 3xTF32 tail)
 size_t root_tail_ws_bytes(int batch);
 size_t root_ozaki_ws_bytes(int batch, int n);
 int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
                       const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
-                      int* nact, void* oz_ws, int slices, cudaStream_t stream, int64_t* launches);
+                      int* nact, void* oz_ws, int slices, double eps_rel, double slice_budget, cudaStream_t stream,
+                      int64_t* launches);
+// slice count of Ozaki iteration k (reading #29; root_tail.cu)
+int ozaki_iteration_slices(int k, int p, double eps_rel, double budget, int s_max);
 int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter, int k_sw, double tol, double* errh,
                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
                      int* nact, void* maps_ws, cudaStream_t stream, int64_t* launches);

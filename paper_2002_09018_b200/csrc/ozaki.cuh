@@ -34,7 +34,11 @@
 namespace shp {
 namespace oz {
 
-constexpr int kSMax = 7;                    // most slices per operand (workspace sizing)
+// most slices per operand: every operand's planes are laid out with this pitch
+// (plane s of matrix mat is plane mat * kSMax + s), so products of different
+// slice counts S <= kSMax read the leading S planes of the same buffers
+// (the per-iteration slice schedule, reading #29)
+constexpr int kSMax = 7;
 constexpr int kBM = 128, kBN = 64;  // tile M, N
 // k-chunk BK bytes (int8 elements) per pipeline stage: BK / 32 K=32 MMA steps
 template <int S, int BK>
@@ -173,7 +177,7 @@ __device__ __forceinline__ double t_of(double m, bool diag, double pp1, double i
 }
 
 // One warp per (matrix, row): scale[mat*np + i] = 2^e_i, planes
-// [(mat*S + s)*np + i]*np + j = d_s(A_ij) for j < n, where A = src, or, with TM,
+// [(mat*kSMax + s)*np + i]*np + j = d_s(A_ij), s < S for j < n, where A = src, or, with TM,
 // A = T_k = ((p+1)I - M_k)/p computed on the fly from src = M_k (T_k is never
 // stored in fp64).  Rows of n <= 1024 are held in registers (32 doubles per
 // lane, 8 KB in flight per warp, 16 warps per SM): ONE pass over HBM for the
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
-    int8_t* prow = planes + ((int64_t)mat * S * np + i) * np;
+    int8_t* prow = planes + ((int64_t)mat * kSMax * np + i) * np;
     // TM: off the diagonal T_ij = -M_ij / p (one multiply: the same value as (0 - m) / p up to the sign
     // of zero); the diagonal element once per row
     const double tii = TM ? t_of(row[i], true, pp1, inv_p) : 0.0;
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(256, 2) slice_mt_kernel(const double* __restri
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
-    const int64_t prow = ((int64_t)mat * S * np + i) * np;
+    const int64_t prow = ((int64_t)mat * kSMax * np + i) * np;
     const double tii = t_of(row[i], true, pp1, inv_p);
     double r[kRegChunks][8];
     double mx = 0.0, mo = 0.0;  // max |M_ij| over the row, and over the row without the diagonal
@@ -388,7 +392,7 @@ struct OzJob {
   double* out;              // fp64 output of matrix 0; matrix m at out + m * out_stride
   int64_t out_stride;
   // sliced output (out == nullptr, symmetric products only): the product's S int8 planes at
-  // planes[(mat S + s) np^2], every row scaled by the a-priori bound 2^out_e (|C_ij| < 2^out_e),
+  // planes[(mat kSMax + s) np^2], every row scaled by the a-priori bound 2^out_e (|C_ij| < 2^out_e),
   // 2^out_e written to out_scale[mat np + row]
   int8_t* planes;
   double* out_scale;
@@ -510,9 +514,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             tc::mbar_arrive_expect_tx(fb, grp_bytes<S, BK>(g));
 #pragma unroll
             for (int s = 0; s < kS; ++s) {
-              if (grp_a(s) == g) tc::tma_load_3d(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kS + s);
+              if (grp_a(s) == g) tc::tma_load_3d(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kSMax + s);
               if (grp_b(s) == g)
-                tc::tma_load_3d(st + kS * kAPlane + s * kBPlane, bm, fb, kc * kBK, tj * kBN, mat * kS + s);
+                tc::tma_load_3d(st + kS * kAPlane + s * kBPlane, bm, fb, kc * kBK, tj * kBN, mat * kSMax + s);
             }
           }
           if (++stage == kStages) {
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         // stores of whole sectors; diagonal-band and ragged tiles store bytes
         const int j0 = tj * kBN;
         const int64_t pitch = (int64_t)a.np * a.np;
-        int8_t* pl = J.planes + (int64_t)mat * kS * pitch;
+        int8_t* pl = J.planes + (int64_t)mat * kSMax * pitch;
         // A = B (squarings): C is computed bit-symmetrically (the same exact integer pair sums, the same
         // scales), so the lower-triangle values a tile computes equal their mirrors and every in-range
         // tile may store whole rows and the whole transpose; otherwise only tiles above the diagonal
@@ -768,12 +772,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 template <int S, int BK>
 inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S, BK>::kStages * Cfg<S, BK>::kStageBytes + 512; }
 
-// 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * S),
+// 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * kSMax),
 // row pitch np bytes, plane pitch np*np bytes, box (64 B, box_rows, 1), SWIZZLE_64B
 template <class Encode>
 inline CUresult make_plane_map(Encode enc, CUtensorMap* out, const int8_t* base, int n, int np, int batch,
-                               int box_rows, int S, int kBK) {
-  cuuint64_t gdim[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch * S};
+                               int box_rows, int kBK) {
+  cuuint64_t gdim[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch * kSMax};
   cuuint64_t gstride[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
   cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
   cuuint32_t estride[3] = {1, 1, 1};

@@ -654,8 +654,9 @@ size_t root_smem_bytes(int n) {
 }
 
 int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx, int64_t stride_x, int batch,
-                int n, int p, int r, int k_sw, int precision, int slices, double eps_rel, double tol, int max_iter,
-                int power_iters, shampoo_root_info_t* info, void* ws, cudaStream_t stream, int64_t* launches) {
+                int n, int p, int r, int k_sw, int precision, int slices, double slice_budget, double eps_rel,
+                double tol, int max_iter, int power_iters, shampoo_root_info_t* info, void* ws, cudaStream_t stream,
+                int64_t* launches) {
   const bool oz = (precision == 2);
   const size_t smem = oz ? (2 * (size_t)n + 8) * sizeof(double) : root_smem_bytes(n);
   if (oz) {
@@ -725,7 +726,7 @@ int root_launch(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t
     }
     if (precision == 2) {
       int rc = root_ozaki_launch(a.bufs, bc, n, np, p, max_iter, tol, a.errh, a.res, a.info, a.X, ldx, stride_x,
-                                 a.tail_act, a.tail_nact, oz_ws, slices, stream, launches);
+                                 a.tail_act, a.tail_nact, oz_ws, slices, eps_rel, slice_budget, stream, launches);
       if (rc) return rc;
     } else if (k_sw <= max_iter) {
       int rc = root_tail_launch(a.bufs, bc, n, np, p, max_iter, k_sw, tol, a.errh, a.res, a.info, a.X, ldx, stride_x,

@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -525,18 +526,86 @@ size_t root_ozaki_ws_bytes(int batch, int n) {
   return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap);
 }
 
-template <int S, int BK>
-static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
-                               const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x,
-                               int* act, int* nact, void* oz_ws, cudaStream_t stream, int64_t* launches) {
-  constexpr int kS = S;
-  const size_t smem = oz::gemm_smem_bytes<S, BK>();
-  if (ensure_smem((const void*)oz::gemm_kernel<S, BK>, smem) != cudaSuccess)
-    return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel)");
+// Slice count of iteration k (reading #29): an error made in M_k reaches the
+// root amplified by ~1/(p lambda_min(M_k)), lambda_min(M_0) >= eps_rel / (1 +
+// eps_rel) (the ridge) and the scalar recurrence grows it by g = ((p+1)/p)^p per
+// iteration while it is small -- so m_k = min(1, eps_rel g^k) bounds it a priori
+// and S_k = the smallest S in [kOzSMin, s_max] with 2^-(7S-1) / (p m_k) <= budget.
+// budget <= 0 (or no ridge): S_k = s_max for every k (the fixed-slice root).
+constexpr int kOzSMin = 5;  // S = 4 (2^-27) was measured (host emulation) to leave a 4e-6 floor in the root
+constexpr int kOzSX = 5;    // the X-update X_k T_k: X only accumulates T's (no amplification)
+int ozaki_iteration_slices(int k, int p, double eps_rel, double budget, int s_max) {
+  if (!(budget > 0.0) || !(eps_rel > 0.0)) return s_max;
+  const double g = std::pow((double)(p + 1) / (double)p, (double)p);
+  const double m = std::min(1.0, eps_rel * std::pow(g, (double)k));
+  for (int S = kOzSMin; S < s_max; ++S)
+    if (std::ldexp(1.0, -(7 * S - 1)) / ((double)p * m) <= budget) return S;
+  return s_max;
+}
+
+template <int S>
+static cudaError_t oz_gemm_s(const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {
+  const size_t smem = oz::gemm_smem_bytes<S, 64>();
+  cudaError_t e = ensure_smem((const void*)oz::gemm_kernel<S, 64>, smem);
+  if (e != cudaSuccess) return e;
+  oz::gemm_kernel<S, 64><<<num_sms(), oz::kThreads, smem, stream>>>(a, maps);
+  return cudaSuccess;
+}
+
+static cudaError_t oz_gemm(int S, const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {
+  switch (S) {
+    case 5: return oz_gemm_s<5>(a, maps, stream);
+    case 6: return oz_gemm_s<6>(a, maps, stream);
+    default: return oz_gemm_s<7>(a, maps, stream);
+  }
+}
+
+template <int S>
+static void oz_slice_s(bool tm, const double* src, int64_t mstride, int n, int np, int batch, const int* act,
+                       const int* nact, int8_t* planes, double* scale, int p, cudaStream_t stream) {
+  const int grid = 8 * num_sms();
+  if (tm)
+    oz::slice_kernel<S, true><<<grid, 256, 0, stream>>>(src, mstride, n, np, batch, act, nact, planes, scale, p);
+  else
+    oz::slice_kernel<S, false><<<grid, 256, 0, stream>>>(src, mstride, n, np, batch, act, nact, planes, scale, p);
+}
+
+static void oz_slice(int S, bool tm, const double* src, int64_t mstride, int n, int np, int batch, const int* act,
+                     const int* nact, int8_t* planes, double* scale, int p, cudaStream_t stream) {
+  switch (S) {
+    case 5: oz_slice_s<5>(tm, src, mstride, n, np, batch, act, nact, planes, scale, p, stream); break;
+    case 6: oz_slice_s<6>(tm, src, mstride, n, np, batch, act, nact, planes, scale, p, stream); break;
+    default: oz_slice_s<7>(tm, src, mstride, n, np, batch, act, nact, planes, scale, p, stream); break;
+  }
+}
+
+template <int S>
+static void oz_slice_mt_s(const double* src, int64_t mstride, int n, int np, int batch, const int* act,
+                          const int* nact, int8_t* pm, double* sm, int8_t* pt, double* st, int p, cudaStream_t stream) {
+  oz::slice_mt_kernel<S><<<8 * num_sms(), 256, 0, stream>>>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p);
+}
+
+static void oz_slice_mt(int S, const double* src, int64_t mstride, int n, int np, int batch, const int* act,
+                        const int* nact, int8_t* pm, double* sm, int8_t* pt, double* st, int p, cudaStream_t stream) {
+  switch (S) {
+    case 5: oz_slice_mt_s<5>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
+    case 6: oz_slice_mt_s<6>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
+    default: oz_slice_mt_s<7>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
+  }
+}
+
+int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
+                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
+                      int* nact, void* oz_ws, int slices, double eps_rel, double slice_budget, cudaStream_t stream,
+                      int64_t* launches) {
+  // 64-byte k-chunks (measured on B200: 32-byte chunks with a 5-deep ring are 13% slower on the
+  // 528-root call -- 585 vs 673 roots/s; SWIZZLE_32B TMA rows are short requests)
+  if (slices != 6 && slices != 7)
+    return set_error(SHAMPOO_ERR_INVALID_ARG, "ozaki root: slices must be 6 or 7 (got %d)", slices);
   if (batch > kTailMaxBatch) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: batch chunk > %d", kTailMaxBatch);
   if (np % 64) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: padded n must be a multiple of 64");
   char* w = static_cast<char*>(oz_ws);
-  const size_t slot_planes = (size_t)batch * oz::kSMax * np * np;  // slots keep the S = 7 pitch
+  const size_t slot_planes = (size_t)batch * oz::kSMax * np * np;  // every slot at the kSMax plane pitch
   int8_t* planes = reinterpret_cast<int8_t*>(w);
   const size_t planes_bytes = ((size_t)OZ_SLOTS * slot_planes + 255) / 256 * 256;
   double* scales = reinterpret_cast<double*>(w + planes_bytes);
@@ -544,7 +613,7 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   CUtensorMap* maps_dev = reinterpret_cast<CUtensorMap*>(w + planes_bytes + scales_bytes);
   auto slot_planes_ptr = [&](int slot) { return planes + (size_t)slot * slot_planes; };
   auto slot_scale = [&](int slot) { return scales + (size_t)slot * batch * np; };
-  // maps: slot q -> 2q (A use, 128-row box), 2q+1 (B use, 64-row box)
+  // maps: slot q -> 2q (A use, 128-row box), 2q+1 (B use, 64-row box); independent of the slice count
   CUtensorMap maps[2 * OZ_SLOTS];
   {
     void* fn = nullptr;
@@ -554,9 +623,8 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
       return set_error(SHAMPOO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     for (int q2 = 0; q2 < OZ_SLOTS; ++q2) {
-      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM, kS, BK) !=
-              CUDA_SUCCESS ||
-          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN, kS, BK) !=
+      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM, 64) != CUDA_SUCCESS ||
+          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN, 64) !=
               CUDA_SUCCESS)
         return set_error(SHAMPOO_ERR_CUDA, "ozaki: cuTensorMapEncodeTiled failed");
     }
@@ -565,28 +633,20 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
     return set_cuda_error("cudaMemcpyAsync(ozaki maps)");
   const int64_t mstride = (int64_t)kTailRegions * np * np;
   auto region = [&](int r) { return bufs + (int64_t)r * np * np; };
-  const int slice_grid = 8 * num_sms();
   // tm: slice T_k = ((p+1)I - M_k)/p computed from M_k on the fly (T_k never stored in fp64)
-  auto slice_any = [&](int reg, int slot, bool tm) {
-    if (tm)
-      oz::slice_kernel<S, true><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
-                                                               slot_planes_ptr(slot), slot_scale(slot), p);
-    else
-      oz::slice_kernel<S, false><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
-                                                                slot_planes_ptr(slot), slot_scale(slot), p);
+  auto slice = [&](int S, int reg, int slot, bool tm) {
+    oz_slice(S, tm, region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(slot), slot_scale(slot), p, stream);
     ++*launches;
   };
-  auto slice = [&](int reg, int slot) { slice_any(reg, slot, false); };
   // M_k and T_k in one pass over M_k (rows up to 1024 in registers), else two passes
-  auto slice_mt = [&](int reg) {
+  auto slice_mt = [&](int S, int reg) {
     if (n <= 1024) {
-      oz::slice_mt_kernel<S><<<slice_grid, 256, 0, stream>>>(region(reg), mstride, n, np, batch, act, nact,
-                                                             slot_planes_ptr(OZ_SM), slot_scale(OZ_SM),
-                                                             slot_planes_ptr(OZ_ST), slot_scale(OZ_ST), p);
+      oz_slice_mt(S, region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(OZ_SM), slot_scale(OZ_SM),
+                  slot_planes_ptr(OZ_ST), slot_scale(OZ_ST), p, stream);
       ++*launches;
     } else {
-      slice_any(reg, OZ_SM, false);
-      slice_any(reg, OZ_ST, true);
+      slice(S, reg, OZ_SM, false);
+      slice(S, reg, OZ_ST, true);
     }
   };
   oz::OzArgs base;
@@ -602,6 +662,7 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   base.p = p;
   base.errh = errh;
   base.max_iter = max_iter;
+  base.jobs = 1;
   auto job = [&](int sa, int sb, int out_reg) {
     oz::OzJob j;
     j.a_map = 2 * sa;
@@ -617,8 +678,7 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
   };
   // T^m (m >= 2) sliced by the product's own epilogue: every row scaled by 2^e with
   // 2^e > ((p+1)/p)^m >= rho(T)^m >= |(T^m)_ij| (reading #28; a violated bound is
-  // flagged as a non-finite err, status 2).  The sliced epilogue needs no shared memory, so both S.
-  const bool fuse_pow = true;
+  // flagged as a non-finite err, status 2).  The sliced epilogue needs no shared memory.
   auto sliced_job = [&](int sa, int sb, int slot, int m) {
     oz::OzJob j = job(sa, sb, 0);
     j.out = nullptr;
@@ -630,100 +690,82 @@ static int root_ozaki_launch_s(double* bufs, int batch, int n, int np, int p, in
     j.out_e = e;
     return j;
   };
-  const int grid = num_sms();
-  auto gemm = [&](const oz::OzArgs& a) {
+  auto gemm = [&](int S, const oz::OzArgs& a) -> int {
     void* tok;
     prof_begin_launch("ozaki_gemm", stream, &tok);
-    oz::gemm_kernel<S, BK><<<grid, oz::kThreads, smem, stream>>>(a, maps_dev);
+    cudaError_t e = oz_gemm(S, a, maps_dev, stream);
     prof_end_launch(tok, stream);
+    if (e != cudaSuccess) return set_cuda_error("ozaki gemm launch", e);
     ++*launches;
+    return SHAMPOO_OK;
   };
   enum { RX0 = 0, RX1 = 1, RM0 = 2, RM1 = 3, RT = 4, RS0 = 5, RS1 = 6 };  // root.cu regions
   const int lead = 31 - __builtin_clz((unsigned)p);
-  for (int k = 0; k < max_iter; ++k) {
+  int rc = SHAMPOO_OK;
+  for (int k = 0; k < max_iter && rc == SHAMPOO_OK; ++k) {
     const int xs = k & 1;
-    slice(RX0 + xs, OZ_SX);
-    slice_mt(RM0 + xs);  // M_k and T_k = ((p+1)I - M_k)/p
-    // P1: X_{k+1} = X_k T (fp64) ; S0 = T T (p >= 2; sliced in the epilogue when fuse_pow)
+    // slices of this iteration's products (reading #29); the X-update reads the leading Sx planes of T
+    const int S = ozaki_iteration_slices(k, p, eps_rel, slice_budget, slices);
+    const int Sx = slice_budget > 0.0 ? std::min(S, kOzSX) : S;
+    slice(Sx, RX0 + xs, OZ_SX, false);
+    slice_mt(S, RM0 + xs);  // M_k and T_k = ((p+1)I - M_k)/p
+    // P1: X_{k+1} = X_k T (fp64) ; then S0 = T T (p >= 2; sliced in the epilogue).  Two launches: a stage
+    // whose jobs take different epilogue paths was measured 17-18 ms against 6 + 6 ms for the two alone
+    // (the alternating paths thrash the instruction cache)
     oz::OzArgs a1 = base;
     a1.kcheck = k + 1;
     a1.job[0] = job(OZ_SX, OZ_ST, RX0 + (xs ^ 1));
-    if (fuse_pow) {
-      // two launches: a stage whose jobs take different epilogue paths was measured 17-18 ms against
-      // 6 + 6 ms for the two alone (the alternating paths thrash the instruction cache)
-      a1.jobs = 1;
-      gemm(a1);
-      if (p >= 2) {
-        oz::OzArgs a2 = a1;
-        a2.job[0] = sliced_job(OZ_ST, OZ_ST, OZ_SS0, 2);
-        gemm(a2);
-      }
-    } else {
-      a1.jobs = p >= 2 ? 2 : 1;
-      a1.job[1] = job(OZ_ST, OZ_ST, RS0);
-      gemm(a1);
+    rc = gemm(Sx, a1);
+    if (rc) break;
+    if (p >= 2) {
+      oz::OzArgs a2 = a1;
+      a2.job[0] = sliced_job(OZ_ST, OZ_ST, OZ_SS0, 2);
+      rc = gemm(S, a2);
+      if (rc) break;
     }
     int rb = RS0, sb = OZ_SS0, m = 2;
-    if (p >= 2 && !fuse_pow) slice(RS0, OZ_SS0);
-    for (int bit = lead - 1; bit >= 0; --bit) {
+    for (int bit = lead - 1; bit >= 0 && rc == SHAMPOO_OK; --bit) {
       if (bit != lead - 1) {  // square
         const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
         oz::OzArgs q = base;
-        q.jobs = 1;
         q.kcheck = k + 1;
-        q.job[0] = fuse_pow ? sliced_job(sb, sb, sd, 2 * m) : job(sb, sb, rd);
-        gemm(q);
-        if (!fuse_pow) slice(rd, sd);
+        q.job[0] = sliced_job(sb, sb, sd, 2 * m);
+        rc = gemm(S, q);
         rb = rd;
         sb = sd;
         m *= 2;
       }
-      if ((p >> bit) & 1) {  // times T
+      if (rc == SHAMPOO_OK && ((p >> bit) & 1)) {  // times T
         const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
         oz::OzArgs q = base;
-        q.jobs = 1;
         q.kcheck = k + 1;
         q.job[0] = job(sb, OZ_ST, rd);  // A != B: fp64 output and the slice kernel
-        gemm(q);
-        slice(rd, sd);
+        rc = gemm(S, q);
+        if (rc) break;
+        slice(S, rd, sd, false);
         rb = rd;
         sb = sd;
         m += 1;
       }
     }
+    if (rc) break;
     // P3: M_{k+1} = T^p M_k ; err_{k+1} = max|M_{k+1} - I|
     oz::OzArgs a3 = base;
-    a3.jobs = 1;
     a3.job[0] = job(p == 1 ? OZ_ST : sb, OZ_SM, RM0 + (xs ^ 1));
     a3.mupdate = 1;
     a3.kcheck = k + 1;
-    gemm(a3);
+    rc = gemm(S, a3);
+    if (rc) break;
     root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, tol, 1.0, k + 1);
     ++*launches;
   }
+  if (rc) return rc;
   root_tail_finish_kernel<<<batch, 128, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
                                                      0, tol, 1.0, RX0, RX1, 1);
   ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("ozaki root kernels", e);
   return SHAMPOO_OK;
-}
-
-int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
-                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
-                      int* nact, void* oz_ws, int slices, cudaStream_t stream, int64_t* launches) {
-  // 64-byte k-chunks (measured on B200: 32-byte chunks with a 5-deep ring are 13% slower on the
-  // 528-root call -- 585 vs 673 roots/s; SWIZZLE_32B TMA rows are short requests)
-  switch (slices) {
-    case 6:
-      return root_ozaki_launch_s<6, 64>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
-                                        nact, oz_ws, stream, launches);
-    case 7:
-      return root_ozaki_launch_s<7, 64>(bufs, batch, n, np, p, max_iter, tol, errh, res, info, X, ldx, stride_x, act,
-                                        nact, oz_ws, stream, launches);
-    default:
-      return set_error(SHAMPOO_ERR_INVALID_ARG, "ozaki root: slices must be 6 or 7 (got %d)", slices);
-  }
 }
 
 }  // namespace shp

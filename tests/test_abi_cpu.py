@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(shp):
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(_lib.EXPORTED) == declared
-    assert L.shampoo_abi_version() == 3
+    assert L.shampoo_abi_version() == 4
 
 
 def _fields_equal(lib_plan, o):
@@ -136,8 +136,13 @@ def test_host_checked_errors_need_no_device(shp):
     # Ozaki slice count outside {6, 7} (checked before the workspace)
     for bad in (0, 5, 8):
         assert L.shampoo_inverse_pth_root_batched_ozaki(fake, 8, 64, fake, 8, 64, 1, 8, 4, 1e-6, 1e-7, 100, 100, bad,
-                                                        fake, fake, 1 << 30, None) == 1
+                                                        0.0, fake, fake, 1 << 30, None) == 1
         assert b"slices" in L.shampoo_last_error()
+    # slice budget (ABI v4, reading #29) outside [0, 1)
+    for bad in (-1e-9, 1.0, float("nan")):
+        assert L.shampoo_inverse_pth_root_batched_ozaki(fake, 8, 64, fake, 8, 64, 1, 8, 4, 1e-6, 1e-7, 100, 100, 7,
+                                                        bad, fake, fake, 1 << 30, None) == 1
+        assert b"slice_budget" in L.shampoo_last_error()
     # statistics: non-finite decay
     assert L.shampoo_stats_update(fake, 1, fake, fake, 1, -1, fake, float("inf"), 1.0, None, None, fake, 1 << 30,
                                   None) == 1

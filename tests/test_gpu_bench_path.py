@@ -154,8 +154,14 @@ def test_bench_sampled_precondition_vs_oracle(run):
         Pg = run["Pd"][b.tensor_id][b.row0:b.row0 + b.rows, b.col0:b.col0 + b.cols].cpu().numpy()
         Po = run["Ps_o"][bi]
         err = rel(Pg, Po)
-        print(f"block {bi}: P rel err {err:.3e}")
-        assert err < 2e-5, (bi, err)
+        two_sided = b.p_left > 0 and b.p_right > 0
+        print(f"block {bi} ({'two' if two_sided else 'one'}-sided): P rel err {err:.3e}")
+        # north star: 1e-3.  Two-sided blocks are held to 2e-5 (3xTF32 products of fp32 roots).  The one-sided
+        # vocabulary blocks are limited by the fp32 ROOT itself: the rows of G_b lie in the range of R_b = G_b^T G_b
+        # while R_b^{-1/2}'s largest eigenvalues ((eps lambda)^{-1/2}, kappa^{1/2} = 1e3 above its range part) sit in
+        # R_b's null space, so P = G_b R_b^{-1/2} cancels them exactly and the fp32 rounding of the root (2^-24
+        # relative) reaches P amplified ~1e3x: ~1e-4 (measured 1.3e-4 on B200, r02b)
+        assert err < (2e-5 if two_sided else 1e-3), (bi, err)
         assert abs(run["sc"][bi] - run["sc_o"][bi]) <= 1e-5 * run["sc_o"][bi], bi
 
 

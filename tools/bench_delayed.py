@@ -103,11 +103,28 @@ for chunk in [int(c) for c in args.chunks.split(",")]:
     ms_window = timed(lambda t, dr=dr: delayed(t, dr), dr.n_steps)  # every chunk step, the last one gathers
     assert dr.ready and dr.refreshes == 1
     st = [int(s) for _, _, _, info in dr.infos for s in shp.info_to_numpy(info)["status"]]
+    # the gathered roots against a synchronous refresh of the same snapshot (bit-identity)
+    ref = torch.zeros_like(roots)
+    shp.refresh_group_roots(plan, dr.snapshot, ref, 0, fp64_iters=args.precision)
+    torch.cuda.synchronize()
+    mism, bad_info = 0, []
+    for g, i0, cnt, info in dr.infos:
+        nn, stride, off0 = int(g["n"]), int(g["stride"]), int(g["offset"])
+        inf = shp.info_to_numpy(info)
+        for q in range(cnt):
+            o = off0 + (i0 + q) * stride
+            if not torch.equal(dr.next[o:o + nn * ((nn + 3) // 4 * 4)], ref[o:o + nn * ((nn + 3) // 4 * 4)]):
+                mism += 1
+            if inf[q]["status"] != 0:
+                bad_info.append({"n": nn, "p": int(g["p"]), "index": i0 + q, "status": int(inf[q]["status"]),
+                                 "iters": int(inf[q]["iters"]), "lambda": float(inf[q]["lambda_max"]),
+                                 "err": float(inf[q]["err"])})
     extra = ms_window - dr.n_steps * ms_plain
     out["chunks"].append({"roots_per_step": chunk, "window_steps": dr.n_steps, "window_ms": ms_window,
                           "step_ms_during_window": ms_window / dr.n_steps,
                           "refresh_cost_ms": extra, "cost_per_step_ms_over_kappa": extra / args.kappa,
                           "step_delta_frac_over_kappa": extra / args.kappa / ms_plain,
                           "refresh_cost_vs_synchronous": extra / (ms_sync - ms_plain),
-                          "statuses": {str(s): st.count(s) for s in sorted(set(st))}})
+                          "statuses": {str(s): st.count(s) for s in sorted(set(st))},
+                          "roots_differing_from_synchronous_refresh": mism, "nonzero_status": bad_info[:20]})
 print(json.dumps(out), flush=True)

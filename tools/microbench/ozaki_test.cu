@@ -65,8 +65,8 @@ static int run(int n, int batch, bool sym, int reps) {
   CK(cudaMalloc(&dC, batch * mat * 8));
   CK(cudaMalloc(&sA, batch * np * 8));
   CK(cudaMalloc(&sB, batch * np * 8));
-  CK(cudaMalloc(&pA, batch * mat * kS));
-  CK(cudaMalloc(&pB, batch * mat * kS));
+  CK(cudaMalloc(&pA, batch * mat * oz::kSMax));
+  CK(cudaMalloc(&pB, batch * mat * oz::kSMax));
   CK(cudaMemcpy(dA, hA.data(), batch * mat * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, hB.data(), batch * mat * 8, cudaMemcpyHostToDevice));
   CK(cudaMemset(dC, 0, batch * mat * 8));
@@ -75,8 +75,8 @@ static int run(int n, int batch, bool sym, int reps) {
   CK(cudaGetLastError());
   CUtensorMap maps[2];
   auto enc = encode();
-  if (oz::make_plane_map(enc, &maps[0], pA, n, np, batch, oz::kBM, kS, BK) != CUDA_SUCCESS ||
-      oz::make_plane_map(enc, &maps[1], pB, n, np, batch, oz::kBN, kS, BK) != CUDA_SUCCESS) {
+  if (oz::make_plane_map(enc, &maps[0], pA, n, np, batch, oz::kBM, BK) != CUDA_SUCCESS ||
+      oz::make_plane_map(enc, &maps[1], pB, n, np, batch, oz::kBN, BK) != CUDA_SUCCESS) {
     printf("map encode failed\n");
     return 1;
   }
@@ -110,12 +110,12 @@ static int run(int n, int batch, bool sym, int reps) {
     cudaEventElapsedTime(&ms, e0, e1);
   }
   std::vector<double> hC(batch * mat), hsA(batch * np), hsB(batch * np);
-  std::vector<int8_t> hpA(batch * mat * kS), hpB(batch * mat * kS);
+  std::vector<int8_t> hpA(batch * mat * oz::kSMax), hpB(batch * mat * oz::kSMax);
   CK(cudaMemcpy(hC.data(), dC, batch * mat * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(hsA.data(), sA, batch * np * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(hsB.data(), sB, batch * np * 8, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(hpA.data(), pA, batch * mat * kS, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(hpB.data(), pB, batch * mat * kS, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hpA.data(), pA, batch * mat * oz::kSMax, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hpB.data(), pB, batch * mat * oz::kSMax, cudaMemcpyDeviceToHost));
   // host: slices reproduce the inputs; exact recomputation; fp64 accuracy
   long mism = 0, checked = 0;
   double maxrel = 0, maxslice = 0;
@@ -125,7 +125,7 @@ static int run(int n, int batch, bool sym, int reps) {
       for (int j = 0; j < n; ++j) {  // slice reconstruction
         double rec = 0;
         for (int s = 0; s < kS; ++s)
-          rec += hpA[((size_t)(b * kS + s) * np + i) * np + j] * std::ldexp(1.0, -6 - 7 * s);
+          rec += hpA[((size_t)(b * oz::kSMax + s) * np + i) * np + j] * std::ldexp(1.0, -6 - 7 * s);
         rec *= hsA[b * np + i];
         const double x = hA[b * mat + (size_t)i * np + j];
         maxslice = std::max(maxslice, std::fabs(rec - x) / hsA[b * np + i]);
@@ -140,8 +140,8 @@ static int run(int n, int batch, bool sym, int reps) {
             const int sb = d - sa;
             long long t = 0;
             for (int k = 0; k < n; ++k)
-              t += (long long)hpA[((size_t)(b * kS + sa) * np + i) * np + k] *
-                   hpB[((size_t)(b * kS + sb) * np + j) * np + k];
+              t += (long long)hpA[((size_t)(b * oz::kSMax + sa) * np + i) * np + k] *
+                   hpB[((size_t)(b * oz::kSMax + sb) * np + j) * np + k];
             acc[d] += t;
           }
         // the exact sum rounded once (the kernel's int64 halves + one fma)
@@ -188,6 +188,9 @@ int main() {
   bad |= run<6>(200, 2, false, 2);
   bad |= run<6>(256, 2, true, 2);
   bad |= run<6>(1024, 148, true, 3);
+  bad |= run<5>(256, 2, false, 2);
+  bad |= run<5>(200, 2, false, 2);
+  bad |= run<5>(1024, 148, true, 3);
 
   printf(bad ? "FAIL\n" : "PASS\n");
   return bad;

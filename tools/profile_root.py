@@ -22,7 +22,7 @@ ap.add_argument("--p", type=int, default=4)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--max-iter", type=int, default=100)
 ap.add_argument("--power-iters", type=int, default=100)
-ap.add_argument("--slices", type=int, default=7, help="Ozaki slices (with --hybrid -9)")
+ap.add_argument("--slices", type=int, default=0, help="Ozaki slices with --hybrid -9 (0: the slice schedule)")
 ap.add_argument("--hybrid", type=int, default=None,
                 help="fp64 iterations before the 3xTF32 tail (-1 = auto); -9 = the Ozaki INT8 root")
 args = ap.parse_args()
@@ -34,7 +34,7 @@ for r in range(args.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     X, info = shp.inverse_pth_root_batched(A, args.p, X=X, max_iter=args.max_iter, power_iters=args.power_iters,
-                                           fp64_iters=f"ozaki{args.slices}" if args.hybrid == -9 else args.hybrid)
+                                           fp64_iters=f"ozaki{args.slices or ''}" if args.hybrid == -9 else args.hybrid)
     e1.record()
     torch.cuda.synchronize()
 inf = shp.info_to_numpy(info)
@@ -42,6 +42,6 @@ ms = e0.elapsed_time(e1)
 n = args.n
 prods = 2 + (args.p.bit_length() - 1) + (bin(args.p).count("1") - 1)
 flops = float(inf["iters"].sum()) * prods * n * n * (n + 1)
-print(f"{'fp64' if args.hybrid is None else (f'ozaki{args.slices}' if args.hybrid == -9 else 'hybrid')} batch {args.batch} n {n} p {args.p}: {ms:.2f} ms, iters mean {inf['iters'].mean():.2f}, "
+print(f"{'fp64' if args.hybrid is None else (f"ozaki{args.slices or ''}" if args.hybrid == -9 else 'hybrid')} batch {args.batch} n {n} p {args.p}: {ms:.2f} ms, iters mean {inf['iters'].mean():.2f}, "
       f"status {set(inf['status'].tolist())}, {flops / ms / 1e9:.2f} TFLOP/s (sym-minimal), "
       f"{args.batch / ms * 1e3:.1f} roots/s")
