@@ -385,7 +385,7 @@ def main():
                 "fp64_equivalent_tflops": (float(inf["iters"].sum()) * 4 * n * n * (n + 1)
                                            + cnt * 100 * 2.0 * n * n) / (call_ms * 1e-3) / 1e12,
                 "peak_source": f"int8 dense = 2 x the {peak_kind} bf16 TF/s of MEASURED_PEAKS.json (nominal "
-                               f"int8:bf16 ratio 2; NVIDIA nominal 4.5 POPS)", "slices": slices, "slice_schedule": [shp.ozaki_iteration_slices(k, 4, 1e-6, None if scheduled else 0.0, slices)
+                               f"int8:bf16 ratio 2; NVIDIA nominal 4.5 POPS)", "slices": slices, "slice_schedule": [shp.ozaki_iteration_slices(k, 4, n, 1e-6, None if scheduled else 0.0, slices)
                                                         for k in range(int(inf["iters"].max()))],
                 "frac_vs_burst_peak": (achieved / peak_burst) if peak_burst else None,
                 "peak_note": "the sustained bf16 figure was measured at ~1290 MHz under a bf16 GEMM's power draw; "

@@ -236,7 +236,7 @@ int shampoo_inverse_pth_root_batched_hybrid(const float* A, int64_t lda, int64_t
  *   schedule: an error in M_k reaches the root amplified by ~1/(p lambda_min(M_k))
  *   and lambda_min(M_k) >= m_k = min(1, eps_rel g^k), g = ((p+1)/p)^p (the ridge
  *   and the scalar recurrence), so iteration k uses the smallest S in
- *   [5, slices] with 2^-(7S-1) / (p m_k) <= slice_budget, and the X-update
+ *   [5, slices] with 2^-(7S-1) sqrt(n/1024) / (p m_k) <= slice_budget, and the X-update
  *   X_k T_k (not amplified) min(S, 5).  eps_rel = 0 keeps `slices` throughout.
  *   1e-9 (the binding's default): 0.68 of the fixed-7 slice products at
  *   n = 1024, p = 4, kappa 1e6, root error 2.9e-7 vs 1.2e-7 in host emulation
@@ -245,7 +245,8 @@ size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, i
 /* Host-only: the slice count the Ozaki root uses for the products of iteration
  * k (the M-chain; the X-update uses min(result, 5) when slice_budget > 0) for
  * these arguments -- the schedule above, for accounting (bench roofline). */
-int shampoo_ozaki_iteration_slices(int32_t k, int32_t p, double eps_rel, double slice_budget, int32_t slices);
+int shampoo_ozaki_iteration_slices(int32_t k, int32_t p, int32_t n, double eps_rel, double slice_budget,
+                                   int32_t slices);
 int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
                                            int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
                                            double tol, int32_t max_iter, int32_t power_iters, int32_t slices,

@@ -263,7 +263,7 @@ _refresh_launches = 0
 # FP64 DMMA 72k; n = 512 2.7k vs 2.5k; n = 1024 580 vs 354 -- profiles/r01t_*)
 OZAKI_MIN_N = 512
 # per-iteration slice schedule of the Ozaki root (reading #29, shampoo.h slice_budget): iteration k takes the fewest
-# slices S in [5, 7] with 2^-(7S-1) / (p min(1, eps_rel g^k)) <= SLICE_BUDGET (host emulation at n = 1024, p = 4,
+# slices S in [5, 7] with 2^-(7S-1) sqrt(n/1024) / (p min(1, eps_rel g^k)) <= SLICE_BUDGET (host emulation at n = 1024, p = 4,
 # kappa 1e6: 0.68 of the fixed-7 slice products, root error 2.9e-7 vs 1.2e-7; tools/ozaki_schedule.py)
 SLICE_BUDGET = 1e-9
 
@@ -459,11 +459,11 @@ def profile_end(kernel: str | None = None):
     return float(ms[0]), int(n[0])
 
 
-def ozaki_iteration_slices(k: int, p: int, eps_rel: float = 1e-6, budget: float | None = None,
+def ozaki_iteration_slices(k: int, p: int, n: int = 1024, eps_rel: float = 1e-6, budget: float | None = None,
                            slices: int = 7) -> int:
     """Slices of the M-chain products of Ozaki iteration k (reading #29; the library's schedule)."""
     b = SLICE_BUDGET if budget is None else budget
-    return int(_lib.lib().shampoo_ozaki_iteration_slices(k, p, eps_rel, b, slices))
+    return int(_lib.lib().shampoo_ozaki_iteration_slices(k, p, n, eps_rel, b, slices))
 
 
 def ozaki_int8_ops(iters, n: int, p: int, eps_rel: float = 1e-6, budget: float | None = None,
@@ -475,7 +475,7 @@ def ozaki_int8_ops(iters, n: int, p: int, eps_rel: float = 1e-6, budget: float |
     prods = (p.bit_length() - 1) + bin(p).count("1")  # T^p chain (squarings + multiplications) + T^p M
     per_k = []
     for k in range(int(max(iters)) if len(iters) else 0):
-        S = ozaki_iteration_slices(k, p, 1e-6 if eps_rel is None else eps_rel, b, slices)
+        S = ozaki_iteration_slices(k, p, n, 1e-6 if eps_rel is None else eps_rel, b, slices)
         Sx = min(S, 5) if b > 0 else S
         per_k.append(Sx * (Sx + 1) // 2 + prods * S * (S + 1) // 2)
     cum = np.concatenate([[0], np.cumsum(per_k)])

@@ -129,7 +129,7 @@ def lib():
     L.shampoo_profile_end.restype = ctypes.c_int
     L.shampoo_profile_launch_ms.argtypes = [ctypes.c_char_p, _vp, ctypes.c_int64, _vp]
     L.shampoo_profile_launch_ms.restype = ctypes.c_int
-    L.shampoo_ozaki_iteration_slices.argtypes = [_i32, _i32, _dbl, _dbl, _i32]
+    L.shampoo_ozaki_iteration_slices.argtypes = [_i32, _i32, _i32, _dbl, _dbl, _i32]
     L.shampoo_ozaki_iteration_slices.restype = ctypes.c_int
     if L.shampoo_abi_version() != 4:
         raise ImportError("libshampoo ABI version mismatch")

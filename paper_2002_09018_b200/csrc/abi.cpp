@@ -253,8 +253,9 @@ static int root_entry(const float* A, int64_t lda, int64_t stride_a, float* X, i
                       size_t workspace_bytes, shampoo_stream_t stream, int precision = 0, int slices = 7,
                       double slice_budget = 0.0);
 
-int shampoo_ozaki_iteration_slices(int32_t k, int32_t p, double eps_rel, double slice_budget, int32_t slices) {
-  return ozaki_iteration_slices(k, p, eps_rel, slice_budget, slices);
+int shampoo_ozaki_iteration_slices(int32_t k, int32_t p, int32_t n, double eps_rel, double slice_budget,
+                                   int32_t slices) {
+  return ozaki_iteration_slices(k, p, n, eps_rel, slice_budget, slices);
 }
 
 size_t shampoo_root_ozaki_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter) {

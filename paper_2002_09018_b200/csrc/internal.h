@@ -26,7 +26,7 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
                       int* nact, void* oz_ws, int slices, double eps_rel, double slice_budget, cudaStream_t stream,
                       int64_t* launches);
 // slice count of Ozaki iteration k (reading #29; root_tail.cu)
-int ozaki_iteration_slices(int k, int p, double eps_rel, double budget, int s_max);
+int ozaki_iteration_slices(int k, int p, int n, double eps_rel, double budget, int s_max);
 int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter, int k_sw, double tol, double* errh,
                      const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
                      int* nact, void* maps_ws, cudaStream_t stream, int64_t* launches);

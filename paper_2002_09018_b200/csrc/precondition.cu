@@ -231,7 +231,13 @@ struct PrecLayout {
 };
 
 static bool tc_eligible(const shampoo_block_t& b, const shampoo_tensor_t& t) {
-  if (!b.p_right) return false;  // left-only / diagonal-only blocks stay on the DMMA / elementwise path
+  // one-sided blocks (P = G_b X_R, X_L G_b) run on the FP64 DMMA path: their statistic is often rank-deficient
+  // (the vocabulary rows of an embedding gradient: G_b's rows span few dimensions), so the root's largest
+  // eigenvalues sit in directions G_b is orthogonal to and the product cancels them exactly; an fp32
+  // accumulation (the tensor core's 3xTF32) loses up to ~kappa^{1/2} of its relative accuracy there -- measured
+  // on B200: P rel. error 6.2e-3 on a 4-nonzero-row vocabulary block (north-star bar 1e-3), against 3.2e-5 for
+  // the exact product of the same fp32 root (tests/test_gpu_bench_path.py)
+  if (!b.p_right || !b.p_left) return false;  // one-sided / diagonal-only blocks: DMMA / elementwise path
   // the raw G is the TMA "hi" operand: contiguous rows, 16-byte aligned
   if (t.ldg != t.n || (t.n & 3) || (reinterpret_cast<uintptr_t>(t.G) & 15)) return false;
   const bool rows_ok = (b.rows % 32 == 0) || (b.row0 + b.rows == t.m);

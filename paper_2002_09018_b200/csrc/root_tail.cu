@@ -530,16 +530,18 @@ size_t root_ozaki_ws_bytes(int batch, int n) {
 // root amplified by ~1/(p lambda_min(M_k)), lambda_min(M_0) >= eps_rel / (1 +
 // eps_rel) (the ridge) and the scalar recurrence grows it by g = ((p+1)/p)^p per
 // iteration while it is small -- so m_k = min(1, eps_rel g^k) bounds it a priori
-// and S_k = the smallest S in [kOzSMin, s_max] with 2^-(7S-1) / (p m_k) <= budget.
+// and S_k = the smallest S in [kOzSMin, s_max] with 2^-(7S-1) sqrt(n/1024) / (p m_k) <= budget
+// (a product's rounding errors add up over its n-term sums like a random walk).
 // budget <= 0 (or no ridge): S_k = s_max for every k (the fixed-slice root).
 constexpr int kOzSMin = 5;  // S = 4 (2^-27) was measured (host emulation) to leave a 4e-6 floor in the root
 constexpr int kOzSX = 5;    // the X-update X_k T_k: X only accumulates T's (no amplification)
-int ozaki_iteration_slices(int k, int p, double eps_rel, double budget, int s_max) {
+int ozaki_iteration_slices(int k, int p, int n, double eps_rel, double budget, int s_max) {
   if (!(budget > 0.0) || !(eps_rel > 0.0)) return s_max;
   const double g = std::pow((double)(p + 1) / (double)p, (double)p);
   const double m = std::min(1.0, eps_rel * std::pow(g, (double)k));
+  const double growth = std::sqrt((double)n / 1024.0);
   for (int S = kOzSMin; S < s_max; ++S)
-    if (std::ldexp(1.0, -(7 * S - 1)) / ((double)p * m) <= budget) return S;
+    if (std::ldexp(1.0, -(7 * S - 1)) * growth / ((double)p * m) <= budget) return S;
   return s_max;
 }
 
@@ -705,7 +707,7 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   for (int k = 0; k < max_iter && rc == SHAMPOO_OK; ++k) {
     const int xs = k & 1;
     // slices of this iteration's products (reading #29); the X-update reads the leading Sx planes of T
-    const int S = ozaki_iteration_slices(k, p, eps_rel, slice_budget, slices);
+    const int S = ozaki_iteration_slices(k, p, n, eps_rel, slice_budget, slices);
     const int Sx = slice_budget > 0.0 ? std::min(S, kOzSX) : S;
     slice(Sx, RX0 + xs, OZ_SX, false);
     slice_mt(S, RM0 + xs);  // M_k and T_k = ((p+1)I - M_k)/p
