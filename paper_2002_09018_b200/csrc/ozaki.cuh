@@ -51,6 +51,12 @@ struct Cfg {
   static constexpr int kStages = (225 * 1024) / kStageBytes;   // as many as fit: 2 / 5 (S = 7), 3 / 6 (S = 6)
 };
 constexpr int kThreads = 192;
+// Bound probes for tools/microbench/ozaki_test.cu only (the library builds with 0):
+// 1 = no MMAs (TMA data movement + barriers + epilogue), 2 = no TMA loads (MMAs on stale tiles),
+// 3 = no accumulator drain (the epilogue releases TMEM at once and stores zeros)
+#ifndef OZ_PROBE
+#define OZ_PROBE 0
+#endif
 constexpr uint32_t kTmemCols = 512;         // S accumulators x 64 columns (448 used for S = 7)
 
 // K-major tile of BK-byte rows, swizzled to match the TMA map (SWIZZLE_32B:
@@ -511,6 +517,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int g = 0; g < kGroups; ++g) {
             uint64_t* fb = full + stage * kGroups + g;
+#if OZ_PROBE == 2
+            tc::mbar_arrive(fb);
+            continue;
+#endif
             tc::mbar_arrive_expect_tx(fb, grp_bytes<S, BK>(g));
 #pragma unroll
             for (int s = 0; s < kS; ++s) {
@@ -562,7 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               const uint64_t db = dB0 + (uint64_t)((tb * kBPlane) >> 4) + adv;
               // sa == 0 initialises every diagonal at the first k-step (it spans d = 0..6)
               const uint32_t acc = (kc == 0 && k == 0 && sa == 0) ? 0u : 1u;
-              if (lane == 0) umma_i8(tmem_base + (uint32_t)((sa + tb) * kBN), da, db, idesc_i8(kBM, kBN * cnt), acc);
+              if (OZ_PROBE != 1 && lane == 0)
+                umma_i8(tmem_base + (uint32_t)((sa + tb) * kBN), da, db, idesc_i8(kBM, kBN * cnt), acc);
             }
           }
         }
@@ -604,6 +615,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // on B200, fp64 instructions issued while tcgen05 MMAs run stall ~100x
       // ("math pipe throttle"), so phase 2 below uses integer arithmetic only.
       double v[kBN];
+#if OZ_PROBE == 3
+#pragma unroll
+      for (int e = 0; e < kBN; ++e) v[e] = 0.0;
+      if (false)
+#endif
 #pragma unroll
       for (int c0 = 0; c0 < kBN; c0 += 8) {
         uint32_t r[kS][8];

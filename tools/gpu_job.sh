@@ -1,15 +1,8 @@
 #!/bin/bash
-# One gpurun session (round 2).  gpurun --timeout 2700 -- bash tools/gpu_job.sh r02c
+# One gpurun session (round 2).  gpurun --timeout 2700 -- bash tools/gpu_job.sh <tag>
 T=${1:-r02x}
 O=gpurun_out/$T
 mkdir -p $O
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_2002_09018_b200/csrc \
-  -o /tmp/ozaki_test tools/microbench/ozaki_test.cu -lcuda > $O/ozaki_test_build.log 2>&1 && \
-  timeout 600 /tmp/ozaki_test > $O/ozaki_test.log 2>&1; echo "exit $?" >> $O/ozaki_test.log
-timeout 1200 python -m pytest tests/test_gpu_ozaki.py tests/test_gpu_bench_path.py tests/test_gpu_schedule.py tests/test_gpu_guard.py -q -rA -s > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_n1.json 2> $O/bench_n1.err
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --root-precision auto7 > $O/bench_n1_auto7.json 2> $O/bench_n1_auto7.err
-timeout 900 python tools/bench_delayed.py --chunks 32,16 > $O/delayed.json 2> $O/delayed.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_root528.csv \
-  python tools/profile_root.py --batch 528 --hybrid -9 --reps 1 > $O/launches_root528.log 2>&1
+for P in 0 1 2 3; do timeout 300 tools/microbench/bin/oz_probe$P > $O/oz_probe$P.log 2>&1; done
+timeout 900 python -m pytest tests/test_gpu_bench_path.py -q -rA -s > $O/pytest_bench_path.log 2>&1; echo "pytest exit $?" >> $O/pytest_bench_path.log
 echo done > $O/DONE
