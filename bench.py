@@ -108,6 +108,10 @@ def parse():
                          "products, roots ~3e-5 from the fp64 oracle, reading #27); "
                          "hybrid: FP64 DMMA then a 3xTF32 tcgen05 tail (§6.3b)")
     ap.add_argument("--hybrid", action="store_true", help="alias of --root-precision hybrid")
+    ap.add_argument("--shard", default="layers", choices=["layers", "roots"],
+                    help="N > 1: layers -- whole tensors per rank (their statistics, roots and P; one all-gather of P "
+                         "per step, reading #30); roots -- every root LPT-assigned on its own, the roots all-gathered "
+                         "and every rank preconditioning every block")
     ap.add_argument("--gather", default="allgather", choices=["overlapped", "allgather"],
                     help="N > 1: one all_gather_into_tensor after all roots (default), or per-group owner broadcasts "
                          "overlapping the next group's roots (measured equal at N = 2, 4: DESIGN §8)")
@@ -236,7 +240,8 @@ def main():
     names_shapes = synth.transformer_big_shapes()
     shapes = [s for _, s in names_shapes]
     B = args.block_size
-    plan = shp.make_plan(shapes, B, args.max_precond_dim, world)
+    layers = args.shard == "layers"
+    plan = shp.make_plan(shapes, B, args.max_precond_dim, world, owners="tensor" if layers else "root")
     n_p4 = int(sum((plan.blocks["p_left"] == 4).sum() + (plan.blocks["p_right"] == 4).sum() for _ in [0]))
     # gradients (device), vocab tensors row-sparse (Zipf ids), others low-rank + noise
     Gs = []
@@ -247,17 +252,31 @@ def main():
         else:
             Gs.append(synth.lowrank_gradient_device(m, n, seed, dev))
     Ds = [torch.zeros_like(G) for G in Gs]
-    Ps = [torch.zeros_like(G) for G in Gs]
+    nb = plan.n_blocks
+    if layers:
+        # whole tensors per rank: statistics, D, graft numerator, roots and P of this rank's tensors only; every
+        # P (and graft scale) in one flat buffer of equal rank segments -> one all-gather per step
+        ls = sdist.LayerShards(plan, world)
+        mine = ls.sub[rank]
+        flatP = torch.zeros(ls.numel, dtype=torch.float32, device=dev)
+        Ps = ls.p_views(flatP)
+        gnum = torch.zeros(max(1, mine.n_blocks), dtype=torch.float64, device=dev)
+        gscale = ls.scales_of(flatP, rank)
+        stats_plan, only = mine, -1
+        seg = slice(rank * plan.segment_elems, (rank + 1) * plan.segment_elems)
+    else:
+        Ps = [torch.zeros_like(G) for G in Gs]
+        gnum = torch.zeros(nb, dtype=torch.float64, device=dev)
+        gscale = torch.zeros(nb, dtype=torch.float32, device=dev)
+        stats_plan, only = plan, (rank if world > 1 else -1)
+        seg = slice(0, plan.stats_elems)
     table = shp.TensorTable(Gs, Ds, Ps)
     stats = torch.zeros(plan.stats_elems, dtype=torch.float32, device=dev)
     roots = torch.zeros_like(stats)
     roots_lo = torch.zeros_like(stats)
-    nb = plan.n_blocks
-    gnum = torch.zeros(nb, dtype=torch.float64, device=dev)
-    gscale = torch.zeros(nb, dtype=torch.float32, device=dev)
     # statistics accumulated over 8 steps before the timed refreshes (config 3 recipe)
     for _ in range(8):
-        shp.stats_update(table, plan, stats, 1.0, 1.0, rank if world > 1 else -1, gnum)
+        shp.stats_update(table, stats_plan, stats, 1.0, 1.0, only, gnum)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -269,13 +288,13 @@ def main():
             before_stats()
         if ev:
             ev[0].record(stream)
-        shp.stats_update(tbl, plan, stats, 1.0, 1.0, rank if world > 1 else -1, gnum)
+        shp.stats_update(tbl, stats_plan, stats, 1.0, 1.0, only, gnum)
         if after_stats:
             after_stats()
         launches[0] += shp.last_launch_count()
         if ev:
             ev[1].record(stream)
-        if world > 1 and args.gather == "overlapped":
+        if world > 1 and args.gather == "overlapped" and not layers:
             # each group's roots go out (NCCL broadcasts from their owners) while the next group computes
             infos, nl = sdist.refresh_gather_overlapped(plan, stats, roots, rank, world, tol=args.tol,
                                                         fp64_iters=ROOT_MODE[args.root_precision])
@@ -288,17 +307,23 @@ def main():
             launches[0] += shp.last_refresh_launch_count()
             if ev:
                 ev[2].record(stream)
-            sdist.all_gather_roots(plan, roots, rank, world)
-        shp.tf32_split(roots, roots_lo)  # once per refresh: the roots' TF32 remainder for the tensor cores
+            if not layers:
+                sdist.all_gather_roots(plan, roots, rank, world)
+        # once per refresh: the roots' TF32 remainder for the tensor cores (layers: this rank's segment only)
+        shp.tf32_split(roots[seg], roots_lo[seg])
         launches[0] += 1
         if ev:
             ev[3].record(stream)
         if before_precond:
             before_precond()
-        shp.precondition(tbl, plan, roots, gnum, gscale, roots_lo=roots_lo)
+        shp.precondition(tbl, stats_plan, roots, gnum, gscale, roots_lo=roots_lo)
         launches[0] += shp.last_launch_count()
         if ev:
             ev[4].record(stream)
+        if layers:
+            ls.gather(flatP, rank)  # every rank's P and graft scales (one NCCL all-gather of equal segments)
+        if ev:
+            ev[5].record(stream)
         if after_precond:
             after_precond()
         return infos
@@ -308,7 +333,7 @@ def main():
     torch.cuda.synchronize()
 
     # timed region: barrier + sync on both sides, CUDA events on the launching stream
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     # per-group root launch timing (the dominant kernel) on the same stream
     clocks = ClockSampler(local)
     if world > 1:
@@ -328,7 +353,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     total_ms = start.elapsed_time(end)
-    phase = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(4)] for k in range(args.steps)])
+    phase = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(5)] for k in range(args.steps)])
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
@@ -444,8 +469,12 @@ def main():
         hostG = [torch.empty(G.shape, dtype=torch.float32, pin_memory=True) for G in Gs]
         for h, G in zip(hostG, Gs):
             h.copy_(G)
-        hostP = [torch.empty(P.shape, dtype=torch.float32, pin_memory=True) for P in Ps]
-        hscale = torch.empty(nb, dtype=torch.float32, pin_memory=True)
+        if layers:  # every P and graft scale in one flat buffer: one D2H copy
+            hostP = [torch.empty(flatP.shape, dtype=torch.float32, pin_memory=True)]
+            hscale = None
+        else:
+            hostP = [torch.empty(P.shape, dtype=torch.float32, pin_memory=True) for P in Ps]
+            hscale = torch.empty(nb, dtype=torch.float32, pin_memory=True)
         Gs2 = [torch.empty_like(G) for G in Gs]
         tables = [table, shp.TensorTable(Gs2, Ds, Ps)]
         bufs = [Gs, Gs2]
@@ -472,9 +501,10 @@ def main():
         def d2h(k):
             with torch.cuda.stream(copy):
                 copy.wait_event(ev_pre[k])
-                for h, P in zip(hostP, Ps):
+                for h, P in zip(hostP, [flatP] if layers else Ps):
                     h.copy_(P, non_blocking=True)
-                hscale.copy_(gscale, non_blocking=True)
+                if hscale is not None:
+                    hscale.copy_(gscale, non_blocking=True)
                 ev_d2h[k].record(copy)
 
         h2d(0)
@@ -492,7 +522,7 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te.item()) / args.steps
         bi = sum(G.numel() * 4 for G in Gs)
-        bo = sum(P.numel() * 4 for P in Ps) + nb * 4
+        bo = flatP.numel() * 4 if layers else sum(P.numel() * 4 for P in Ps) + nb * 4
         e2e = {"value": n_p4_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo, "ms_per_step": e2e_ms}
 
@@ -509,13 +539,17 @@ def main():
                        "block_size": B, "max_precond_dim": args.max_precond_dim, "blocks": nb,
                        "roots_p4": n_p4_total, "roots_p2": int(sum(int(g["count"]) for g in plan.groups if int(g["p"]) == 2)),
                        "eps_rel": 1e-6, "tol": args.tol, "power_iters": 100,
-                       "parallelism": f"root-shard{world}",
-                       "root_exchange": (("per-group owner broadcasts overlapping the next group's roots "
+                       "parallelism": (f"layer-shard{world}" if layers else f"root-shard{world}"),
+                       "root_exchange": ("none: whole tensors per rank, one all_gather_into_tensor of P + graft "
+                                         "scales per step" if layers else
+                                         ("per-group owner broadcasts overlapping the next group's roots "
                                           "(phase 'roots' includes them)") if args.gather == "overlapped"
-                                         else "one all_gather_into_tensor") if world > 1 else None,
+                                         else "one all_gather_into_tensor of the roots") if world > 1 else None,
                        "root_precision": ROOT_LABEL[args.root_precision], "l2": "inputs larger than L2 (stats 2.6 GB, roots 2.6 GB, G 1.5 GB)"},
-            "phase_ms": {"stats": ph[0], "roots": ph[1], "allgather_and_roots_split": ph[2], "precondition": ph[3]},
-            "shampoo_step_ms": ph[0] + ph[3], "amortized_step_ms_kappa500": ph[0] + ph[3] + (ph[1] + ph[2]) / KAPPA_REFRESH,
+            "phase_ms": {"stats": ph[0], "roots": ph[1], "root_allgather_and_split": ph[2], "precondition": ph[3],
+                         "p_allgather": ph[4]},
+            "shampoo_step_ms": ph[0] + ph[3] + ph[4],
+            "amortized_step_ms_kappa500": ph[0] + ph[3] + ph[4] + (ph[1] + ph[2]) / KAPPA_REFRESH,
             "root_phase_roots_per_s": n_p4_total / (ph[1] * 1e-3),
             "newton_iters_mean": iters_mean,
             "root_status_hist": {str(k): v for k, v in sorted(st_hist.items())},

@@ -129,6 +129,20 @@ int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, i
                  shampoo_group_t* groups, int32_t group_capacity, int32_t* n_groups,
                  int64_t* stats_elems, int64_t* segment_elems);
 
+/* Layer-granular variant (reading #30; "As preconditioners need to be
+ * computed for every layer of the network, we distribute the computation across
+ * all the CPUs"): every root of tensor t is owned by tensor_owner[t], the tensors
+ * assigned LPT -- sorted by (cost desc, index), cost = sum of the tensor's root
+ * costs (n^3 x products per iteration) + m*n, each to the least-loaded rank
+ * (lowest on ties).  Packing as shampoo_plan.  An owner then holds whole tensors:
+ * their statistics, roots and preconditioned gradient, so the multi-GPU step
+ * exchanges P (one all-gather) instead of the roots.
+ *   tensor_owner (host, out, nullable) n_tensors entries. */
+int shampoo_plan_layers(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
+                        int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* blocks,
+                        int32_t capacity, int32_t* n_blocks, shampoo_group_t* groups, int32_t group_capacity,
+                        int32_t* n_groups, int64_t* stats_elems, int64_t* segment_elems, int32_t* tensor_owner);
+
 /* ------------------------------------------------------- a2: statistics step
  * For every block b (Alg. 1; contract in DESIGN.md §6.2):
  *   if any G_b entry is non-finite: block_status[b] = 2, L_b/R_b/D_b untouched,

@@ -21,6 +21,11 @@ Rule (DESIGN.md §3 readings #5, #12, #13, #17):
   Owners: roots sorted by (-cost, tensor_id, block_index, side) and assigned
   longest-processing-time first to the least-loaded rank (lowest rank on
   ties) -- "we distribute the computation across all the CPUs" (P:300-303).
+  owners="tensor" (reading #30, "As preconditioners need to be computed for
+  every layer of the network, we distribute the computation"):
+  tensors sorted by (-cost_t, t) with cost_t = sum of the tensor's root costs
+  + m*n, each assigned to the least-loaded rank (lowest on ties); every root
+  of tensor t is owned by t's owner.
 * Packing: one fp32 buffer holds all statistics (and, at the same offsets,
   all roots).  Rank r's segment holds the roots it owns, grouped by (n desc,
   p desc, r desc), each matrix ``n x ld`` with ``ld = roundup(n, 4)`` and a group
@@ -90,9 +95,10 @@ class Plan:
     stats_elems: int = 0
     segment_elems: int = 0
     loads: list = field(default_factory=list)
+    tensor_owner: list | None = None
 
 
-def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(1, 2)) -> Plan:
+def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(1, 2), owners: str = "root") -> Plan:
     if block_size < 1 or max_precond_dim < 1 or world_size < 1:
         raise ValueError("block_size, max_precond_dim and world_size must be >= 1")
     sa, sd = split
@@ -131,10 +137,26 @@ def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(
         if b.p_right:
             roots.append((b.cols ** 3 * products_per_iteration(b.p_right), b.tensor_id, b.block_index, 1))
     roots.sort(key=lambda r: (-r[0], r[1], r[2], r[3]))
+    tensor_owner = None
+    if owners == "tensor":
+        tcost = [m * n for (m, n) in shapes]
+        for cost, t, _b, _s in roots:
+            tcost[t] += cost
+        tload = [0] * world_size
+        tensor_owner = [0] * len(shapes)
+        for t in sorted(range(len(shapes)), key=lambda t: (-tcost[t], t)):
+            r = min(range(world_size), key=lambda i: (tload[i], i))
+            tload[r] += tcost[t]
+            tensor_owner[t] = r
+    elif owners != "root":
+        raise ValueError("owners must be 'root' or 'tensor'")
     loads = [0] * world_size
     owned = [[] for _ in range(world_size)]  # (n, p, r, sort position, block, side)
-    for pos, (cost, _t, bidx, side) in enumerate(roots):
-        r = min(range(world_size), key=lambda i: (loads[i], i))
+    for pos, (cost, t_, bidx, side) in enumerate(roots):
+        if tensor_owner is not None:
+            r = tensor_owner[t_]
+        else:
+            r = min(range(world_size), key=lambda i: (loads[i], i))
         loads[r] += cost
         b = out.blocks[bidx]
         nn = b.rows if side == 0 else b.cols
@@ -180,4 +202,5 @@ def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(
         if b.right_off >= 0:
             b.right_off += b.owner_right * seg
     out.loads = loads
+    out.tensor_owner = tensor_owner
     return out

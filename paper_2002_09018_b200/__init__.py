@@ -75,6 +75,7 @@ class Plan:
     stats_elems: int
     segment_elems: int
     _dev: dict = field(default_factory=dict, repr=False)
+    tensor_owner: np.ndarray | None = None   # layer-granular plans (owners="tensor"): owner rank of every tensor
 
     @property
     def n_blocks(self) -> int:
@@ -91,24 +92,41 @@ class Plan:
 
 
 def make_plan(shapes, block_size: int = 1024, max_precond_dim: int = 8192, world_size: int = 1,
-              split=(1, 2)) -> Plan:
-    """split = (a, d): the Lemma's 1/p = a/d (f4); (1, 2) -> L^{-1/4} G R^{-1/4}."""
+              split=(1, 2), owners: str = "root") -> Plan:
+    """split = (a, d): the Lemma's 1/p = a/d (f4); (1, 2) -> L^{-1/4} G R^{-1/4}.
+    owners: "root" -- every root assigned LPT on its own (shampoo_plan); "tensor" -- whole tensors (layers)
+    assigned LPT, every root of a tensor on its owner (shampoo_plan_layers, reading #30)."""
+    if owners not in ("root", "tensor"):
+        raise ValueError("owners must be 'root' or 'tensor'")
     L = _lib.lib()
+    fn = L.shampoo_plan if owners == "root" else L.shampoo_plan_layers
     sa, sd = int(split[0]), int(split[1])
     sh = np.ascontiguousarray(np.asarray(shapes, dtype=np.int64).reshape(-1, 2))
     nb = np.zeros(1, np.int32)
     ng = np.zeros(1, np.int32)
     se = np.zeros(1, np.int64)
     sg = np.zeros(1, np.int64)
-    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, sa, sd, None, 0,
-                         nb.ctypes.data, None, 0, ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
+    towner = np.zeros(max(1, sh.shape[0]), np.int32)
+    extra = (towner.ctypes.data,) if owners == "tensor" else ()
+    check(fn(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, sa, sd, None, 0,
+             nb.ctypes.data, None, 0, ng.ctypes.data, se.ctypes.data, sg.ctypes.data, *extra))
     blocks = np.zeros(int(nb[0]), BLOCK_DTYPE)
     groups = np.zeros(int(ng[0]), GROUP_DTYPE)
-    check(L.shampoo_plan(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, sa, sd,
-                         blocks.ctypes.data, blocks.shape[0], nb.ctypes.data, groups.ctypes.data, groups.shape[0],
-                         ng.ctypes.data, se.ctypes.data, sg.ctypes.data))
+    check(fn(sh.ctypes.data, sh.shape[0], block_size, max_precond_dim, world_size, sa, sd,
+             blocks.ctypes.data, blocks.shape[0], nb.ctypes.data, groups.ctypes.data, groups.shape[0],
+             ng.ctypes.data, se.ctypes.data, sg.ctypes.data, *extra))
     return Plan([tuple(map(int, s)) for s in sh], block_size, max_precond_dim, world_size, blocks, groups,
-                int(se[0]), int(sg[0]))
+                int(se[0]), int(sg[0]), tensor_owner=towner[:sh.shape[0]].copy() if owners == "tensor" else None)
+
+
+def subplan(plan: Plan, block_indices) -> Plan:
+    """The plan restricted to some of its blocks (same packed offsets and groups): e.g. the blocks of one
+    rank's tensors in a layer-granular plan.  Per-block outputs (graft numerator / scale) of calls made with it
+    are indexed by position in ``block_indices``."""
+    idx = np.asarray(block_indices, dtype=np.int64)
+    return Plan(plan.shapes, plan.block_size, plan.max_precond_dim, plan.world_size,
+                np.ascontiguousarray(plan.blocks[idx]), plan.groups, plan.stats_elems, plan.segment_elems,
+                tensor_owner=plan.tensor_owner)
 
 
 # ------------------------------------------------------------- tensor table

@@ -35,7 +35,7 @@ assert TTENSOR_DTYPE.itemsize == 64 and TBLOCK_DTYPE.itemsize == 136
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "CUDA", 4: "WORKSPACE", 5: "CAPACITY"}
 
 EXPORTED = [
-    "shampoo_abi_version", "shampoo_last_error", "shampoo_last_launch_count", "shampoo_plan",
+    "shampoo_abi_version", "shampoo_last_error", "shampoo_last_launch_count", "shampoo_plan", "shampoo_plan_layers",
     "shampoo_stats_workspace_bytes", "shampoo_stats_update",
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_inverse_pth_root_batched_hybrid", "shampoo_root_ozaki_workspace_bytes",
@@ -77,6 +77,9 @@ def lib():
     L.shampoo_last_launch_count.restype = _i64
     L.shampoo_plan.argtypes = [_vp, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp]
     L.shampoo_plan.restype = ctypes.c_int
+    L.shampoo_plan_layers.argtypes = [_vp, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp,
+                                      _vp]
+    L.shampoo_plan_layers.restype = ctypes.c_int
     L.shampoo_stats_workspace_bytes.argtypes = [_vp, _i32, _i32]
     L.shampoo_stats_workspace_bytes.restype = _sz
     L.shampoo_stats_update.argtypes = [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _dbl, _dbl, _vp, _vp, _vp, _sz, _vp]

@@ -23,8 +23,9 @@ CU_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLU
             "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
-SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu", "tc_gemm.cu", "momentum.cu", "tensor.cu", "root_tail.cu"]
-HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h", "tc_common.cuh", "tc_gemm.h", "ozaki.cuh"]
+SOURCES = ["abi.cpp", "plan.cpp", "stats.cu", "root.cu", "precondition.cu", "tc_gemm.cu", "momentum.cu", "tensor.cu",
+           "root_tail.cu", "oz_precondition.cu"]
+HEADERS = ["common.cuh", "dmma_gemm.cuh", "internal.h", "tc_common.cuh", "tc_gemm.h", "ozaki.cuh", "oz_precondition.h"]
 
 
 def _newer(target: str, deps) -> bool:

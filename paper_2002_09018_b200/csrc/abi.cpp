@@ -90,7 +90,7 @@ cudaError_t ensure_smem(const void* func, size_t smem) {
 int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
               int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
               shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
-              int64_t* segment_elems);
+              int64_t* segment_elems, int32_t layer_owners, int32_t* tensor_owner_out);
 
 int tensor_plan_impl(const int64_t* dims, const int32_t* orders, int32_t n_tensors, int32_t block_size,
                      int64_t max_precond_dim, int32_t world_size, shampoo_tblock_t* out_blocks, int32_t capacity,
@@ -206,7 +206,16 @@ int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, i
                  int64_t* segment_elems) {
   g_err[0] = 0;
   return plan_impl(shapes, n_tensors, block_size, max_precond_dim, world_size, split_num, split_den, blocks, capacity, n_blocks, groups,
-                   group_capacity, n_groups, stats_elems, segment_elems);
+                   group_capacity, n_groups, stats_elems, segment_elems, 0, nullptr);
+}
+
+int shampoo_plan_layers(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
+                        int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* blocks,
+                        int32_t capacity, int32_t* n_blocks, shampoo_group_t* groups, int32_t group_capacity,
+                        int32_t* n_groups, int64_t* stats_elems, int64_t* segment_elems, int32_t* tensor_owner) {
+  g_err[0] = 0;
+  return plan_impl(shapes, n_tensors, block_size, max_precond_dim, world_size, split_num, split_den, blocks, capacity,
+                   n_blocks, groups, group_capacity, n_groups, stats_elems, segment_elems, 1, tensor_owner);
 }
 
 size_t shampoo_stats_workspace_bytes(const shampoo_block_t* blocks_host, int32_t n_blocks, int32_t only_owner) {

@@ -359,6 +359,25 @@ __device__ __forceinline__ unsigned long long int_w(double c, int e_out, bool& o
   return (unsigned long long)(V + kC);
 }
 
+// fp32 round-to-nearest-even of a double on the integer pipe (normal fp32 results and zeros; anything else
+// -- subnormal fp32 results, inf, NaN -- through the out-of-line conversion)
+static __device__ __noinline__ float f32_of_slow(double x) { return __double2float_rn(x); }
+__device__ __forceinline__ float f32_of(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const unsigned sign = (unsigned)(b >> 32) & 0x80000000u;
+  const int ex = (int)((b >> 52) & 0x7FF);
+  const int e32 = ex - 1023 + 127;
+  if ((b << 1) == 0ull) return __uint_as_float(sign);
+  if (e32 >= 1 && e32 <= 254) {
+    const unsigned long long m = b & 0xFFFFFFFFFFFFFull;
+    unsigned q = (unsigned)(m >> 29);
+    const unsigned long long rem = m & ((1ull << 29) - 1ull);
+    q += (rem > (1ull << 28) || (rem == (1ull << 28) && (q & 1u))) ? 1u : 0u;
+    return __uint_as_float(sign | (((unsigned)e32 << 23) + q));  // a mantissa carry bumps the exponent (inf past 254)
+  }
+  return f32_of_slow(x);
+}
+
 // byte of plane s (digit u_s - 64) from W; plane 0 takes 8 bits (top digit in [-64, 64])
 template <int S>
 __device__ __forceinline__ uint32_t w_byte(unsigned long long W, int s) {
@@ -375,7 +394,7 @@ __device__ __forceinline__ int exp2_of(double x) {
 }
 // x 2^k by two fp64 multiplies with exact power-of-two factors (|k| < 2000);
 // out of line so the compiler cannot if-convert it into the common path
-__device__ __noinline__ double scale2_slow(double x, int k) {
+static __device__ __noinline__ double scale2_slow(double x, int k) {
   if (x == 0.0 || !isfinite(x)) return x;
   const int k1 = k / 2;
   return x * __longlong_as_double((long long)(k1 + 1023) << 52) * __longlong_as_double((long long)(k - k1 + 1023) << 52);
@@ -403,6 +422,12 @@ struct OzJob {
   int8_t* planes;
   double* out_scale;
   int out_e;
+  // fp32 output (out == nullptr, planes == nullptr; the preconditioned gradient of one-sided blocks, a8):
+  // matrix mat's rows i < outf_rows[mat] go to outf[mat] + i * outf_ld[mat] (columns j < n), rounded to
+  // nearest fp32 by integer arithmetic (no fp64 instruction while the tensor pipe runs)
+  float* const* outf;
+  const int64_t* outf_ld;
+  const int* outf_rows;
 };
 
 struct OzArgs {
@@ -724,6 +749,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (ovf)  // the a-priori bound failed: poison this matrix's next err check (status 2, never silent)
           atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + a.kcheck),
                     0x7FF8000000000000ull);
+      } else if (J.outf) {
+        // fp32 output (a8, one-sided blocks: P_b = G_b X_R; non-symmetric tiles, no mirror)
+        if (row_ok && i < J.outf_rows[mat]) {
+          const int j0 = tj * kBN;
+          const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
+          float* orow = J.outf[mat] + (int64_t)i * J.outf_ld[mat] + j0;
+          const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
+          const bool vec = j0 + kBN <= a.n && ((reinterpret_cast<uintptr_t>(orow) & 15) == 0);
+#pragma unroll
+          for (int e = 0; e < kBN; e += 4) {
+            const double2 b01 = *reinterpret_cast<const double2*>(bs + e);
+            const double2 b23 = *reinterpret_cast<const double2*>(bs + e + 2);
+            const float f0 = f32_of(scale2(v[e], ka + exp2_of(b01.x)));
+            const float f1 = f32_of(scale2(v[e + 1], ka + exp2_of(b01.y)));
+            const float f2 = f32_of(scale2(v[e + 2], ka + exp2_of(b23.x)));
+            const float f3 = f32_of(scale2(v[e + 3], ka + exp2_of(b23.y)));
+            if (vec) {
+              __stcs(reinterpret_cast<float4*>(orow + e), make_float4(f0, f1, f2, f3));
+            } else {
+              if (j0 + e < a.n) orow[e] = f0;
+              if (j0 + e + 1 < a.n) orow[e + 1] = f1;
+              if (j0 + e + 2 < a.n) orow[e + 2] = f2;
+              if (j0 + e + 3 < a.n) orow[e + 3] = f3;
+            }
+          }
+        }
       } else if (row_ok) {
         const int j0 = tj * kBN;
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;

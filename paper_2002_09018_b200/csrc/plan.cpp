@@ -48,9 +48,11 @@ struct RootRef {
 // stride roundup(n*ld, 64); segments padded to the largest (roundup 64).
 // set(root, owner, absolute offset, ld) records each root's placement.
 // Returns the segment size.
+// tensor_owner (optional): every root of tensor t goes to tensor_owner[t] instead of the per-root LPT
+// (layer-granular distribution, reading #30).
 template <class Set>
 static int64_t assign_and_pack(std::vector<RootRef>& roots, int world_size, std::vector<shampoo_group_t>& groups,
-                               Set set) {
+                               Set set, const std::vector<int>* tensor_owner = nullptr) {
   std::stable_sort(roots.begin(), roots.end(), [](const RootRef& x, const RootRef& y) {
     return std::make_tuple(-x.cost, x.tensor, x.block, x.side) < std::make_tuple(-y.cost, y.tensor, y.block, y.side);
   });
@@ -59,8 +61,12 @@ static int64_t assign_and_pack(std::vector<RootRef>& roots, int world_size, std:
   std::vector<int> owner_of(roots.size(), 0);
   for (int32_t pos = 0; pos < (int32_t)roots.size(); ++pos) {
     int r = 0;
-    for (int q = 1; q < world_size; ++q)
-      if (load[q] < load[r]) r = q;
+    if (tensor_owner) {
+      r = (*tensor_owner)[roots[pos].tensor];
+    } else {
+      for (int q = 1; q < world_size; ++q)
+        if (load[q] < load[r]) r = q;
+    }
     load[r] += roots[pos].cost;
     owned[r].push_back(pos);
     owner_of[pos] = r;
@@ -107,10 +113,34 @@ static int64_t assign_and_pack(std::vector<RootRef>& roots, int world_size, std:
   return seg;
 }
 
+// Layer-granular owners (reading #30): tensors sorted by (cost desc, index) with cost = the sum of their
+// roots' costs plus m*n (so tensors without a preconditioned side still spread), each assigned to the
+// least-loaded rank (lowest rank on ties).
+static std::vector<int> tensor_owners(const std::vector<RootRef>& roots, const int64_t* shapes, int32_t n_tensors,
+                                      int world_size) {
+  std::vector<int64_t> cost(n_tensors, 0);
+  for (int32_t t = 0; t < n_tensors; ++t) cost[t] = shapes[2 * t] * shapes[2 * t + 1];
+  for (const RootRef& r : roots) cost[r.tensor] += r.cost;
+  std::vector<int32_t> order(n_tensors);
+  for (int32_t t = 0; t < n_tensors; ++t) order[t] = t;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return std::make_tuple(-cost[a], a) < std::make_tuple(-cost[b], b); });
+  std::vector<int64_t> load(world_size, 0);
+  std::vector<int> owner(n_tensors, 0);
+  for (int32_t t : order) {
+    int r = 0;
+    for (int q = 1; q < world_size; ++q)
+      if (load[q] < load[r]) r = q;
+    load[r] += cost[t];
+    owner[t] = r;
+  }
+  return owner;
+}
+
 int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int64_t max_precond_dim,
               int32_t world_size, int32_t split_num, int32_t split_den, shampoo_block_t* out_blocks, int32_t capacity, int32_t* n_blocks_out,
               shampoo_group_t* out_groups, int32_t group_capacity, int32_t* n_groups_out, int64_t* stats_elems,
-              int64_t* segment_elems) {
+              int64_t* segment_elems, int32_t layer_owners, int32_t* tensor_owner_out) {
   if (!shapes || n_tensors < 0 || block_size < 1 || max_precond_dim < 1 || world_size < 1)
     return set_error(SHAMPOO_ERR_INVALID_ARG, "plan: bad arguments");
   if (split_num < 1 || split_num >= split_den)
@@ -159,6 +189,10 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
     }
   }
   std::vector<shampoo_group_t> groups;
+  std::vector<int> towner;
+  if (layer_owners) towner = tensor_owners(roots, shapes, n_tensors, world_size);
+  if (tensor_owner_out && layer_owners)
+    for (int32_t t = 0; t < n_tensors; ++t) tensor_owner_out[t] = towner[t];
   const int64_t seg = assign_and_pack(roots, world_size, groups, [&](const RootRef& rr, int owner, int64_t off, int ld) {
     shampoo_block_t& b = blocks[rr.block];
     if (rr.side == 0) {
@@ -170,7 +204,7 @@ int plan_impl(const int64_t* shapes, int32_t n_tensors, int32_t block_size, int6
       b.right_off = off;
       b.right_ld = ld;
     }
-  });
+  }, layer_owners ? &towner : nullptr);
   if (n_blocks_out) *n_blocks_out = (int32_t)blocks.size();
   if (n_groups_out) *n_groups_out = (int32_t)groups.size();
   if (stats_elems) *stats_elems = seg * world_size;

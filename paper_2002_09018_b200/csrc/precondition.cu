@@ -16,6 +16,7 @@
 
 #include "dmma_gemm.cuh"
 #include "internal.h"
+#include "oz_precondition.h"
 #include "tc_gemm.h"
 
 namespace shp {
@@ -226,18 +227,21 @@ struct PrecLayout {
   int64_t tiles1 = 0, tiles2 = 0;
   bool any_dmma = false;
   // device regions (offsets from ws)
-  size_t off_pre = 0, off_part = 0, off_Y = 0, off_rlo = 0, off_glo = 0, off_zhi = 0, off_zlo = 0, total = 0;
+  size_t off_pre = 0, off_part = 0, off_Y = 0, off_rlo = 0, off_glo = 0, off_zhi = 0, off_zlo = 0, off_oz = 0,
+         total = 0;
+  std::vector<int> flags;  // per block: 1 tcgen05 3xTF32, 2 INT8 Ozaki (oz_precondition.cu), 0 DMMA / diagonal
   int64_t roots_elems = 0;
 };
 
 static bool tc_eligible(const shampoo_block_t& b, const shampoo_tensor_t& t) {
-  // one-sided blocks (P = G_b X_R, X_L G_b) run on the FP64 DMMA path: their statistic is often rank-deficient
+  // one-sided blocks (P = G_b X_R, X_L G_b) never take the 3xTF32 path: their statistic is often rank-deficient
   // (the vocabulary rows of an embedding gradient: G_b's rows span few dimensions), so the root's largest
   // eigenvalues sit in directions G_b is orthogonal to and the product cancels them exactly; an fp32
   // accumulation (the tensor core's 3xTF32) loses up to ~kappa^{1/2} of its relative accuracy there -- measured
   // on B200: P rel. error 6.2e-3 on a 4-nonzero-row vocabulary block (north-star bar 1e-3), against 3.2e-5 for
-  // the exact product of the same fp32 root (tests/test_gpu_bench_path.py)
-  if (!b.p_right || !b.p_left) return false;  // one-sided / diagonal-only blocks: DMMA / elementwise path
+  // the exact product of the same fp32 root (tests/test_gpu_bench_path.py).  Right-only blocks run on the INT8
+  // Ozaki path (oz_precondition.cu, exact int32 products), the rest on FP64 DMMA.
+  if (!b.p_right || !b.p_left) return false;  // one-sided / diagonal-only blocks: Ozaki / DMMA / elementwise
   // the raw G is the TMA "hi" operand: contiguous rows, 16-byte aligned
   if (t.ldg != t.n || (t.n & 3) || (reinterpret_cast<uintptr_t>(t.G) & 15)) return false;
   const bool rows_ok = (b.rows % 32 == 0) || (b.row0 + b.rows == t.m);
@@ -258,11 +262,13 @@ static size_t put(std::vector<uint8_t>& blob, const T* p, size_t n, size_t align
 // Builds the layout; when `ws` is null only sizes are computed (maps need real pointers).
 static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_block_t* B, int n_blocks,
                         const float* roots, const float* roots_lo, char* ws, PrecLayout& L) {
-  std::vector<int> flags(n_blocks, 0);
+  std::vector<int>& flags = L.flags;
+  flags.assign(n_blocks, 0);
   std::vector<char> t_g(n_tensors, 0), t_z(n_tensors, 0);
   size_t y_elems = 0;
   for (int b = 0; b < n_blocks; ++b) {
-    flags[b] = tc_eligible(B[b], T[B[b].tensor_id]) ? 1 : 0;
+    flags[b] = tc_eligible(B[b], T[B[b].tensor_id]) ? 1 : oz_precondition_eligible(B[b]) ? 2 : 0;
+    if (flags[b] == 2) continue;
     if (flags[b]) {
       t_g[B[b].tensor_id] = 1;
       if (B[b].p_left) t_z[B[b].tensor_id] = 1;
@@ -317,6 +323,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
   L.off_glo = region(gsz);
   L.off_zhi = region(zsz);
   L.off_zlo = region(zsz);
+  L.off_oz = region(oz_precondition_bytes(B, n_blocks, flags.data()));
   L.total = q;
   if (!ws) return SHAMPOO_OK;
 
@@ -384,7 +391,7 @@ static int build_layout(const shampoo_tensor_t* T, int n_tensors, const shampoo_
   std::vector<TcJob> j1, j2;
   int64_t t1 = 0, t2 = 0;
   for (int b = 0; b < n_blocks; ++b) {
-    if (!flags[b]) continue;
+    if (flags[b] != 1) continue;
     const shampoo_block_t& bk = B[b];
     const shampoo_tensor_t& tt = T[bk.tensor_id];
     const int tm = (bk.rows + 127) / 128, tn = (bk.cols + kTcGemmBN - 1) / kTcGemmBN;
@@ -490,6 +497,10 @@ int precondition_launch(const shampoo_tensor_t* tensors_host, int n_tensors, con
   rc = tc_gemm_launch(reinterpret_cast<const TcJob*>(w + L.off_jobs1), L.n_jobs1, L.tiles1, maps, stream, launches);
   if (rc) return rc;
   rc = tc_gemm_launch(reinterpret_cast<const TcJob*>(w + L.off_jobs2), L.n_jobs2, L.tiles2, maps, stream, launches);
+  if (rc) return rc;
+  // INT8 Ozaki path for the one-sided blocks (exact int32 products, fp32 P)
+  rc = oz_precondition_launch(tensors_host, blocks_host, n_blocks, L.flags.data(), roots, w + L.off_oz, stream,
+                              launches);
   if (rc) return rc;
   // DMMA path for the remaining blocks (left-only, unaligned)
   if (L.any_dmma) {

@@ -676,6 +676,9 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
     j.planes = nullptr;
     j.out_scale = nullptr;
     j.out_e = 0;
+    j.outf = nullptr;
+    j.outf_ld = nullptr;
+    j.outf_rows = nullptr;
     return j;
   };
   // T^m (m >= 2) sliced by the product's own epilogue: every row scaled by 2^e with

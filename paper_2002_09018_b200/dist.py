@@ -14,7 +14,12 @@ that are part of the training system".  One process per GPU:
   * or (``refresh_gather_overlapped``) per root group: once the owners have
     computed a group, its region of every segment is broadcast from its owner on
     NCCL's stream while the next group computes -- the same bytes, but only the
-    last group's transfer stays on the critical path.
+    last group's transfer stays on the critical path;
+  * or (``LayerShards``, reading #30) whole tensors per rank: a layer-granular
+    plan (``make_plan(..., owners="tensor")``) gives every root of a tensor to
+    one rank, which also updates that tensor's statistics and computes its
+    preconditioned gradient; ONE all-gather of P (+ the graft scales) per step
+    replaces the roots' all-gather and the replicated preconditioning.
 """
 
 from __future__ import annotations
@@ -22,7 +27,9 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import Plan, inverse_pth_root_ptr, last_launch_count, new_info, refresh_group_roots
+import numpy as np
+
+from . import Plan, inverse_pth_root_ptr, last_launch_count, new_info, refresh_group_roots, subplan
 
 
 def segment(plan: Plan, buf: torch.Tensor, rank: int) -> torch.Tensor:
@@ -106,3 +113,73 @@ def refresh_gather_overlapped(plan: Plan, stats: torch.Tensor, roots: torch.Tens
     for w in works:
         w.wait()
     return out, launches
+
+
+class LayerShards:
+    """Layer-granular sharding of the whole step (reading #30; "As preconditioners need to be computed
+    for every layer of the network, we distribute the computation across all the CPUs").
+
+    ``plan`` comes from ``make_plan(..., owners="tensor")``.  Rank r owns the tensors with ``tensor_owner == r``:
+    ``sub[r]`` is the plan restricted to their blocks (statistics, D, graft numerator, roots and P of those
+    blocks only).  The preconditioned gradients live in ONE flat fp32 buffer laid out rank-major: segment r holds
+    rank r's tensors (index order, offsets rounded up to 4 elements = 16 bytes), then the graft scales of its
+    blocks (``sub[r]`` order); every segment is padded to the largest (rounded up to 64 elements), so one
+    ``all_gather_into_tensor`` of equal segments rebuilds every P and every scale on every rank."""
+
+    def __init__(self, plan: Plan, world_size: int):
+        if plan.tensor_owner is None:
+            raise ValueError("LayerShards needs a layer-granular plan (make_plan(..., owners='tensor'))")
+        self.world = world_size
+        self.shapes = [tuple(s) for s in plan.shapes]
+        self.owner = np.asarray(plan.tensor_owner, dtype=np.int64)
+        tid = plan.blocks["tensor_id"].astype(np.int64)
+        self.block_idx = [np.nonzero(self.owner[tid] == r)[0] for r in range(world_size)]
+        self.sub = [subplan(plan, self.block_idx[r]) for r in range(world_size)]
+        self.offset = np.zeros(len(self.shapes), dtype=np.int64)   # absolute offset of tensor t's P
+        self.scale_off = np.zeros(world_size, dtype=np.int64)      # absolute offset of rank r's scales
+        used = []
+        for r in range(world_size):
+            off = 0
+            for t in range(len(self.shapes)):
+                if self.owner[t] == r:
+                    self.offset[t] = off
+                    m, n = self.shapes[t]
+                    off += (m * n + 3) // 4 * 4
+            self.scale_off[r] = off
+            used.append(off + len(self.block_idx[r]))
+        self.segment = (max(used) + 63) // 64 * 64
+        for t in range(len(self.shapes)):
+            self.offset[t] += self.owner[t] * self.segment
+        self.scale_off += np.arange(world_size, dtype=np.int64) * self.segment
+        self.numel = self.segment * world_size
+
+    def p_views(self, flat):
+        """Row-major (m, n) views of every tensor's P inside the flat buffer."""
+        out = []
+        for t, (m, n) in enumerate(self.shapes):
+            o = int(self.offset[t])
+            out.append(flat[o:o + m * n].view(m, n))
+        return out
+
+    def scales_of(self, flat, rank: int):
+        o = int(self.scale_off[rank])
+        return flat[o:o + len(self.block_idx[rank])]
+
+    def gather(self, flat, rank: int, group=None):
+        """All-gather of the equal segments (in place for NCCL)."""
+        if self.world == 1:
+            return
+        mine = flat[rank * self.segment:(rank + 1) * self.segment]
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(flat[:self.numel], mine, group=group)
+        else:  # gloo (CPU tests): out-of-place
+            out = torch.empty_like(flat[:self.numel])
+            dist.all_gather_into_tensor(out, mine.clone(), group=group)
+            flat[:self.numel].copy_(out)
+
+    def unpack_scales(self, flat, scales_full):
+        """Graft scales of every block (full-plan order) from the gathered segments."""
+        for r in range(self.world):
+            idx = torch.as_tensor(self.block_idx[r], device=scales_full.device)
+            if idx.numel():
+                scales_full.index_copy_(0, idx, self.scales_of(flat, r).to(scales_full.dtype))

@@ -74,6 +74,17 @@ def test_plan_bit_exact_vs_oracle(shp, case, W):
     _fields_equal(shp.make_plan(shapes, b, mpd, W), oplan.plan(shapes, b, mpd, W))
 
 
+@pytest.mark.parametrize("W", [1, 2, 3, 8])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_plan_layers_bit_exact_vs_oracle(shp, case, W):
+    """Layer-granular owners (shampoo_plan_layers, reading #30): blocks, groups and the tensor owners."""
+    shapes, b, mpd = CASES[case]
+    lp = shp.make_plan(shapes, b, mpd, W, owners="tensor")
+    op = oplan.plan(shapes, b, mpd, W, owners="tensor")
+    _fields_equal(lp, op)
+    assert list(map(int, lp.tensor_owner)) == op.tensor_owner
+
+
 # f4 splits 1/p = a/d: (1,4) -> 1/8, 3/8; (3,4) -> 3/8, 1/8; (1,3) -> 1/6, 1/3; (2,5) -> 1/5, 3/10
 @pytest.mark.parametrize("split", [(1, 4), (3, 4), (1, 3), (2, 5), (1, 8)])
 @pytest.mark.parametrize("W", [1, 3])

@@ -133,3 +133,60 @@ def test_overlapped_group_broadcasts_equal_the_all_gather(world):
     for rank, ref, got in out:
         assert np.array_equal(np.nan_to_num(ref, nan=-1), np.nan_to_num(got, nan=-1)), rank
     assert np.array_equal(np.nan_to_num(out[0][2], nan=-1), np.nan_to_num(out[-1][2], nan=-1))
+
+
+def _layer_worker(rank, world, port, shapes, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2002_09018_b200 as shp
+        from paper_2002_09018_b200 import dist as sdist
+        plan = shp.make_plan(shapes, 128, 8192, world, owners="tensor")
+        ls = sdist.LayerShards(plan, world)
+        flat = torch.full((ls.numel,), float("nan"))
+        P = ls.p_views(flat)
+        # this rank "preconditions" its own tensors: P[t] = t + 1 + (index in the tensor) * 1e-3
+        for t, (m, n) in enumerate(shapes):
+            if ls.owner[t] == rank:
+                P[t].copy_(float(t + 1) + 1e-3 * torch.arange(m * n, dtype=torch.float32).view(m, n))
+        sc = ls.scales_of(flat, rank)
+        sc.copy_(torch.as_tensor(ls.block_idx[rank], dtype=torch.float32) + 0.5)
+        ls.gather(flat, rank)
+        full = torch.zeros(plan.n_blocks)
+        ls.unpack_scales(flat, full)
+        q.put((rank, [p.clone().numpy() for p in ls.p_views(flat)], full.numpy().copy(),
+               [len(s.blocks) for s in ls.sub], ls.block_idx))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_layer_shards_gather_every_p_and_scale(world):
+    """Layer-granular step (reading #30): each rank writes only its tensors' P and its blocks' graft scales into
+    its segment of the flat buffer; one all-gather of the equal segments gives every rank every P and every
+    scale; the per-rank sub-plans partition the blocks (no block twice, none missing)."""
+    shapes = [(300, 200), (128, 128), (1000, 64), (64, 1), (50, 700), (256, 384)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_layer_worker, args=(r, world, port, shapes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, Ps, sc, counts, idx = q.get(timeout=240)
+        out[r] = (Ps, sc, counts, idx)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Ps0, sc0, counts, idx = out[0]
+    allidx = np.sort(np.concatenate(idx))
+    assert np.array_equal(allidx, np.arange(len(allidx)))  # sub-plans partition the blocks
+    assert sum(counts) == len(allidx)
+    for r in range(world):
+        Ps, sc, _, _ = out[r]
+        for t, (m, n) in enumerate(shapes):
+            want = float(t + 1) + 1e-3 * np.arange(m * n, dtype=np.float32).reshape(m, n)
+            assert np.array_equal(Ps[t], want), (r, t)
+        assert np.array_equal(sc, np.arange(len(sc), dtype=np.float32) + 0.5)

@@ -315,6 +315,49 @@ def test_precondition_with_oracle_roots(shp):
     np.testing.assert_allclose(sc.cpu().numpy(), sc_o, rtol=1e-5)
 
 
+def test_precondition_one_sided_rank_deficient(shp):
+    """Right-only vocabulary blocks (rows <= cols: the INT8 Ozaki path, oz_precondition.cu) whose statistic is
+    rank-deficient: G_b has a few nonzero rows, R_b = G_b^T G_b + the ridge has kappa ~1e6 and X_R is largest
+    exactly where G_b's rows vanish, so P = G_b X_R cancels ~kappa^{1/2}.  With the ORACLE's roots (fp32) the
+    product must match the oracle's fp64 product to fp32 rounding -- an fp32 accumulation (3xTF32) was 6.2e-3 off
+    on such a block (r02c).  Ragged last block (rows 300 of 512), a block with 3 nonzero rows."""
+    m, n, block = 1324, 512, 512
+    G = np.zeros((m, n), np.float32)
+    rng = np.random.default_rng(synth.BASE_SEED + 321)
+    for r in rng.choice(512, 40, replace=False):           # block 0: 40 nonzero rows
+        G[r] = rng.normal(0, 0.01, n)
+    for r in 512 + rng.choice(512, 3, replace=False):      # block 1: 3 nonzero rows
+        G[r] = rng.normal(0, 0.01, n)
+    for r in 1024 + rng.choice(300, 12, replace=False):    # block 2 (ragged, 300 rows): 12 nonzero rows
+        G[r] = rng.normal(0, 0.01, n)
+    shapes = [(m, n)]
+    pl_o = oplan.plan(shapes, block, 1024, 1)
+    pl = shp.make_plan(shapes, block, 1024, 1)
+    assert all(b.p_left == 0 and b.p_right == 2 for b in pl_o.blocks) and len(pl_o.blocks) == 3
+    stats_o = np.zeros(pl_o.stats_elems, np.float32)
+    D_o = [np.zeros(G.shape, np.float32)]
+    num_o, _ = ostats.stats_update([G], D_o, pl_o, stats_o, 1.0, 1.0)
+
+    def rf(b, side, nn):
+        A = stats_o[b.right_off:b.right_off + nn * b.right_ld].reshape(nn, b.right_ld)[:, :nn].astype(np.float64)
+        return oroot.inverse_pth_root(A, 2)[0].astype(np.float32)
+
+    roots = _pack_roots(pl_o, rf)
+    Ps_o, sc_o, den_o = opre.precondition_plan([G], D_o, pl_o, roots.astype(np.float64), num_o)
+    Pd = torch.full(G.shape, np.nan, dtype=torch.float32, device=DEV)
+    table = shp.TensorTable([torch.from_numpy(G).to(DEV)], [torch.from_numpy(D_o[0]).to(DEV)], [Pd])
+    sc = torch.zeros(pl.n_blocks, dtype=torch.float32, device=DEV)
+    shp.precondition(table, pl, torch.from_numpy(roots).to(DEV), torch.from_numpy(num_o).to(DEV), sc)
+    torch.cuda.synchronize()
+    Pg = Pd.cpu().numpy()
+    for b in pl_o.blocks:
+        sl = (slice(b.row0, b.row0 + b.rows), slice(b.col0, b.col0 + b.cols))
+        err = rel(Pg[sl], Ps_o[0][sl])
+        print(f"one-sided block {b.block_index} ({b.rows} rows): P rel err {err:.3e}")
+        assert err < 1e-6, (b.block_index, err)
+    np.testing.assert_allclose(sc.cpu().numpy(), sc_o, rtol=1e-5)
+
+
 # ---------------------------------------------------------------- full chain
 
 def test_full_step_config1_chain(shp):

@@ -118,3 +118,38 @@ def test_plan_is_deterministic():
     a = oplan.plan(shapes, 1024, 8192, 8)
     b = oplan.plan(shapes, 1024, 8192, 8)
     assert [vars(x) for x in a.blocks] == [vars(x) for x in b.blocks]
+
+
+def test_layer_owners_hand_worked():
+    """owners="tensor" (reading #30), worked by hand: costs are sum(n^3 x products) + m*n per tensor.
+    4 equal 1024^2 tensors at W=4 -> one tensor per rank (LPT deals them 0, 1, 2, 3); at W=3 the fourth goes
+    back to rank 0 (all loads equal, lowest rank).  Sizes 256, 512, 512, 1024 (two-sided, 4 products each:
+    costs 2*4*n^3 + n^2) at W=2: the 1024 tensor alone on rank 0, the rest on rank 1 (1024-cost 8.59e9 >
+    2 x 1.07e9 + 1.3e8)."""
+    pl = oplan.plan([(1024, 1024)] * 4, 1024, 8192, 4, owners="tensor")
+    assert pl.tensor_owner == [0, 1, 2, 3]
+    assert [(b.owner_left, b.owner_right) for b in pl.blocks] == [(r, r) for r in range(4)]
+    pl3 = oplan.plan([(1024, 1024)] * 4, 1024, 8192, 3, owners="tensor")
+    assert pl3.tensor_owner == [0, 1, 2, 0]
+    pl2 = oplan.plan([(256, 256), (512, 512), (512, 512), (1024, 1024)], 1024, 8192, 2, owners="tensor")
+    assert pl2.tensor_owner == [1, 1, 1, 0]
+    assert pl2.loads == [2 * 4 * 1024 ** 3, 2 * 4 * (256 ** 3 + 2 * 512 ** 3)]
+
+
+def test_layer_owners_keep_tensors_whole():
+    """Every root of a tensor has the tensor's owner; segments still rebuild the buffer (equal, padded)."""
+    shapes = [s for _, s in transformer_big_shapes()]
+    for W in (2, 3, 8):
+        pl = oplan.plan(shapes, 1024, 8192, W, owners="tensor")
+        for b in pl.blocks:
+            for p, o in ((b.p_left, b.owner_left), (b.p_right, b.owner_right)):
+                if p:
+                    assert o == pl.tensor_owner[b.tensor_id]
+        assert pl.stats_elems == W * pl.segment_elems
+        # LPT over layers: the spread of the root loads is at most one tensor's cost
+        tcost = {}
+        for b in pl.blocks:
+            c = (b.rows ** 3 * oplan.products_per_iteration(b.p_left) if b.p_left else 0) + \
+                (b.cols ** 3 * oplan.products_per_iteration(b.p_right) if b.p_right else 0)
+            tcost[b.tensor_id] = tcost.get(b.tensor_id, 0) + c
+        assert max(pl.loads) - min(pl.loads) <= max(tcost.values()) + max(m * n for m, n in shapes)
