@@ -156,15 +156,17 @@ def test_bench_sampled_precondition_vs_oracle(run):
         err = rel(Pg, Po)
         two_sided = b.p_left > 0 and b.p_right > 0
         print(f"block {bi} ({'two' if two_sided else 'one'}-sided): P rel err {err:.3e}")
-        # north star: 1e-3.  Two-sided blocks are held to 2e-5 (3xTF32 products of fp32 roots).  One-sided
-        # vocabulary blocks run on FP64 DMMA (precondition.cu tc_eligible) and are held to the north star's 1e-3:
-        # the rows of G_b lie in the range of R_b = G_b^T G_b while R_b^{-1/2}'s largest eigenvalues sit in its
-        # null space, so P = G_b R_b^{-1/2} cancels them exactly and any root error there reaches P amplified
-        # ~kappa^{1/2} -- the exact product of the fp32-rounded ORACLE root is already 3.2e-5 off on block 31
-        # (4 nonzero rows); measured on B200 (r02d): 4.9e-6 (block 0), 2.6e-4 (block 31); 3xTF32 had 6.2e-3
-        assert err < (2e-5 if two_sided else 1e-3), (bi, err)
-        # scale = sqrt(num) / ||P||_F: its relative error is bounded by P's (1e-5 two-sided, north star 1e-3)
-        assert abs(run["sc"][bi] - run["sc_o"][bi]) <= (1e-5 if two_sided else 1e-3) * run["sc_o"][bi], bi
+        # north star: 1e-3.  P here is the product of the GPU's own roots (slice-scheduled Ozaki, 2.2e-7 from the
+        # oracle's), and a root's error reaches P amplified by the cancellation in X_L G_b X_R: the rows of G_b lie
+        # mostly in the range of its statistics while X's largest eigenvalues sit where they are ~0 (kappa 1e6
+        # after the ridge).  Measured on B200 (r02f): two-sided 3.0e-5, held to 1e-4; one-sided vocabulary blocks
+        # (their R_b has 4..842 nonzero directions
+        # of 1024) 4.9e-6 .. 2.6e-4 -- the exact fp64 product of the fp32-rounded ORACLE root is already 3.2e-5
+        # off on block 31 -- held to the north star's 1e-3 (3xTF32 had 6.2e-3 there, r02c)
+        bar = 1e-4 if two_sided else 1e-3
+        assert err < bar, (bi, err)
+        # scale = sqrt(num) / ||P||_F: its relative error is bounded by P's
+        assert abs(run["sc"][bi] - run["sc_o"][bi]) <= bar * run["sc_o"][bi], bi
 
 
 # ------------------------------------------------------------------ helpers
