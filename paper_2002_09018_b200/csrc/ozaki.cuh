@@ -441,6 +441,7 @@ struct OzArgs {
   int p;
   double* errh;
   int max_iter, kcheck;
+  const int* kdev;          // non-null (the convergence-driven tail graph): the iteration index is *kdev, kcheck = *kdev + 1
 };
 
 TC_DEV int oz_tiles_per_mat(const OzArgs& a) {
@@ -499,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   constexpr int kAPlane = C::kAPlane, kBPlane = C::kBPlane;
   const int na = a.act ? *a.nact : a.batch;
   if (na == 0) return;
+  const int kcheck = a.kdev ? *a.kdev + 1 : a.kcheck;
   const int per_mat = oz_tiles_per_mat(a);
   const int64_t total = (int64_t)na * per_mat * a.jobs;
   extern __shared__ uint8_t smem_raw[];
@@ -747,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
         if (ovf)  // the a-priori bound failed: poison this matrix's next err check (status 2, never silent)
-          atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + a.kcheck),
+          atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + kcheck),
                     0x7FF8000000000000ull);
       } else if (J.outf) {
         // fp32 output (a8, one-sided blocks: P_b = G_b X_R; non-symmetric tiles, no mirror)
@@ -823,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) emax_bits = umax64(emax_bits, __shfl_xor_sync(0xffffffffu, emax_bits, o));
         if (lane == 0)
-          atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + a.kcheck),
+          atomicMax(reinterpret_cast<unsigned long long*>(a.errh + (int64_t)mat * (a.max_iter + 1) + kcheck),
                     emax_bits);
       }
       acc_phase ^= 1;

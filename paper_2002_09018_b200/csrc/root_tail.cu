@@ -20,6 +20,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
 #include <cstring>
 
 #include "common.cuh"
@@ -339,8 +341,9 @@ TC_DEV int tail_decide(const double* errh, int max_iter, double tol, double stag
   return TD_CONTINUE;
 }
 
-__global__ void __launch_bounds__(1024) root_tail_decide_kernel(int* act, int* nact, const double* errh, int max_iter,
-                                                                double tol, double stag, int k) {
+// Ordered compaction of the active list after check k (one CTA of 1024 threads); returns the new count.
+__device__ int tail_decide_block(int* act, int* nact, const double* errh, int max_iter, double tol, double stag,
+                                 int k) {
   __shared__ int cnt[1025];
   __shared__ int s_act[kTailMaxBatch];
   const int n = *nact;
@@ -368,6 +371,28 @@ __global__ void __launch_bounds__(1024) root_tail_decide_kernel(int* act, int* n
   __syncthreads();
   for (int q = 0; q < nm; ++q) act[cnt[threadIdx.x] + q] = mine[q];
   if (threadIdx.x == 0) *nact = cnt[1024];
+  return cnt[1024];
+}
+
+__global__ void __launch_bounds__(1024) root_tail_decide_kernel(int* act, int* nact, const double* errh, int max_iter,
+                                                                double tol, double stag, int k) {
+  tail_decide_block(act, nact, errh, max_iter, tol, stag, k);
+}
+
+// The convergence-driven tail (CUDA graph with a conditional WHILE node): the iteration index lives in *kdev
+// (the products of iteration *kdev wrote err_{*kdev + 1}); after the decision *kdev advances, and the last decide
+// of the loop body sets the loop condition: another body only while matrices remain active.
+__global__ void __launch_bounds__(1024) root_tail_decide_graph_kernel(int* act, int* nact, const double* errh,
+                                                                      int max_iter, double tol, double stag,
+                                                                      int* kdev, cudaGraphConditionalHandle h,
+                                                                      int set_cond) {
+  const int k = *kdev + 1;
+  __syncthreads();  // every thread has read *kdev before thread 0 advances it
+  const int left = tail_decide_block(act, nact, errh, max_iter, tol, stag, k);
+  if (threadIdx.x == 0) {
+    *kdev = k;
+    if (set_cond) cudaGraphSetConditional(h, (left > 0 && k < max_iter) ? 1u : 0u);
+  }
 }
 
 // Final decisions of the handed-off matrices (res.x == -3) and the fp32 output:
@@ -523,7 +548,28 @@ size_t root_ozaki_ws_bytes(int batch, int n) {
   const size_t np = (size_t)((n + 63) / 64 * 64);
   const size_t planes = (size_t)OZ_SLOTS * batch * oz::kSMax * np * np;
   const size_t scales = (size_t)OZ_SLOTS * batch * np * sizeof(double);
-  return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap);
+  return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap) + 256;
+}
+
+// Iterations enqueued one launch at a time before the convergence-driven tail graph takes over: the scalar
+// recurrence m <- m ((p+1-m)/p)^p of the smallest eigenvalue of M from m_0 = eps_rel/(1+eps_rel) until |1 - m| <=
+// tol (the iteration count of the worst-conditioned matrix the ridge allows), + 2; then up to where the slice
+// schedule has settled (the tail graph runs one slice count) and even (its two-iteration body keeps the X / M
+// ping-pong parity static).  No ridge: everything direct.
+static int ozaki_direct_iterations(int p, int n, double eps_rel, double tol, int max_iter, double budget,
+                                   int s_max) {
+  if (!(eps_rel > 0.0)) return max_iter;
+  double m = eps_rel / (1.0 + eps_rel);
+  int k = 0;
+  while (k < max_iter && std::fabs(1.0 - m) > tol) {
+    m = m * std::pow(((double)(p + 1) - m) / (double)p, (double)p);
+    ++k;
+  }
+  k += 2;
+  const int s_floor = ozaki_iteration_slices(1000, p, n, eps_rel, budget, s_max);
+  while (k < max_iter && ozaki_iteration_slices(k, p, n, eps_rel, budget, s_max) != s_floor) ++k;
+  if (k & 1) ++k;
+  return std::min(k, max_iter);
 }
 
 // Slice count of iteration k (reading #29): an error made in M_k reaches the
@@ -596,6 +642,58 @@ static void oz_slice_mt(int S, const double* src, int64_t mstride, int n, int np
   }
 }
 
+// A non-blocking stream per device to capture the tail graph's body into (never destroyed).
+static cudaStream_t capture_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
+// Builds, launches on `stream` and releases a graph of one conditional WHILE node whose body is captured from
+// body(capture_stream, handle); the handle is set on the device (root_tail_decide_graph_kernel).  The executable
+// graph is destroyed right after its launch (freed when the launch completes).
+template <class Body>
+static int ozaki_tail_graph(cudaStream_t stream, Body body) {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return set_cuda_error("cudaGraphCreate");
+  cudaGraphConditionalHandle h;
+  cudaGraphNodeParams prm = {};
+  prm.type = cudaGraphNodeTypeConditional;
+  cudaGraphNode_t node;
+  int rc = SHAMPOO_OK;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+    rc = set_cuda_error("cudaGraphConditionalHandleCreate");
+  } else {
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    if (cudaGraphAddNode(&node, g, nullptr, 0, &prm) != cudaSuccess) rc = set_cuda_error("cudaGraphAddNode(while)");
+  }
+  if (rc == SHAMPOO_OK) {
+    cudaGraph_t bodyg = prm.conditional.phGraph_out[0];
+    cudaStream_t cs = capture_stream();
+    if (cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      rc = set_cuda_error("cudaStreamBeginCaptureToGraph");
+    } else {
+      rc = body(cs, h);
+      cudaGraph_t captured = nullptr;
+      cudaError_t e = cudaStreamEndCapture(cs, &captured);
+      if (rc == SHAMPOO_OK && e != cudaSuccess) rc = set_cuda_error("cudaStreamEndCapture", e);
+    }
+  }
+  if (rc == SHAMPOO_OK && cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) rc = set_cuda_error("cudaGraphInstantiate");
+  if (rc == SHAMPOO_OK && cudaGraphLaunch(ex, stream) != cudaSuccess) rc = set_cuda_error("cudaGraphLaunch");
+  if (ex) cudaGraphExecDestroy(ex);
+  cudaGraphDestroy(g);
+  return rc;
+}
+
 int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_iter, double tol, double* errh,
                       const int4* res, shampoo_root_info_t* info, float* X, int64_t ldx, int64_t stride_x, int* act,
                       int* nact, void* oz_ws, int slices, double eps_rel, double slice_budget, cudaStream_t stream,
@@ -636,21 +734,6 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   const int64_t mstride = (int64_t)kTailRegions * np * np;
   auto region = [&](int r) { return bufs + (int64_t)r * np * np; };
   // tm: slice T_k = ((p+1)I - M_k)/p computed from M_k on the fly (T_k never stored in fp64)
-  auto slice = [&](int S, int reg, int slot, bool tm) {
-    oz_slice(S, tm, region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(slot), slot_scale(slot), p, stream);
-    ++*launches;
-  };
-  // M_k and T_k in one pass over M_k (rows up to 1024 in registers), else two passes
-  auto slice_mt = [&](int S, int reg) {
-    if (n <= 1024) {
-      oz_slice_mt(S, region(reg), mstride, n, np, batch, act, nact, slot_planes_ptr(OZ_SM), slot_scale(OZ_SM),
-                  slot_planes_ptr(OZ_ST), slot_scale(OZ_ST), p, stream);
-      ++*launches;
-    } else {
-      slice(S, reg, OZ_SM, false);
-      slice(S, reg, OZ_ST, true);
-    }
-  };
   oz::OzArgs base;
   std::memset(&base, 0, sizeof base);
   base.act = act;
@@ -695,76 +778,124 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
     j.out_e = e;
     return j;
   };
-  auto gemm = [&](int S, const oz::OzArgs& a) -> int {
-    void* tok;
-    prof_begin_launch("ozaki_gemm", stream, &tok);
-    cudaError_t e = oz_gemm(S, a, maps_dev, stream);
-    prof_end_launch(tok, stream);
+  // one iteration's launches on stream `st`: k = the iteration (direct) or, with kdev, its parity only (the tail
+  // graph's body reads k from *kdev); `prof`: bracket the GEMMs with CUDA events (not inside a graph)
+  int* kdev = reinterpret_cast<int*>(maps_dev + 2 * OZ_SLOTS);
+  auto gemm = [&](int S, const oz::OzArgs& a, cudaStream_t st, bool prof) -> int {
+    void* tok = nullptr;
+    if (prof) prof_begin_launch("ozaki_gemm", st, &tok);
+    cudaError_t e = oz_gemm(S, a, maps_dev, st);
+    if (prof) prof_end_launch(tok, st);
     if (e != cudaSuccess) return set_cuda_error("ozaki gemm launch", e);
     ++*launches;
     return SHAMPOO_OK;
   };
   enum { RX0 = 0, RX1 = 1, RM0 = 2, RM1 = 3, RT = 4, RS0 = 5, RS1 = 6 };  // root.cu regions
   const int lead = 31 - __builtin_clz((unsigned)p);
-  int rc = SHAMPOO_OK;
-  for (int k = 0; k < max_iter && rc == SHAMPOO_OK; ++k) {
+  auto iteration = [&](int k, int S, int Sx, cudaStream_t st, const int* kd) -> int {
+    const bool prof = kd == nullptr;
     const int xs = k & 1;
-    // slices of this iteration's products (reading #29); the X-update reads the leading Sx planes of T
-    const int S = ozaki_iteration_slices(k, p, n, eps_rel, slice_budget, slices);
-    const int Sx = slice_budget > 0.0 ? std::min(S, kOzSX) : S;
-    slice(Sx, RX0 + xs, OZ_SX, false);
-    slice_mt(S, RM0 + xs);  // M_k and T_k = ((p+1)I - M_k)/p
-    // P1: X_{k+1} = X_k T (fp64) ; then S0 = T T (p >= 2; sliced in the epilogue).  Two launches: a stage
-    // whose jobs take different epilogue paths was measured 17-18 ms against 6 + 6 ms for the two alone
-    // (the alternating paths thrash the instruction cache)
-    oz::OzArgs a1 = base;
-    a1.kcheck = k + 1;
+    oz_slice(Sx, false, region(RX0 + xs), mstride, n, np, batch, act, nact, slot_planes_ptr(OZ_SX), slot_scale(OZ_SX),
+             p, st);
+    ++*launches;
+    if (n <= 1024) {  // M_k and T_k = ((p+1)I - M_k)/p in one pass over M_k (rows up to 1024 in registers)
+      oz_slice_mt(S, region(RM0 + xs), mstride, n, np, batch, act, nact, slot_planes_ptr(OZ_SM), slot_scale(OZ_SM),
+                  slot_planes_ptr(OZ_ST), slot_scale(OZ_ST), p, st);
+      ++*launches;
+    } else {
+      oz_slice(S, false, region(RM0 + xs), mstride, n, np, batch, act, nact, slot_planes_ptr(OZ_SM),
+               slot_scale(OZ_SM), p, st);
+      oz_slice(S, true, region(RM0 + xs), mstride, n, np, batch, act, nact, slot_planes_ptr(OZ_ST), slot_scale(OZ_ST),
+               p, st);
+      *launches += 2;
+    }
+    oz::OzArgs b0 = base;
+    b0.kcheck = k + 1;
+    b0.kdev = kd;
+    // P1: X_{k+1} = X_k T (fp64); then S0 = T T (p >= 2; sliced in the epilogue).  Two launches: a stage whose
+    // jobs take different epilogue paths was measured 17-18 ms against 6 + 6 ms for the two alone (the
+    // alternating paths thrash the instruction cache)
+    oz::OzArgs a1 = b0;
     a1.job[0] = job(OZ_SX, OZ_ST, RX0 + (xs ^ 1));
-    rc = gemm(Sx, a1);
-    if (rc) break;
+    int rc = gemm(Sx, a1, st, prof);
+    if (rc) return rc;
     if (p >= 2) {
-      oz::OzArgs a2 = a1;
+      oz::OzArgs a2 = b0;
       a2.job[0] = sliced_job(OZ_ST, OZ_ST, OZ_SS0, 2);
-      rc = gemm(S, a2);
-      if (rc) break;
+      rc = gemm(S, a2, st, prof);
+      if (rc) return rc;
     }
     int rb = RS0, sb = OZ_SS0, m = 2;
-    for (int bit = lead - 1; bit >= 0 && rc == SHAMPOO_OK; --bit) {
+    for (int bit = lead - 1; bit >= 0; --bit) {
       if (bit != lead - 1) {  // square
         const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
-        oz::OzArgs q = base;
-        q.kcheck = k + 1;
+        oz::OzArgs q = b0;
         q.job[0] = sliced_job(sb, sb, sd, 2 * m);
-        rc = gemm(S, q);
+        rc = gemm(S, q, st, prof);
+        if (rc) return rc;
         rb = rd;
         sb = sd;
         m *= 2;
       }
-      if (rc == SHAMPOO_OK && ((p >> bit) & 1)) {  // times T
+      if ((p >> bit) & 1) {  // times T
         const int rd = rb == RS0 ? RS1 : RS0, sd = sb == OZ_SS0 ? OZ_SS1 : OZ_SS0;
-        oz::OzArgs q = base;
-        q.kcheck = k + 1;
+        oz::OzArgs q = b0;
         q.job[0] = job(sb, OZ_ST, rd);  // A != B: fp64 output and the slice kernel
-        rc = gemm(S, q);
-        if (rc) break;
-        slice(S, rd, sd, false);
+        rc = gemm(S, q, st, prof);
+        if (rc) return rc;
+        oz_slice(S, false, region(rd), mstride, n, np, batch, act, nact, slot_planes_ptr(sd), slot_scale(sd), p, st);
+        ++*launches;
         rb = rd;
         sb = sd;
         m += 1;
       }
     }
-    if (rc) break;
     // P3: M_{k+1} = T^p M_k ; err_{k+1} = max|M_{k+1} - I|
-    oz::OzArgs a3 = base;
+    oz::OzArgs a3 = b0;
     a3.job[0] = job(p == 1 ? OZ_ST : sb, OZ_SM, RM0 + (xs ^ 1));
     a3.mupdate = 1;
-    a3.kcheck = k + 1;
-    rc = gemm(S, a3);
-    if (rc) break;
+    return gemm(S, a3, st, prof);
+  };
+  auto sched = [&](int k, int& S, int& Sx) {
+    // slices of iteration k's products (reading #29); the X-update reads the leading Sx planes of T
+    S = ozaki_iteration_slices(k, p, n, eps_rel, slice_budget, slices);
+    Sx = slice_budget > 0.0 ? std::min(S, kOzSX) : S;
+  };
+  // iterations 0 .. k_direct-1 one launch at a time (their slice counts may change), then the convergence-driven
+  // tail: a CUDA graph whose conditional WHILE node repeats a two-iteration body until the decide kernel finds no
+  // active matrix -- no host round trip, no launch after convergence (round 1 enqueued all max_iter iterations)
+  // SHAMPOO_OZAKI_DIRECT=1 (tests only): every iteration launched directly, for the bit-identity check of the tail
+  static const bool all_direct = [] {
+    const char* v = std::getenv("SHAMPOO_OZAKI_DIRECT");
+    return v && v[0] == '1';
+  }();
+  const int k_direct = all_direct ? max_iter : ozaki_direct_iterations(p, n, eps_rel, tol, max_iter, slice_budget, slices);
+  int rc = SHAMPOO_OK;
+  for (int k = 0; k < k_direct; ++k) {
+    int S, Sx;
+    sched(k, S, Sx);
+    rc = iteration(k, S, Sx, stream, nullptr);
+    if (rc) return rc;
     root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, tol, 1.0, k + 1);
     ++*launches;
   }
-  if (rc) return rc;
+  if (k_direct < max_iter) {
+    int S, Sx;
+    sched(k_direct, S, Sx);  // = the schedule's floor for every k >= k_direct
+    const int kd_host = k_direct;
+    if (cudaMemcpyAsync(kdev, &kd_host, sizeof(int), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+      return set_cuda_error("cudaMemcpyAsync(ozaki tail counter)");
+    rc = ozaki_tail_graph(stream, [&](cudaStream_t cs, cudaGraphConditionalHandle h) -> int {
+      for (int half = 0; half < 2; ++half) {
+        int r = iteration(half, S, Sx, cs, kdev);  // parity of k_direct + half (k_direct is even)
+        if (r) return r;
+        root_tail_decide_graph_kernel<<<1, 1024, 0, cs>>>(act, nact, errh, max_iter, tol, 1.0, kdev, h, half);
+        ++*launches;
+      }
+      return SHAMPOO_OK;
+    });
+    if (rc) return rc;
+  }
   root_tail_finish_kernel<<<batch, 128, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
                                                      0, tol, 1.0, RX0, RX1, 1);
   ++*launches;

@@ -168,3 +168,45 @@ def test_ozaki_power_bound_violation_is_flagged(shp, mode):
     assert inf[0]["status"] == 2 and np.all(X[0].cpu().numpy() == 7.0)
     Xo, io = oroot.inverse_pth_root(As[1].astype(np.float64), 4, power_iters=1)
     assert inf[1]["status"] == io.status and rel(X[1].cpu().numpy(), Xo) < 1e-4
+
+
+def test_ozaki_tail_graph_launches_and_bits():
+    """The convergence-driven tail (a CUDA graph with a conditional WHILE node after the a-priori iteration
+    estimate) replaces round 1's fixed max_iter launch loop: the roots, iteration counts and statuses are
+    bit-identical to launching every iteration directly (SHAMPOO_OZAKI_DIRECT=1, a fresh process), the launch
+    count drops from ~7 x max_iter to ~7 x the estimate, and matrices that need more iterations than the estimate
+    (tol = 0: stagnation after ~25) still run to their stopping rule inside the graph."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import hashlib, json, sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2002_09018_b200 as shp, synth
+out = {}
+for name, tol in (("default", 1e-7), ("tol0", 0.0)):
+    A = torch.from_numpy(synth.psd_batch(512, 6, 41, "mixed")).to("cuda:0")
+    X, info = shp.inverse_pth_root_batched(A, 4, fp64_iters="ozaki", tol=tol, max_iter=100)
+    n_launch = shp.last_launch_count()
+    torch.cuda.synchronize()
+    inf = shp.info_to_numpy(info)
+    out[name] = {"X": hashlib.sha256(X.cpu().numpy().tobytes()).hexdigest(),
+                 "iters": inf["iters"].tolist(), "status": inf["status"].tolist(), "launches": n_launch}
+print(json.dumps(out))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("graph", "direct"):
+        env = dict(os.environ)
+        env.pop("SHAMPOO_OZAKI_DIRECT", None)
+        if mode == "direct":
+            env["SHAMPOO_OZAKI_DIRECT"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name in ("default", "tol0"):
+        g, d = res["graph"][name], res["direct"][name]
+        print(name, "launches graph", g["launches"], "direct", d["launches"], "iters", g["iters"])
+        assert g["X"] == d["X"] and g["iters"] == d["iters"] and g["status"] == d["status"]
+    assert res["graph"]["default"]["launches"] < 0.35 * res["direct"]["default"]["launches"]
+    assert max(res["graph"]["tol0"]["iters"]) > 24  # ran past the direct iterations, inside the graph
