@@ -63,9 +63,10 @@ def _int8_peak():
         pass
     return 2 * 1687.1, "burst (earlier measurement; MEASURED_PEAKS.json absent)", 2 * 1687.1
 # dram read + write per Ozaki GEMM launch per 1024^2 matrix: the mean over the four product launches of one
-# iteration (X T 14.1 GB, T T sliced 8.5 GB, T^2 T^2 sliced 8.6 GB, T^4 M 12.8 GB for 528 matrices), ncu launch
-# list profiles/r01za_launches_root528_summary.txt
-OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = ((9.71 + 4.39) + (4.67 + 3.85) + (4.71 + 3.85) + (8.37 + 4.39)) / 4 * 1e9 / 528
+# iteration, from the ncu --set full capture of the round-2 kernel (profiles/r02/r02a_ncu_gemm7_full_summary.txt, 148
+# matrices): X T 3.377 GB, T T sliced 2.130 GB, T^2 T^2 sliced 2.132 GB, T^4 M 3.379 GB -> 22.8 / 14.4 / 14.4 / 22.8 MB per
+# matrix = the algorithmic planes + output (no re-reads); measured at S = 7 (fewer planes move at S = 5, 6)
+OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = (3.377 + 2.130 + 2.132 + 3.379) / 4 * 1e9 / 148
 # the arithmetic of the dominant phase (the roots): fp64 iterates, products per the root precision
 DTYPE = {"auto": "f64 iterates, int8 Ozaki products S=7..5 per iteration (exact int32 accumulation)",
          "auto7": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
@@ -433,7 +434,8 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
                 "frac": achieved / peak, "traffic": OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE * cnt,
                 "traffic_note": "dram read+write bytes per GEMM launch (mean of the 4 product launches of an "
-                                "iteration), ncu launch list of a 528-matrix root call scaled per matrix",
+                                "iteration at S = 7), ncu --set full of the same kernel (148 matrices) scaled to "
+                                "this batch: the algorithmic planes + output, no re-reads",
                 "kernel": f"oz::gemm_kernel (INT8 tcgen05 Ozaki products, batch {cnt} x {n}^2, p=4)",
                 "kernel_ms": float(working.mean()) if working.size else None,
                 "kernel_launches": int(working.size), "kernel_launches_total": gemm_launches,

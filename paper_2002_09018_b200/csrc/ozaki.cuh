@@ -48,7 +48,11 @@ struct Cfg {
   static constexpr int kAPlane = kBM * BK;                     // 8 KB (BK = 64)
   static constexpr int kBPlane = kBN * BK;                     // 4 KB
   static constexpr int kStageBytes = S * (kAPlane + kBPlane);  // 84 KB (S = 7, BK = 64), 72 KB (S = 6)
+#ifdef OZ_STAGES  // microbenchmark probes only
+  static constexpr int kStages = OZ_STAGES < (225 * 1024) / kStageBytes ? OZ_STAGES : (225 * 1024) / kStageBytes;
+#else
   static constexpr int kStages = (225 * 1024) / kStageBytes;   // as many as fit: 2 / 5 (S = 7), 3 / 6 (S = 6)
+#endif
 };
 constexpr int kThreads = 192;
 // Bound probes for tools/microbench/ozaki_test.cu only (the library builds with 0):

@@ -864,12 +864,23 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   // iterations 0 .. k_direct-1 one launch at a time (their slice counts may change), then the convergence-driven
   // tail: a CUDA graph whose conditional WHILE node repeats a two-iteration body until the decide kernel finds no
   // active matrix -- no host round trip, no launch after convergence (round 1 enqueued all max_iter iterations)
-  // SHAMPOO_OZAKI_DIRECT=1 (tests only): every iteration launched directly, for the bit-identity check of the tail
-  static const bool all_direct = [] {
+  // SHAMPOO_OZAKI_DIRECT (tests only): "all" -- every iteration launched directly; an integer k -- the tail graph
+  // from k on (rounded up to even and to the schedule's floor), for the bit-identity check of the tail
+  static const int direct_env = [] {
     const char* v = std::getenv("SHAMPOO_OZAKI_DIRECT");
-    return v && v[0] == '1';
+    if (!v || !*v) return -1;
+    if (std::strcmp(v, "all") == 0) return 1 << 30;
+    return std::atoi(v);
   }();
-  const int k_direct = all_direct ? max_iter : ozaki_direct_iterations(p, n, eps_rel, tol, max_iter, slice_budget, slices);
+  int k_direct = ozaki_direct_iterations(p, n, eps_rel, tol, max_iter, slice_budget, slices);
+  if (direct_env >= 0) {
+    const int s_floor = ozaki_iteration_slices(1000, p, n, eps_rel, slice_budget, slices);
+    k_direct = std::min(direct_env, max_iter);
+    while (k_direct < max_iter && ozaki_iteration_slices(k_direct, p, n, eps_rel, slice_budget, slices) != s_floor)
+      ++k_direct;
+    if (k_direct & 1) ++k_direct;
+    k_direct = std::min(k_direct, max_iter);
+  }
   int rc = SHAMPOO_OK;
   for (int k = 0; k < k_direct; ++k) {
     int S, Sx;

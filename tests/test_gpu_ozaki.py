@@ -172,10 +172,11 @@ def test_ozaki_power_bound_violation_is_flagged(shp, mode):
 
 def test_ozaki_tail_graph_launches_and_bits():
     """The convergence-driven tail (a CUDA graph with a conditional WHILE node after the a-priori iteration
-    estimate) replaces round 1's fixed max_iter launch loop: the roots, iteration counts and statuses are
-    bit-identical to launching every iteration directly (SHAMPOO_OZAKI_DIRECT=1, a fresh process), the launch
-    count drops from ~7 x max_iter to ~7 x the estimate, and matrices that need more iterations than the estimate
-    (tol = 0: stagnation after ~25) still run to their stopping rule inside the graph."""
+    estimate) replaces round 1's fixed max_iter launch loop.  In fresh processes: the default call launches ~7 x the
+    estimate instead of ~7 x max_iter kernels with the roots, iteration counts and statuses of launching every
+    iteration directly (SHAMPOO_OZAKI_DIRECT=all); and with the graph taking over at iteration 6
+    (SHAMPOO_OZAKI_DIRECT=6, fixed 7 slices) the matrices iterate ~14 more times INSIDE the graph, still bit-identical
+    to the direct launches."""
     import json
     import os
     import subprocess
@@ -185,9 +186,9 @@ import hashlib, json, sys, numpy as np, torch
 sys.path.insert(0, %r)
 import paper_2002_09018_b200 as shp, synth
 out = {}
-for name, tol in (("default", 1e-7), ("tol0", 0.0)):
+for name, mode in (("sched", "ozaki"), ("fixed7", "ozaki7")):
     A = torch.from_numpy(synth.psd_batch(512, 6, 41, "mixed")).to("cuda:0")
-    X, info = shp.inverse_pth_root_batched(A, 4, fp64_iters="ozaki", tol=tol, max_iter=100)
+    X, info = shp.inverse_pth_root_batched(A, 4, fp64_iters=mode, max_iter=100)
     n_launch = shp.last_launch_count()
     torch.cuda.synchronize()
     inf = shp.info_to_numpy(info)
@@ -196,17 +197,20 @@ for name, tol in (("default", 1e-7), ("tol0", 0.0)):
 print(json.dumps(out))
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for mode in ("graph", "direct"):
+    for env_val in (None, "all", "6"):
         env = dict(os.environ)
         env.pop("SHAMPOO_OZAKI_DIRECT", None)
-        if mode == "direct":
-            env["SHAMPOO_OZAKI_DIRECT"] = "1"
+        if env_val:
+            env["SHAMPOO_OZAKI_DIRECT"] = env_val
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
-        res[mode] = json.loads(r.stdout.strip().splitlines()[-1])
-    for name in ("default", "tol0"):
-        g, d = res["graph"][name], res["direct"][name]
+        res[env_val] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name in ("sched", "fixed7"):
+        g, d = res[None][name], res["all"][name]
         print(name, "launches graph", g["launches"], "direct", d["launches"], "iters", g["iters"])
         assert g["X"] == d["X"] and g["iters"] == d["iters"] and g["status"] == d["status"]
-    assert res["graph"]["default"]["launches"] < 0.35 * res["direct"]["default"]["launches"]
-    assert max(res["graph"]["tol0"]["iters"]) > 24  # ran past the direct iterations, inside the graph
+        assert g["launches"] < 0.35 * d["launches"]
+    early, d = res["6"]["fixed7"], res["all"]["fixed7"]
+    print("graph from k = 6: launches", early["launches"], "iters", early["iters"])
+    assert early["X"] == d["X"] and early["iters"] == d["iters"] and early["status"] == d["status"]
+    assert min(early["iters"]) > 6 and early["launches"] < res[None]["fixed7"]["launches"]

@@ -3,8 +3,6 @@
 T=${1:-r02x}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 60 tools/microbench/bin/cg_probe > $O/cg_probe.log 2>&1; echo "exit $?" >> $O/cg_probe.log
-timeout 1500 python -m pytest tests -m gpu -q -rA -s > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
-timeout 600 python bench.py --steps 5 --warmup 3 > $O/bench_n1.json 2> $O/bench_n1.err
+for P in stages2 stages3 stagesmax; do timeout 300 tools/microbench/bin/oz_$P > $O/oz_$P.log 2>&1; done
+timeout 900 python -m pytest tests/test_gpu_ozaki.py -q -rA -s -k "tail or 2048 or 1024" > $O/pytest_ozaki.log 2>&1; echo "pytest exit $?" >> $O/pytest_ozaki.log
 echo done > $O/DONE

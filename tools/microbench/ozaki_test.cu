@@ -180,7 +180,15 @@ static int run(int n, int batch, bool sym, int reps) {
 
 int main() {
   int bad = 0;
-#if OZ_PROBE
+#if OZ_PROBE == 9
+  // stage-count / k-chunk probes (OZ_STAGES): correct results, timing of S = 5..7 at n = 1024, 148 matrices
+  bad |= run<7, 32>(1024, 148, true, 3);
+  bad |= run<5, 64>(1024, 148, true, 3);
+  bad |= run<5, 32>(1024, 148, true, 3);
+  bad |= run<6, 32>(1024, 148, true, 3);
+  printf(bad ? "FAIL\n" : "PASS\n");
+  return bad;
+#elif OZ_PROBE
   // bound probes: timing only (results are meaningless), n = 1024, 148 matrices, symmetric
   run<7>(1024, 148, true, 3);
   run<6>(1024, 148, true, 3);
