@@ -132,8 +132,8 @@ int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, i
 /* Layer-granular variant (reading #30; "As preconditioners need to be
  * computed for every layer of the network, we distribute the computation across
  * all the CPUs"): every root of tensor t is owned by tensor_owner[t], the tensors
- * assigned LPT -- sorted by (cost desc, index), cost = sum of the tensor's root
- * costs (n^3 x products per iteration) + m*n, each to the least-loaded rank
+ * assigned LPT -- sorted by (cost desc, index), cost = sum over the tensor's roots
+ * of n^3 x (products per iteration + 4) + m*n, each to the least-loaded rank
  * (lowest on ties).  Packing as shampoo_plan.  An owner then holds whole tensors:
  * their statistics, roots and preconditioned gradient, so the multi-GPU step
  * exchanges P (one all-gather) instead of the roots.

@@ -23,9 +23,11 @@ Rule (DESIGN.md §3 readings #5, #12, #13, #17):
   ties) -- "we distribute the computation across all the CPUs" (P:300-303).
   owners="tensor" (reading #30, "As preconditioners need to be computed for
   every layer of the network, we distribute the computation"):
-  tensors sorted by (-cost_t, t) with cost_t = sum of the tensor's root costs
-  + m*n, each assigned to the least-loaded rank (lowest on ties); every root
-  of tensor t is owned by t's owner.
+  tensors sorted by (-cost_t, t) with cost_t = sum over the tensor's roots of
+  n^3 (products_per_iteration(p) + 4) + m*n (the +4: per-iteration work that
+  does not scale with the products, fitted to measured per-root times), each
+  assigned to the least-loaded rank (lowest on ties); every root of tensor t is
+  owned by t's owner.
 * Packing: one fp32 buffer holds all statistics (and, at the same offsets,
   all roots).  Rank r's segment holds the roots it owns, grouped by (n desc,
   p desc, r desc), each matrix ``n x ld`` with ``ld = roundup(n, 4)`` and a group
@@ -140,8 +142,10 @@ def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(
     tensor_owner = None
     if owners == "tensor":
         tcost = [m * n for (m, n) in shapes]
-        for cost, t, _b, _s in roots:
-            tcost[t] += cost
+        for _cost, t, bidx, side in roots:
+            b = out.blocks[bidx]
+            nn, pp = (b.rows, b.p_left) if side == 0 else (b.cols, b.p_right)
+            tcost[t] += nn ** 3 * (products_per_iteration(pp) + 4)
         tload = [0] * world_size
         tensor_owner = [0] * len(shapes)
         for t in sorted(range(len(shapes)), key=lambda t: (-tcost[t], t)):
