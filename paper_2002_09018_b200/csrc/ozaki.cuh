@@ -265,30 +265,19 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
   }
 }
 
-// Digits of 8 consecutive row elements stored into the S planes (out of line: the
-// fused M/T slicer calls it twice per chunk, and its temporaries must not stay live
-// across the chunks held in registers).
+// M_k and T_k = ((p+1)I - M_k)/p sliced in ONE pass over M_k (rows of n <= 1024): saves the second 8 MB read
+// per matrix of separate M and T slicers.  Each warp stages its row in shared memory (8 KB; one HBM pass, all
+// of the row's loads in flight at once), then slices M and T chunk by chunk from there: only 8 elements live in
+// registers at a time (round 1 held the whole row in registers and spilled; 50-55% of HBM bandwidth).
+constexpr int kSliceMtWarps = 4;
 template <int S>
-__device__ __noinline__ void slice_store8(double r0, double r1, double r2, double r3, double r4, double r5,
-                                          double r6, double r7, double scl, int8_t* dst, int64_t plane_pitch,
-                                          int j, int n) {
-  const double r[8] = {r0, r1, r2, r3, r4, r5, r6, r7};
-  uint32_t dig[S][2];
-  slice8<S>(r, scl, dig);
-#pragma unroll
-  for (int s = 0; s < S; ++s) store8<S>(dst + s * plane_pitch, j, n, dig[s]);
-}
-
-// M_k and T_k = ((p+1)I - M_k)/p sliced in ONE pass over M_k (rows of n <= 1024 held
-// in registers): saves the second 8 MB read per matrix of separate M and T slicers.
-template <int S>
-__global__ void __launch_bounds__(256, 2) slice_mt_kernel(const double* __restrict__ src, int64_t mat_stride, int n,
-                                                          int np, int batch, const int* __restrict__ act,
-                                                          const int* nact, int8_t* __restrict__ planes_m,
-                                                          double* __restrict__ scale_m, int8_t* __restrict__ planes_t,
-                                                          double* __restrict__ scale_t, int p) {
-  constexpr int kRegChunks = 4;
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32 * kSliceMtWarps, 4) slice_mt_kernel(
+    const double* __restrict__ src, int64_t mat_stride, int n, int np, int batch, const int* __restrict__ act,
+    const int* nact, int8_t* __restrict__ planes_m, double* __restrict__ scale_m, int8_t* __restrict__ planes_t,
+    double* __restrict__ scale_t, int p) {
+  __shared__ __align__(16) double srow[kSliceMtWarps][1024];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* my = srow[wib];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = act ? *nact : batch;
@@ -300,21 +289,29 @@ __global__ void __launch_bounds__(256, 2) slice_mt_kernel(const double* __restri
     const double* row = src + mat * mat_stride + (int64_t)i * np;
     const int64_t prow = ((int64_t)mat * kSMax * np + i) * np;
     const double tii = t_of(row[i], true, pp1, inv_p);
-    double r[kRegChunks][8];
     double mx = 0.0, mo = 0.0;  // max |M_ij| over the row, and over the row without the diagonal
+    {
+      double r[4][8];
 #pragma unroll
-    for (int c = 0; c < kRegChunks; ++c) {
-      const int j = 256 * c + 8 * lane;
-      if (j < n) {
-        load8(row, j, n, r[c]);
-      } else {
+      for (int c = 0; c < 4; ++c) {
+        const int j = 256 * c + 8 * lane;
+        if (j < n) {
+          load8(row, j, n, r[c]);
+        } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) r[c][q] = 0.0;
+          for (int q = 0; q < 8; ++q) r[c][q] = 0.0;
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        mx = fmax(mx, fabs(r[c][q]));
-        mo = fmax(mo, (j + q == i) ? 0.0 : fabs(r[c][q]));
+      for (int c = 0; c < 4; ++c) {
+        const int j = 256 * c + 8 * lane;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          mx = fmax(mx, fabs(r[c][q]));
+          mo = fmax(mo, (j + q == i) ? 0.0 : fabs(r[c][q]));
+        }
+        reinterpret_cast<double4*>(my + j)[0] = make_double4(r[c][0], r[c][1], r[c][2], r[c][3]);
+        reinterpret_cast<double4*>(my + j)[1] = make_double4(r[c][4], r[c][5], r[c][6], r[c][7]);
       }
     }
     const int e = row_exponent(mx);
@@ -325,18 +322,27 @@ __global__ void __launch_bounds__(256, 2) slice_mt_kernel(const double* __restri
       scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
     }
     const double sm = digit_scale<S>(e), st = digit_scale<S>(et);
-#pragma unroll
-    for (int c = 0; c < kRegChunks; ++c) {
+    __syncwarp();
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
       const int j = 256 * c + 8 * lane;
       if (j < n) {
-        slice_store8<S>(r[c][0], r[c][1], r[c][2], r[c][3], r[c][4], r[c][5], r[c][6], r[c][7], sm,
-                        planes_m + prow, plane_pitch, j, n);
-        double t[8];
+        double r[8];
+        const double4 a0 = reinterpret_cast<const double4*>(my + j)[0];
+        const double4 a1 = reinterpret_cast<const double4*>(my + j)[1];
+        r[0] = a0.x; r[1] = a0.y; r[2] = a0.z; r[3] = a0.w; r[4] = a1.x; r[5] = a1.y; r[6] = a1.z; r[7] = a1.w;
+        uint32_t dig[S][2];
+        slice8<S>(r, sm, dig);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = (j + q == i) ? tii : r[c][q] * ninv_p;
-        slice_store8<S>(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], st, planes_t + prow, plane_pitch, j, n);
+        for (int s = 0; s < S; ++s) store8<S>(planes_m + prow + s * plane_pitch, j, n, dig[s]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = (j + q == i) ? tii : r[q] * ninv_p;
+        slice8<S>(r, st, dig);
+#pragma unroll
+        for (int s = 0; s < S; ++s) store8<S>(planes_t + prow + s * plane_pitch, j, n, dig[s]);
       }
     }
+    __syncwarp();  // the row buffer is rewritten by the next row
   }
 }
 

@@ -630,7 +630,7 @@ static void oz_slice(int S, bool tm, const double* src, int64_t mstride, int n, 
 template <int S>
 static void oz_slice_mt_s(const double* src, int64_t mstride, int n, int np, int batch, const int* act,
                           const int* nact, int8_t* pm, double* sm, int8_t* pt, double* st, int p, cudaStream_t stream) {
-  oz::slice_mt_kernel<S><<<8 * num_sms(), 256, 0, stream>>>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p);
+  oz::slice_mt_kernel<S><<<4 * num_sms(), 32 * oz::kSliceMtWarps, 0, stream>>>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p);
 }
 
 static void oz_slice_mt(int S, const double* src, int64_t mstride, int n, int np, int batch, const int* act,
