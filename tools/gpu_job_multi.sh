@@ -12,7 +12,8 @@ fi
 R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29533"
 timeout 600 $R tools/check_multi_gpu.py --full --shard layers > $O/check_layers_n$N.txt 2>&1; echo "exit $?" >> $O/check_layers_n$N.txt
 timeout 600 $R tools/check_multi_gpu.py --shard roots > $O/check_roots_n$N.txt 2>&1; echo "exit $?" >> $O/check_roots_n$N.txt
-timeout 600 python bench.py --steps 5 --warmup 3 > $O/bench_n1.json 2> $O/bench_n1.err
+timeout 600 $R tools/check_delayed_multi.py > $O/check_delayed_n$N.txt 2>&1; echo "exit $?" >> $O/check_delayed_n$N.txt
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_n1.json 2> $O/bench_n1.err
 timeout 900 $R bench.py --gpus $N --steps 5 --warmup 3 --shard layers > $O/bench_n${N}_layers.json 2> $O/bench_n${N}_layers.err
 timeout 900 $R bench.py --gpus $N --steps 5 --warmup 3 --shard roots > $O/bench_n${N}_roots.json 2> $O/bench_n${N}_roots.err
 echo done > $O/DONE
