@@ -267,6 +267,20 @@ int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t 
                                            double slice_budget, shampoo_root_info_t* info, void* workspace,
                                            size_t workspace_bytes, shampoo_stream_t stream);
 
+/* Precision "auto" (the bench's): the Ozaki root above (slices, slice_budget)
+ * for n >= SHAMPOO_OZAKI_MIN_N, shampoo_inverse_pth_root_batched (FP64 DMMA)
+ * below -- the Ozaki loop launches ~7 kernels per iteration and tiles 128 rows,
+ * which small matrices cannot fill (measured on B200: n = 128 Ozaki 19k vs
+ * FP64 72k roots/s; n = 512 2.7k vs 2.5k; n = 1024 580 vs 354).  Arguments as
+ * the Ozaki call; workspace >= shampoo_root_auto_workspace_bytes(...). */
+#define SHAMPOO_OZAKI_MIN_N 512
+size_t shampoo_root_auto_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter);
+int shampoo_inverse_pth_root_batched_auto(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                          int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                          double tol, int32_t max_iter, int32_t power_iters, int32_t slices,
+                                          double slice_budget, shampoo_root_info_t* info, void* workspace,
+                                          size_t workspace_bytes, shampoo_stream_t stream);
+
 /* Independent root check (config 2, north-star invariant):
  *   residual_i = || X_i^p (A_i + eps_rel*lambda_i*I) - I ||_F   in fp64,
  * lambda_i = info[i].lambda_max from the root call.  out: double[batch]. */

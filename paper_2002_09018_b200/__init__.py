@@ -195,8 +195,17 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
     fp64_iters="auto" / "auto7" / "auto6": "ozaki" / "ozaki7" / "ozaki6" for n >= OZAKI_MIN_N, FP64 DMMA below.
     ws_tag: workspace cache key -- calls that may run concurrently on different streams need different tags."""
     L = _lib.lib()
-    if fp64_iters in ("auto", "auto6", "auto7"):  # the INT8 Ozaki loop pays off from n = 512 (launches, 128-row tiles)
-        fp64_iters = ("ozaki" + fp64_iters[4:]) if (n >= OZAKI_MIN_N and r == 1) else None
+    if fp64_iters in ("auto", "auto6", "auto7") and r == 1:  # the library picks Ozaki (n >= 512) or FP64 DMMA
+        slices = int(fp64_iters[4:] or 7)
+        budget = SLICE_BUDGET if fp64_iters == "auto" else 0.0
+        wsb = L.shampoo_root_auto_workspace_bytes(batch, n, p, max_iter)
+        ws = workspace(wsb, device if device is not None else info.device, ws_tag)
+        check(L.shampoo_inverse_pth_root_batched_auto(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
+                                                      tol, max_iter, power_iters, slices, budget, info.data_ptr(),
+                                                      ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+        return
+    if fp64_iters in ("auto", "auto6", "auto7"):  # rational roots (r > 1): the FP64 path
+        fp64_iters = None
     if isinstance(fp64_iters, str) and fp64_iters.startswith("ozaki"):
         slices = int(fp64_iters[5:] or 7)
         budget = SLICE_BUDGET if fp64_iters == "ozaki" else 0.0
@@ -279,7 +288,7 @@ def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.
 _refresh_launches = 0
 # smallest n for which precision "auto" picks the Ozaki root (measured on B200: n = 128 ozaki 19k roots/s vs
 # FP64 DMMA 72k; n = 512 2.7k vs 2.5k; n = 1024 580 vs 354 -- profiles/r01t_*)
-OZAKI_MIN_N = 512
+OZAKI_MIN_N = 512  # = SHAMPOO_OZAKI_MIN_N of include/shampoo.h (the library's "auto" switch; for reporting)
 # per-iteration slice schedule of the Ozaki root (reading #29, shampoo.h slice_budget): iteration k takes the fewest
 # slices S in [5, 7] with 2^-(7S-1) sqrt(n/1024) / (p min(1, eps_rel g^k)) <= SLICE_BUDGET (host emulation at n = 1024, p = 4,
 # kappa 1e6: 0.68 of the fixed-7 slice products, root error 2.9e-7 vs 1.2e-7; tools/ozaki_schedule.py)

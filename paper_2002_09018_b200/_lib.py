@@ -40,7 +40,8 @@ EXPORTED = [
     "shampoo_root_workspace_bytes", "shampoo_inverse_pth_root_batched", "shampoo_inverse_root_rational_batched",
     "shampoo_inverse_pth_root_batched_hybrid", "shampoo_root_ozaki_workspace_bytes",
     "shampoo_inverse_pth_root_batched_ozaki", "shampoo_profile_begin", "shampoo_profile_end",
-    "shampoo_profile_launch_ms", "shampoo_ozaki_iteration_slices",
+    "shampoo_profile_launch_ms", "shampoo_ozaki_iteration_slices", "shampoo_root_auto_workspace_bytes",
+    "shampoo_inverse_pth_root_batched_auto",
     "shampoo_root_residual_workspace_bytes", "shampoo_root_residual_batched",
     "shampoo_precondition_workspace_bytes", "shampoo_precondition", "shampoo_precondition_split",
     "shampoo_tf32_split",
@@ -100,6 +101,10 @@ def lib():
     L.shampoo_inverse_pth_root_batched_ozaki.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl,
                                                          _dbl, _i32, _i32, _i32, _dbl, _vp, _vp, _sz, _vp]
     L.shampoo_inverse_pth_root_batched_ozaki.restype = ctypes.c_int
+    L.shampoo_root_auto_workspace_bytes.argtypes = [_i32, _i32, _i32, _i32]
+    L.shampoo_root_auto_workspace_bytes.restype = _sz
+    L.shampoo_inverse_pth_root_batched_auto.argtypes = L.shampoo_inverse_pth_root_batched_ozaki.argtypes
+    L.shampoo_inverse_pth_root_batched_auto.restype = ctypes.c_int
     L.shampoo_root_residual_workspace_bytes.argtypes = [_i32, _i32, _i32]
     L.shampoo_root_residual_workspace_bytes.restype = _sz
     L.shampoo_root_residual_batched.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i32, _i32, _dbl, _vp, _vp,

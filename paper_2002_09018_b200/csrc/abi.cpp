@@ -282,6 +282,24 @@ int shampoo_inverse_pth_root_batched_ozaki(const float* A, int64_t lda, int64_t 
                     workspace, workspace_bytes, stream, 2, slices, slice_budget);
 }
 
+size_t shampoo_root_auto_workspace_bytes(int32_t batch, int32_t n, int32_t p, int32_t max_iter) {
+  return n >= SHAMPOO_OZAKI_MIN_N ? shampoo_root_ozaki_workspace_bytes(batch, n, p, max_iter)
+                                  : shampoo_root_workspace_bytes(batch, n, p, max_iter);
+}
+
+int shampoo_inverse_pth_root_batched_auto(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
+                                          int64_t stride_x, int32_t batch, int32_t n, int32_t p, double eps_rel,
+                                          double tol, int32_t max_iter, int32_t power_iters, int32_t slices,
+                                          double slice_budget, shampoo_root_info_t* info, void* workspace,
+                                          size_t workspace_bytes, shampoo_stream_t stream) {
+  if (n >= SHAMPOO_OZAKI_MIN_N)
+    return shampoo_inverse_pth_root_batched_ozaki(A, lda, stride_a, X, ldx, stride_x, batch, n, p, eps_rel, tol,
+                                                  max_iter, power_iters, slices, slice_budget, info, workspace,
+                                                  workspace_bytes, stream);
+  return shampoo_inverse_pth_root_batched(A, lda, stride_a, X, ldx, stride_x, batch, n, p, eps_rel, tol, max_iter,
+                                          power_iters, info, workspace, workspace_bytes, stream);
+}
+
 int shampoo_inverse_root_rational_batched(const float* A, int64_t lda, int64_t stride_a, float* X, int64_t ldx,
                                           int64_t stride_x, int32_t batch, int32_t n, int32_t p, int32_t r,
                                           double eps_rel, double tol, int32_t max_iter, int32_t power_iters,

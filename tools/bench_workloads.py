@@ -33,7 +33,8 @@ import paper_2002_09018_b200 as shp  # noqa: E402
 import synth  # noqa: E402
 
 
-MODE = {"auto": "auto", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki6": "ozaki6", "hybrid": -1}
+MODE = {"auto": "auto", "auto7": "auto7", "auto6": "auto6", "fp64": None, "ozaki": "ozaki", "ozaki7": "ozaki7",
+        "ozaki6": "ozaki6", "hybrid": -1}
 
 
 def timed(fn, steps, warmup, stream):
