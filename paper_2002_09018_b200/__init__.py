@@ -48,13 +48,17 @@ def _stream_ptr(stream=None) -> int:
 _WS: dict = {}
 
 
-def workspace(nbytes: int, device, tag: str = "default") -> torch.Tensor:
-    """Cached device workspace (torch allocations are >= 512-B aligned)."""
-    key = (str(device), tag)
+def workspace(nbytes: int, device, tag: str = "default", stream=None) -> torch.Tensor:
+    """Cached device workspace (torch allocations are >= 512-B aligned), one per (device, tag, stream) and
+    allocated ON the stream the library call runs on: the caching allocator then reuses a replaced (smaller)
+    workspace's memory only in that stream's order, never under a launch still running on it."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (str(device), tag, int(s.cuda_stream))
     w = _WS.get(key)
     if w is None or w.numel() < nbytes:
         _WS.pop(key, None)
-        w = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        with torch.cuda.stream(s):
+            w = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
         _WS[key] = w
     return w
 
@@ -170,7 +174,7 @@ def stats_update(table: TensorTable, plan: Plan, stats: torch.Tensor, decay: flo
     L = _lib.lib()
     nb = plan.n_blocks
     wsb = L.shampoo_stats_workspace_bytes(plan.blocks.ctypes.data, nb, only_owner)
-    ws = workspace(wsb, stats.device, "stats")
+    ws = workspace(wsb, stats.device, "stats", stream)
     check(L.shampoo_stats_update(table.dev.data_ptr(), table.n, plan.device_blocks(stats.device).data_ptr(),
                                  plan.blocks.ctypes.data, nb, only_owner, stats.data_ptr(), float(decay), float(weight),
                                  graft_num.data_ptr() if graft_num is not None else None,
@@ -199,7 +203,7 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
         slices = int(fp64_iters[4:] or 7)
         budget = SLICE_BUDGET if fp64_iters == "auto" else 0.0
         wsb = L.shampoo_root_auto_workspace_bytes(batch, n, p, max_iter)
-        ws = workspace(wsb, device if device is not None else info.device, ws_tag)
+        ws = workspace(wsb, device if device is not None else info.device, ws_tag, stream)
         check(L.shampoo_inverse_pth_root_batched_auto(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
                                                       tol, max_iter, power_iters, slices, budget, info.data_ptr(),
                                                       ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
@@ -212,13 +216,13 @@ def inverse_pth_root_ptr(A_ptr: int, lda: int, stride_a: int, X_ptr: int, ldx: i
         if r != 1:
             raise ValueError("the ozaki root serves r = 1 only")
         wsb = L.shampoo_root_ozaki_workspace_bytes(batch, n, p, max_iter)
-        ws = workspace(wsb, device if device is not None else info.device, ws_tag)
+        ws = workspace(wsb, device if device is not None else info.device, ws_tag, stream)
         check(L.shampoo_inverse_pth_root_batched_ozaki(A_ptr, lda, stride_a, X_ptr, ldx, stride_x, batch, n, p, eps_rel,
                                                        tol, max_iter, power_iters, slices, budget, info.data_ptr(),
                                                        ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
         return
     wsb = L.shampoo_root_workspace_bytes(batch, n, p, max_iter)
-    ws = workspace(wsb, device if device is not None else info.device, ws_tag)
+    ws = workspace(wsb, device if device is not None else info.device, ws_tag, stream)
     if fp64_iters is not None:
         if r != 1:
             raise ValueError("the hybrid root serves r = 1 only")
@@ -278,7 +282,7 @@ def root_residual_batched(A: torch.Tensor, X: torch.Tensor, p: int, info: torch.
     L = _lib.lib()
     out = torch.empty(batch, dtype=torch.float64, device=A3.device)
     wsb = L.shampoo_root_residual_workspace_bytes(batch, n, p)
-    ws = workspace(wsb, A3.device, "residual")
+    ws = workspace(wsb, A3.device, "residual", stream)
     check(L.shampoo_root_residual_batched(A3.data_ptr(), A3.stride(1), A3.stride(0), X3.data_ptr(), X3.stride(1),
                                           X3.stride(0), batch, n, p, eps_rel, info.data_ptr(), out.data_ptr(),
                                           ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
@@ -344,7 +348,7 @@ def precondition(table: TensorTable, plan: Plan, roots: torch.Tensor, graft_num:
     nb = plan.n_blocks
     th, bh = table.host, plan.blocks
     wsb = L.shampoo_precondition_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb)
-    ws = workspace(wsb, roots.device, "precondition")
+    ws = workspace(wsb, roots.device, "precondition", stream)
     check(L.shampoo_precondition_split(th.ctypes.data, table.n, bh.ctypes.data, nb, roots.data_ptr(),
                                  roots_lo.data_ptr() if roots_lo is not None else None,
                                  graft_num.data_ptr() if graft_num is not None else None,
@@ -376,7 +380,7 @@ def momentum_step(table: TensorTable, states: StateTable, plan: Plan, beta1: flo
     size and the parameter update (f2)."""
     L = _lib.lib()
     nb = plan.n_blocks
-    ws = workspace(L.shampoo_momentum_workspace_bytes(nb), table.device, "momentum")
+    ws = workspace(L.shampoo_momentum_workspace_bytes(nb), table.device, "momentum", stream)
     check(L.shampoo_momentum_step(table.dev.data_ptr(), states.dev.data_ptr(), table.n,
                                   plan.device_blocks(table.device).data_ptr(), nb, float(beta1), float(eta0),
                                   1 if shampoo_branch else 0, eta_out.data_ptr() if eta_out is not None else None,
@@ -449,7 +453,7 @@ def tensor_stats_update(table: TTensorTable, plan: Plan, stats: torch.Tensor, de
     nb = plan.n_blocks
     th, bh = table.host, plan.blocks
     wsb = L.shampoo_tensor_stats_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb, only_owner)
-    ws = workspace(wsb, stats.device, "tstats")
+    ws = workspace(wsb, stats.device, "tstats", stream)
     check(L.shampoo_tensor_stats_update(th.ctypes.data, table.n, bh.ctypes.data, nb, only_owner, stats.data_ptr(),
                                         float(decay), float(weight),
                                         graft_num.data_ptr() if graft_num is not None else None,
@@ -464,7 +468,7 @@ def tensor_precondition(table: TTensorTable, plan: Plan, roots: torch.Tensor, gr
     nb = plan.n_blocks
     th, bh = table.host, plan.blocks
     wsb = L.shampoo_tensor_precondition_workspace_bytes(th.ctypes.data, table.n, bh.ctypes.data, nb)
-    ws = workspace(wsb, roots.device, "tprecondition")
+    ws = workspace(wsb, roots.device, "tprecondition", stream)
     check(L.shampoo_tensor_precondition(th.ctypes.data, table.n, bh.ctypes.data, nb, roots.data_ptr(),
                                         graft_num.data_ptr() if graft_num is not None else None,
                                         graft_scale.data_ptr() if graft_scale is not None else None,
