@@ -54,10 +54,13 @@ struct Cfg {
   static constexpr int kStages = (225 * 1024) / kStageBytes;   // as many as fit: 2 / 5 (S = 7), 3 / 6 (S = 6)
 #endif
 };
-constexpr int kThreads = 192;
+// warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer, warps 2.. the epilogue: two warps per TMEM lane
+// quadrant, each draining and storing 32 of the tile's 64 columns (kEpiCols) -- a tile's epilogue then costs half
+// the time per warp, so it keeps pace with the MMAs of the next tile also at S = 5, 6 (round 1: 4 warps x 64 columns)
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 // Bound probes for tools/microbench/ozaki_test.cu only (the library builds with 0):
 // 1 = no MMAs (TMA data movement + barriers + epilogue), 2 = no TMA loads (MMAs on stale tiles),
-// 3 = no accumulator drain (the epilogue releases TMEM at once and stores zeros)
 #ifndef OZ_PROBE
 #define OZ_PROBE 0
 #endif
@@ -501,7 +504,7 @@ __host__ __device__ constexpr int grp_bytes(int g) {
 }
 
 template <int S, int BK>
-__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
+__global__ void __maxnreg__(200) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
   using C = Cfg<S, BK>;
   constexpr int kS = S, kBK = BK, kStages = C::kStages, kStageBytes = C::kStageBytes;
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       tc::mbar_init(empty + s, 1);
     }
     tc::mbar_init(tmem_full, 1);
-    tc::mbar_init(tmem_empty, 128);
+    tc::mbar_init(tmem_empty, 32 * kEpiWarps);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<kTmemCols>(tmem_base_slot);
@@ -627,7 +630,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int quad = warp & 3;
+    const int quad = warp & 3;                  // TMEM lane quadrant of this warp (hardware: warp % 4)
+    constexpr int kEpiCols = kBN / (kEpiWarps / 4);
+    const int cb = ((warp - 2) >> 2) * kEpiCols;  // this warp's first column of the tile
     const int row_in_tile = quad * 32 + lane;
     uint32_t acc_phase = 0;
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -651,18 +656,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // where the tensor pipe is idle (the MMA warp waits for TMEM): measured
       // on B200, fp64 instructions issued while tcgen05 MMAs run stall ~100x
       // ("math pipe throttle"), so phase 2 below uses integer arithmetic only.
-      double v[kBN];
-#if OZ_PROBE == 3
+      double v[kEpiCols];  // columns cb .. cb + kEpiCols - 1 of the tile
 #pragma unroll
-      for (int e = 0; e < kBN; ++e) v[e] = 0.0;
-      if (false)
-#endif
-#pragma unroll
-      for (int c0 = 0; c0 < kBN; c0 += 8) {
+      for (int c0 = 0; c0 < kEpiCols; c0 += 8) {
         uint32_t r[kS][8];
 #pragma unroll
         for (int d = 0; d < kS; ++d)
-          tc::tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(d * kBN + c0), r[d]);
+          tc::tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(d * kBN + cb + c0), r[d]);
         tc::tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // next tile's MMAs, where fp64 instructions crawl
       uint32_t dep = 0u;
 #pragma unroll
-      for (int e = 0; e < kBN; ++e) dep |= (uint32_t)(__double_as_longlong(v[e]) >> 32);
+      for (int e = 0; e < kEpiCols; ++e) dep |= (uint32_t)(__double_as_longlong(v[e]) >> 32);
       tc::tc_fence_before();
       tc::mbar_arrive(tmem_empty + ((dep == 0xFFFFFFFFu && a.n < 0) ? 1 : 0));
       // phase 2: scale by 2^(e_i + f_j - 12 - 7(S-1)) (exponent arithmetic), store
@@ -707,18 +707,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int i0w = ti * kBM + quad * 32;  // this warp's first row
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
         const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
-        if (row_ok && tj == 2 * ti)
+        if (row_ok && tj == 2 * ti && cb == 0)
           J.out_scale[(int64_t)mat * a.np + i] = __longlong_as_double((long long)(J.out_e + 1023) << 52);
-        // two halves of 32 columns (bounds the live registers: 32 W values)
-#pragma unroll
-        for (int h = 0; h < kBN; h += 32) {
+        // this warp's 32 columns
+        static_assert(kEpiCols == 32, "the sliced epilogue's mirror transposes 32-column segments");
+        {
+          const int h = cb;
           unsigned long long w[32];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             if (row_ok) {
               const double2 b2 = *reinterpret_cast<const double2*>(bs + h + e);
-              w[e] = int_w<kS>(scale2(v[h + e], ka + exp2_of(b2.x)), J.out_e, ovf);
-              w[e + 1] = int_w<kS>(scale2(v[h + e + 1], ka + exp2_of(b2.y)), J.out_e, ovf);
+              w[e] = int_w<kS>(scale2(v[e], ka + exp2_of(b2.x)), J.out_e, ovf);
+              w[e + 1] = int_w<kS>(scale2(v[e + 1], ka + exp2_of(b2.y)), J.out_e, ovf);
             } else {
               w[e] = w[e + 1] = 0ull;
             }
@@ -768,15 +769,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
           float* orow = J.outf[mat] + (int64_t)i * J.outf_ld[mat] + j0;
           const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
-          const bool vec = j0 + kBN <= a.n && ((reinterpret_cast<uintptr_t>(orow) & 15) == 0);
+          const bool vec = j0 + cb + kEpiCols <= a.n && ((reinterpret_cast<uintptr_t>(orow) & 15) == 0);
 #pragma unroll
-          for (int e = 0; e < kBN; e += 4) {
+          for (int e = cb; e < cb + kEpiCols; e += 4) {
             const double2 b01 = *reinterpret_cast<const double2*>(bs + e);
             const double2 b23 = *reinterpret_cast<const double2*>(bs + e + 2);
-            const float f0 = f32_of(scale2(v[e], ka + exp2_of(b01.x)));
-            const float f1 = f32_of(scale2(v[e + 1], ka + exp2_of(b01.y)));
-            const float f2 = f32_of(scale2(v[e + 2], ka + exp2_of(b23.x)));
-            const float f3 = f32_of(scale2(v[e + 3], ka + exp2_of(b23.y)));
+            const float f0 = f32_of(scale2(v[e - cb], ka + exp2_of(b01.x)));
+            const float f1 = f32_of(scale2(v[e - cb + 1], ka + exp2_of(b01.y)));
+            const float f2 = f32_of(scale2(v[e - cb + 2], ka + exp2_of(b23.x)));
+            const float f3 = f32_of(scale2(v[e - cb + 3], ka + exp2_of(b23.y)));
             if (vec) {
               __stcs(reinterpret_cast<float4*>(orow + e), make_float4(f0, f1, f2, f3));
             } else {
@@ -791,14 +792,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int j0 = tj * kBN;
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
         double* orow = out + (int64_t)i * a.np + j0;
-        const bool full_row = j0 + kBN <= a.n && (!a.sym || j0 >= i);
+        const bool full_row = j0 + cb + kEpiCols <= a.n && (!a.sym || j0 + cb >= i);
         const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
 #pragma unroll
-        for (int e = 0; e < kBN; e += 2) {
+        for (int e = cb; e < cb + kEpiCols; e += 2) {
           const double2 b2 = *reinterpret_cast<const double2*>(bs + e);
-          const double c0 = scale2(v[e], ka + exp2_of(b2.x)), c1 = scale2(v[e + 1], ka + exp2_of(b2.y));
-          v[e] = c0;
-          v[e + 1] = c1;
+          const double c0 = scale2(v[e - cb], ka + exp2_of(b2.x)), c1 = scale2(v[e - cb + 1], ka + exp2_of(b2.y));
+          v[e - cb] = c0;
+          v[e - cb + 1] = c1;
           if (full_row) {
             __stcs(reinterpret_cast<double2*>(orow + e), make_double2(c0, c1));
           } else {
@@ -821,13 +822,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
         // the one fp64 subtraction of the M-update, once per row of a diagonal tile
-        if (mup && i >= j0 && i < j0 + kBN) emax_bits = umax64(emax_bits, abs_bits(__longlong_as_double((long long)diag_bits) - 1.0));
+        if (mup && i >= j0 + cb && i < j0 + cb + kEpiCols)
+          emax_bits = umax64(emax_bits, abs_bits(__longlong_as_double((long long)diag_bits) - 1.0));
         if (a.sym) {  // mirror: lanes are consecutive rows -> coalesced
 #pragma unroll
-          for (int e = 0; e < kBN; ++e) {
+          for (int e = cb; e < cb + kEpiCols; ++e) {
             const int j = j0 + e;
             if (j >= a.n || j <= i) continue;
-            __stcs(out + (int64_t)j * a.np + i, v[e]);
+            __stcs(out + (int64_t)j * a.np + i, v[e - cb]);
           }
         }
       }
