@@ -227,3 +227,23 @@ def test_tensor_entry_points_validate_host_tables(shp):
     assert b"null G or P" in L.shampoo_last_error()
     with pytest.raises(ShampooError):
         shp.make_tensor_plan([(0, 3)])
+
+
+def test_ozaki_slice_schedule_worked_values(shp):
+    """Reading #29's schedule (host function of the library), worked by hand: S_k = the fewest slices in [5, s_max]
+    with 2^-(7S-1) sqrt(n/1024) / (p m_k) <= budget, m_k = min(1, eps g^k), g = ((p+1)/p)^p.
+    n = 1024, p = 4 (g = 2.4414): S = 6 needs m >= 2^-41 / 4e-9 = 1.14e-4 -> g^k >= 113.7 -> k >= 5.30; S = 5 needs
+    m >= 2^-34 / 4e-9 = 0.01455 -> g^k >= 14552 -> k >= 10.74.  p = 2 (g = 2.25, amplification 1/(2m)): k >= 6.69
+    and 12.67.  n = 2048 (x sqrt 2): k >= 5.69 and 11.13.  eps = 0 or budget = 0: s_max throughout."""
+    from paper_2002_09018_b200 import _lib
+    L = _lib.lib()
+
+    def sched(p, n, eps=1e-6, budget=1e-9, smax=7, ks=range(16)):
+        return [L.shampoo_ozaki_iteration_slices(k, p, n, eps, budget, smax) for k in ks]
+
+    assert sched(4, 1024) == [7] * 6 + [6] * 5 + [5] * 5
+    assert sched(2, 1024) == [7] * 7 + [6] * 6 + [5] * 3
+    assert sched(4, 2048) == [7] * 6 + [6] * 6 + [5] * 4
+    assert sched(4, 1024, eps=0.0) == [7] * 16
+    assert sched(4, 1024, budget=0.0) == [7] * 16
+    assert sched(4, 1024, smax=6) == [6] * 11 + [5] * 5
