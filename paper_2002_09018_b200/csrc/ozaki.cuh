@@ -504,7 +504,7 @@ __host__ __device__ constexpr int grp_bytes(int g) {
 }
 
 template <int S, int BK>
-__global__ void __maxnreg__(200) gemm_kernel(const __grid_constant__ OzArgs a,
+__global__ void __maxnreg__(192) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
   using C = Cfg<S, BK>;
   constexpr int kS = S, kBK = BK, kStages = C::kStages, kStageBytes = C::kStageBytes;
