@@ -56,7 +56,8 @@ struct Cfg {
 };
 // warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer, warps 2.. the epilogue: two warps per TMEM lane
 // quadrant, each draining and storing 32 of the tile's 64 columns (kEpiCols) -- a tile's epilogue then costs half
-// the time per warp, so it keeps pace with the MMAs of the next tile also at S = 5, 6 (round 1: 4 warps x 64 columns)
+// the time per warp, so it keeps pace with the MMAs of the next tile also at S = 5, 6 (round 1: 4 warps x 64
+// columns).  10 warps put 3 on two of the SM's four 16K-register partitions: <= 168 registers per thread.
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 // Bound probes for tools/microbench/ozaki_test.cu only (the library builds with 0):
@@ -504,7 +505,7 @@ __host__ __device__ constexpr int grp_bytes(int g) {
 }
 
 template <int S, int BK>
-__global__ void __maxnreg__(192) gemm_kernel(const __grid_constant__ OzArgs a,
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
   using C = Cfg<S, BK>;
   constexpr int kS = S, kBK = BK, kStages = C::kStages, kStageBytes = C::kStageBytes;
