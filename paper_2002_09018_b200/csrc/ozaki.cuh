@@ -58,7 +58,11 @@ struct Cfg {
 // quadrant, each draining and storing 32 of the tile's 64 columns (kEpiCols) -- a tile's epilogue then costs half
 // the time per warp, so it keeps pace with the MMAs of the next tile also at S = 5, 6 (round 1: 4 warps x 64
 // columns).  10 warps put 3 on two of the SM's four 16K-register partitions: <= 168 registers per thread.
-constexpr int kEpiWarps = 8;
+#ifndef OZ_EPI_WARPS
+#define OZ_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = OZ_EPI_WARPS;  // 8 (library) or 16 (microbenchmark variant: 16 columns per warp)
+static_assert(kEpiWarps == 8 || kEpiWarps == 16, "two or four epilogue warps per TMEM lane quadrant");
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 // Bound probes for tools/microbench/ozaki_test.cu only (the library builds with 0):
 // 1 = no MMAs (TMA data movement + barriers + epilogue), 2 = no TMA loads (MMAs on stale tiles),
@@ -710,13 +714,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
         if (row_ok && tj == 2 * ti && cb == 0)
           J.out_scale[(int64_t)mat * a.np + i] = __longlong_as_double((long long)(J.out_e + 1023) << 52);
-        // this warp's 32 columns
-        static_assert(kEpiCols == 32, "the sliced epilogue's mirror transposes 32-column segments");
+        // this warp's kEpiCols columns
         {
           const int h = cb;
-          unsigned long long w[32];
+          unsigned long long w[kEpiCols];
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
+          for (int e = 0; e < kEpiCols; e += 2) {
             if (row_ok) {
               const double2 b2 = *reinterpret_cast<const double2*>(bs + h + e);
               w[e] = int_w<kS>(scale2(v[e], ka + exp2_of(b2.x)), J.out_e, ovf);
@@ -728,19 +731,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll 1
           for (int s2 = 0; s2 < kS; ++s2) {
             int8_t* ps = pl + s2 * pitch;
-            uint32_t wd[8];
+            constexpr int kW = kEpiCols / 4;  // 4-byte words per row segment
+            uint32_t wd[kW];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < kW; ++k)
               wd[k] = w_byte<kS>(w[4 * k], s2) | (w_byte<kS>(w[4 * k + 1], s2) << 8) |
                       (w_byte<kS>(w[4 * k + 2], s2) << 16) | (w_byte<kS>(w[4 * k + 3], s2) << 24);
             if (interior) {
               uint4* dst = reinterpret_cast<uint4*>(ps + (int64_t)i * a.np + j0 + h);
-              dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-              dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+#pragma unroll
+              for (int q = 0; q < kW / 4; ++q) dst[q] = make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
               // mirror rows j0 + h + 4k + (lane >> 3), columns i0w + 4 (lane & 7) .. + 3
               const int src = 4 * (lane & 7), sel = 8 * (lane >> 3);
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
+              for (int k = 0; k < kW; ++k) {
                 const uint32_t x0 = __shfl_sync(0xffffffffu, wd[k], src);
                 const uint32_t x1 = __shfl_sync(0xffffffffu, wd[k], src + 1);
                 const uint32_t x2 = __shfl_sync(0xffffffffu, wd[k], src + 2);
@@ -751,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               }
             } else if (row_ok) {
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
+              for (int e = 0; e < kEpiCols; ++e) {
                 const int j = j0 + h + e;
                 const int8_t byte = (int8_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
                 if (j < a.n && j >= i) ps[(int64_t)i * a.np + j] = byte;
