@@ -642,14 +642,13 @@ static void oz_slice_mt(int S, const double* src, int64_t mstride, int n, int np
   }
 }
 
-// A non-blocking stream per device to capture the tail graph's body into (never destroyed).
+// A non-blocking stream per (host thread, device) to capture the tail graph's body into (never destroyed): root
+// calls from different host threads capture independently.
 static cudaStream_t capture_stream() {
-  static std::mutex mu;
-  static cudaStream_t streams[64] = {};
+  thread_local cudaStream_t streams[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  std::lock_guard<std::mutex> lock(mu);
   if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
   return streams[dev];
 }
