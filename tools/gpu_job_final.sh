@@ -19,6 +19,6 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref
 timeout 900 python tools/bench_delayed.py --chunks 32,16 > $O/delayed.json 2> $O/delayed.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_root528.csv \
   python tools/profile_root.py --batch 528 --hybrid -9 --reps 1 > $O/launches_root528.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 80 -c 4 -f -o $O/gemm148 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 48 -c 4 -f -o $O/gemm148 \
   python tools/profile_root.py --batch 148 --hybrid -9 --reps 1 > $O/ncu_gemm148.log 2>&1
 echo done > $O/DONE
