@@ -85,15 +85,18 @@ class DelayedRefresh:
     def __init__(self, plan: Plan, stats: torch.Tensor, roots: torch.Tensor, rank: int = 0, world_size: int = 1,
                  kappa: int = 500, spread: int | None = None, eps_rel: float = 1e-6, tol: float = 1e-7,
                  max_iter: int = 100, power_iters: int = 100, group=None, fp64_iters="auto",
-                 chunk: int | None = None, stream: torch.cuda.Stream | None = None):
+                 chunk: int | None = None, stream: torch.cuda.Stream | None = None, gather_roots: bool = True):
         """spread: the number of steps a refresh is spread over (<= kappa; default: as many as the chunk size
         needs, at most kappa).  chunk: roots per step on the busiest rank (default: ceil(max owned / spread)).
-        stream: the refresh stream (default: a new lowest-priority stream on the statistics' device)."""
+        stream: the refresh stream (default: a new lowest-priority stream on the statistics' device).
+        gather_roots: all-gather the new roots at the end of the window (root shards); False for layer shards
+        (``make_plan(..., owners="tensor")``), whose roots stay with their owner -- the step then exchanges P."""
         self.plan, self.stats, self.rank, self.world = plan, stats, rank, world_size
         self.kappa = int(kappa)
         self.kw = dict(eps_rel=eps_rel, tol=tol, max_iter=max_iter, power_iters=power_iters)
         self.fp64_iters = fp64_iters  # root precision: "auto" (Ozaki for n >= 512), None (FP64 DMMA), "ozaki"...
         self.group = group
+        self.gather_roots = gather_roots
         self.current = roots                       # roots the step uses (stale by <= 2 kappa)
         self.next = torch.zeros_like(roots)        # roots being built from the last snapshot
         # TF32 remainder of the current roots for shampoo_precondition_split,
@@ -157,7 +160,8 @@ class DelayedRefresh:
             if not self.pending:
                 self.ev_done.record(self.stream)
                 cur.wait_event(self.ev_done)  # the gather (on the training stream / NCCL's) sees finished roots
-                all_gather_roots(self.plan, self.next, self.rank, self.world, self.group)
+                if self.gather_roots:
+                    all_gather_roots(self.plan, self.next, self.rank, self.world, self.group)
                 self.ready = True
                 self.refreshes += 1
         return adopted
