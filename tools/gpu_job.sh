@@ -3,8 +3,6 @@
 T=${1:-r02x}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 300 tools/microbench/bin/ozaki_test_epi16 > $O/ozaki_test_epi16.log 2>&1; echo "exit $?" >> $O/ozaki_test_epi16.log
-timeout 300 tools/microbench/bin/oz_probe0 > $O/oz_epi8.log 2>&1
-timeout 300 tools/microbench/bin/oz_epi16 > $O/oz_epi16.log 2>&1
-timeout 300 tools/microbench/bin/oz_probe0 > $O/oz_epi8b.log 2>&1
+timeout 900 python tools/profile_layer_ranks.py --world 1 2 4 8 --owners tensor root > $O/layer_ranks.jsonl 2> $O/layer_ranks.err
+for w in config2 config4 resnet50; do timeout 900 python tools/bench_workloads.py --workload $w > $O/workload_$w.json 2> $O/workload_$w.err; done
 echo done > $O/DONE
