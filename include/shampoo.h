@@ -133,7 +133,7 @@ int shampoo_plan(const int64_t* shapes, int32_t n_tensors, int32_t block_size, i
  * computed for every layer of the network, we distribute the computation across
  * all the CPUs"): every root of tensor t is owned by tensor_owner[t], the tensors
  * assigned LPT -- sorted by (cost desc, index), cost = sum over the tensor's roots
- * of n^3 x (products per iteration + 4) + m*n, each to the least-loaded rank
+ * of n^3 x (products per iteration + 12) + m*n, each to the least-loaded rank
  * (lowest on ties).  Packing as shampoo_plan.  An owner then holds whole tensors:
  * their statistics, roots and preconditioned gradient, so the multi-GPU step
  * exchanges P (one all-gather) instead of the roots.

@@ -24,10 +24,10 @@ Rule (DESIGN.md §3 readings #5, #12, #13, #17):
   owners="tensor" (reading #30, "As preconditioners need to be computed for
   every layer of the network, we distribute the computation"):
   tensors sorted by (-cost_t, t) with cost_t = sum over the tensor's roots of
-  n^3 (products_per_iteration(p) + 4) + m*n (the +4: per-iteration work that
-  does not scale with the products, fitted to measured per-root times), each
-  assigned to the least-loaded rank (lowest on ties); every root of tensor t is
-  owned by t's owner.
+  n^3 (products_per_iteration(p) + 12) + m*n (the +12: a root's time on the
+  Ozaki path hardly depends on p -- measured), each assigned to the
+  least-loaded rank (lowest on ties); every root of tensor t is owned by t's
+  owner.
 * Packing: one fp32 buffer holds all statistics (and, at the same offsets,
   all roots).  Rank r's segment holds the roots it owns, grouped by (n desc,
   p desc, r desc), each matrix ``n x ld`` with ``ld = roundup(n, 4)`` and a group
@@ -145,7 +145,7 @@ def plan(shapes, block_size: int, max_precond_dim: int, world_size: int, split=(
         for _cost, t, bidx, side in roots:
             b = out.blocks[bidx]
             nn, pp = (b.rows, b.p_left) if side == 0 else (b.cols, b.p_right)
-            tcost[t] += nn ** 3 * (products_per_iteration(pp) + 4)
+            tcost[t] += nn ** 3 * (products_per_iteration(pp) + 12)
         tload = [0] * world_size
         tensor_owner = [0] * len(shapes)
         for t in sorted(range(len(shapes)), key=lambda t: (-tcost[t], t)):

@@ -114,15 +114,15 @@ static int64_t assign_and_pack(std::vector<RootRef>& roots, int world_size, std:
 }
 
 // Layer-granular owners (reading #30): tensors sorted by (cost desc, index) with cost = sum over their roots of
-// n^3 (products per iteration + 4) -- the +4 product-equivalents per iteration stand for the work that does not
-// scale with the product count (the X / M / T slicing passes and the decision), fitted to the measured per-root
-// times of the Ozaki path (a p = 2 root takes 0.93 of a p = 4 one; products alone say 0.75) -- plus m*n (so
+// n^3 (products per iteration + 12) -- on the Ozaki path a root's time hardly depends on p (measured per 1024^2
+// root: p = 4 0.96-1.04 ms, p = 2 1.03-1.10 ms, more iterations and small-batch costs; products alone would say
+// 0.75), so a large p-independent term; K >= 12 all give the same order for Transformer-Big -- plus m*n (so
 // tensors without a preconditioned side still spread), each assigned to the least-loaded rank (lowest on ties).
 static std::vector<int> tensor_owners(const std::vector<RootRef>& roots, const int64_t* shapes, int32_t n_tensors,
                                       int world_size) {
   std::vector<int64_t> cost(n_tensors, 0);
   for (int32_t t = 0; t < n_tensors; ++t) cost[t] = shapes[2 * t] * shapes[2 * t + 1];
-  for (const RootRef& r : roots) cost[r.tensor] += (int64_t)r.n * r.n * r.n * (products_per_iteration(r.p) + 4);
+  for (const RootRef& r : roots) cost[r.tensor] += (int64_t)r.n * r.n * r.n * (products_per_iteration(r.p) + 12);
   std::vector<int32_t> order(n_tensors);
   for (int32_t t = 0; t < n_tensors; ++t) order[t] = t;
   std::stable_sort(order.begin(), order.end(),

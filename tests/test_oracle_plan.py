@@ -121,13 +121,13 @@ def test_plan_is_deterministic():
 
 
 def test_layer_owners_hand_worked():
-    """owners="tensor" (reading #30), worked by hand: costs are sum(n^3 x (products + 4)) + m*n per tensor.
+    """owners="tensor" (reading #30), worked by hand: costs are sum(n^3 x (products + 12)) + m*n per tensor.
     4 equal 1024^2 tensors at W=4 -> one tensor per rank (LPT deals them 0, 1, 2, 3); at W=3 the fourth goes
     back to rank 0 (all loads equal, lowest rank).  Sizes 256, 512, 512, 1024 (two-sided, 4 products each:
-    costs 2*(4+4)*n^3 + n^2) at W=2: the 1024 tensor alone on rank 0, the rest on rank 1 (1024-cost 1.72e10 >
-    2 x 2.15e9 + 2.7e8).  The +4 decides the order of a one-sided and a two-sided tensor: (24576, 1024)
-    has 24 p=2 roots (24 x 7 = 168 units of 1024^3; products alone: 72), (2048, 5120) 20 p=4 roots (160; 80):
-    the vocabulary-like tensor goes first (rank 0), then the two-sided one and the small (1024, 1024) (16) to
+    costs 2*(4+12)*n^3 + n^2) at W=2: the 1024 tensor alone on rank 0, the rest on rank 1 (1024-cost 3.44e10 >
+    2 x 4.3e9 + 5.4e8).  The +12 decides the order of a one-sided and a two-sided tensor: (24576, 1024)
+    has 24 p=2 roots (24 x 15 = 360 units of 1024^3; products alone: 72), (2048, 5120) 20 p=4 roots (320; 80):
+    the vocabulary-like tensor goes first (rank 0), then the two-sided one and the small (1024, 1024) (32) to
     rank 1 -- with products alone the order, and the owners, would flip."""
     pl = oplan.plan([(1024, 1024)] * 4, 1024, 8192, 4, owners="tensor")
     assert pl.tensor_owner == [0, 1, 2, 3]
