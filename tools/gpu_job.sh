@@ -3,6 +3,10 @@
 T=${1:-r02x}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 900 python tools/profile_layer_ranks.py --world 1 2 4 8 --owners tensor root > $O/layer_ranks.jsonl 2> $O/layer_ranks.err
-for w in config2 config4 resnet50; do timeout 900 python tools/bench_workloads.py --workload $w > $O/workload_$w.json 2> $O/workload_$w.err; done
+timeout 240 tools/microbench/bin/ozaki_test > $O/ozaki_test.log 2>&1; echo "exit $?" >> $O/ozaki_test.log
+if grep -q "^PASS" $O/ozaki_test.log; then
+  timeout 900 python -m pytest tests/test_gpu_ozaki.py tests/test_gpu_bench_path.py -q -rA -s -x > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_n1_pair.json 2> $O/bench_n1_pair.err
+  SHAMPOO_OZAKI_PAIR=0 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_n1_single.json 2> $O/bench_n1_single.err
+fi
 echo done > $O/DONE
