@@ -490,6 +490,25 @@ TC_DEV void oz_decode(const OzArgs& a, int per_mat, int64_t tile, int& mat, int&
   mat = a.act ? a.act[pos] : pos;
 }
 
+// Debug watchdog for the microbenchmark (OZ_WATCHDOG builds only): a bounded barrier wait that records which wait
+// timed out in g_oz_watchdog (bit `code`) and gives up instead of hanging.
+#ifdef OZ_WATCHDOG
+__device__ unsigned long long g_oz_watchdog;
+TC_DEV void oz_wait(uint64_t* bar, uint32_t phase, int code) {
+  const uint32_t addr = tc::smem_u32(bar);
+  for (long it = 0; it < (1L << 24); ++it) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P1;\n\t}\n" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+    if (ok) return;
+  }
+  atomicOr(&g_oz_watchdog, 1ull << code);
+}
+#define OZ_WAIT(bar, phase, code) oz_wait(bar, phase, code)
+#else
+#define OZ_WAIT(bar, phase, code) tc::mbar_wait(bar, phase)
+#endif
+
 // CTA pairs (kPair): the two CTAs of a cluster compute the tiles (ti, tj) and (ti, tj + 1) of one row block, so
 // they share the A planes: each CTA loads half of them and multicasts them into both (one L2 read of A per pair,
 // round 2).  A pair item = (matrix, job, ti, first tj); with an odd tile count in a row the second CTA's tile is a
@@ -606,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const CUtensorMap* am = maps + a.job[job].a_map;
         const CUtensorMap* bm = maps + a.job[job].b_map;
         for (int kc = 0; kc < k_chunks; ++kc) {
-          tc::mbar_wait(empty + stage, phase ^ 1);
+          OZ_WAIT(empty + stage, phase ^ 1, 0);
           uint8_t* st = smem + stage * kStageBytes;
 #pragma unroll
           for (int g = 0; g < kGroups; ++g) {
@@ -641,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     uint32_t phase = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = item0; tile < total; tile += istep) {
-      tc::mbar_wait(tmem_empty, acc_phase ^ 1);
+      OZ_WAIT(tmem_empty, acc_phase ^ 1, 1);
       tc::tc_fence_after();
       for (int kc = 0; kc < k_chunks; ++kc) {
         const uint32_t s0 = tc::smem_u32(smem + stage * kStageBytes);
@@ -663,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               const int need = grp_a(sa) > grp_b(tb) ? grp_a(sa) : grp_b(tb);
               while (ready < need) {
                 ++ready;
-                tc::mbar_wait(full + stage * kGroups + ready, phase);
+                OZ_WAIT(full + stage * kGroups + ready, phase, 2 + ready);
                 tc::tc_fence_after();
               }
               const int cnt = (kS - sa - tb) < 4 ? (kS - sa - tb) : 4;
@@ -703,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       int mat, job, ti, tj;
       bool dummy;
       decode(tile, mat, job, ti, tj, dummy);
-      tc::mbar_wait(tmem_full, acc_phase);
+      OZ_WAIT(tmem_full, acc_phase, 6);
       tc::tc_fence_after();
       const int i = ti * kBM + row_in_tile;
       const bool row_ok = i < a.n && !dummy;

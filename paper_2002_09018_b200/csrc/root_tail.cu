@@ -591,12 +591,12 @@ int ozaki_iteration_slices(int k, int p, int n, double eps_rel, double budget, i
   return s_max;
 }
 
-// CTA pairs sharing the A planes through TMA multicast (ozaki.cuh kPair); SHAMPOO_OZAKI_PAIR=0 selects the
-// single-CTA kernel (A/B measurements).  The grid is as many 2-CTA clusters as can be resident at once.
+// CTA pairs sharing the A planes through TMA multicast (ozaki.cuh kPair): opt-in with SHAMPOO_OZAKI_PAIR=1 while
+// being validated; the default is the single-CTA kernel.  The grid is as many 2-CTA clusters as fit at once.
 static bool oz_pair_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("SHAMPOO_OZAKI_PAIR");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }

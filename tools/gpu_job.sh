@@ -3,10 +3,5 @@
 T=${1:-r02x}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 240 tools/microbench/bin/ozaki_test > $O/ozaki_test.log 2>&1; echo "exit $?" >> $O/ozaki_test.log
-if grep -q "^PASS" $O/ozaki_test.log; then
-  timeout 900 python -m pytest tests/test_gpu_ozaki.py tests/test_gpu_bench_path.py -q -rA -s -x > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
-  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_n1_pair.json 2> $O/bench_n1_pair.err
-  SHAMPOO_OZAKI_PAIR=0 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_n1_single.json 2> $O/bench_n1_single.err
-fi
+timeout 600 tools/microbench/bin/ozaki_test_wd > $O/ozaki_test_wd.log 2>&1; echo "exit $?" >> $O/ozaki_test_wd.log
 echo done > $O/DONE

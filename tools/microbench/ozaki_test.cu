@@ -131,6 +131,16 @@ static int run(int n, int batch, bool sym, int reps) {
     CK(cudaGetLastError());
     cudaEventElapsedTime(&ms, e0, e1);
   }
+#ifdef OZ_WATCHDOG
+  {
+    unsigned long long wd = 0;
+    CK(cudaMemcpyFromSymbol(&wd, oz::g_oz_watchdog, sizeof wd));
+    if (wd) printf("    WATCHDOG: barrier waits timed out, bits 0x%llx (0 producer-empty, 1 mma-tmem_empty, "
+                   "2..5 mma-full group, 6 epilogue-tmem_full)\n", wd);
+    wd = 0;
+    CK(cudaMemcpyToSymbol(oz::g_oz_watchdog, &wd, sizeof wd));
+  }
+#endif
   std::vector<double> hC(batch * mat), hsA(batch * np), hsB(batch * np);
   std::vector<int8_t> hpA(batch * mat * oz::kSMax), hpB(batch * mat * oz::kSMax);
   CK(cudaMemcpy(hC.data(), dC, batch * mat * 8, cudaMemcpyDeviceToHost));
@@ -202,6 +212,7 @@ static int run(int n, int batch, bool sym, int reps) {
 }
 
 int main() {
+  setvbuf(stdout, nullptr, _IOLBF, 0);  // line-buffered: a killed run still shows how far it got
   int bad = 0;
 #if OZ_PROBE == 9
   // stage-count / k-chunk probes (OZ_STAGES): correct results, timing of S = 5..7 at n = 1024, 148 matrices
