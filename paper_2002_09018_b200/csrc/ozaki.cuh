@@ -505,8 +505,10 @@ TC_DEV void oz_wait(uint64_t* bar, uint32_t phase, int code) {
   atomicOr(&g_oz_watchdog, 1ull << code);
 }
 #define OZ_WAIT(bar, phase, code) oz_wait(bar, phase, code)
+#define OZ_WAIT_REMOTE(bar, phase, code) oz_wait(bar, phase, code)
 #else
 #define OZ_WAIT(bar, phase, code) tc::mbar_wait(bar, phase)
+#define OZ_WAIT_REMOTE(bar, phase, code) tc::mbar_wait_remote(bar, phase)
 #endif
 
 // CTA pairs (kPair): the two CTAs of a cluster compute the tiles (ti, tj) and (ti, tj + 1) of one row block, so
@@ -625,7 +627,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const CUtensorMap* am = maps + a.job[job].a_map;
         const CUtensorMap* bm = maps + a.job[job].b_map;
         for (int kc = 0; kc < k_chunks; ++kc) {
-          OZ_WAIT(empty + stage, phase ^ 1, 0);
+          if (kPair)
+            OZ_WAIT_REMOTE(empty + stage, phase ^ 1, 0);
+          else
+            OZ_WAIT(empty + stage, phase ^ 1, 0);
           uint8_t* st = smem + stage * kStageBytes;
 #pragma unroll
           for (int g = 0; g < kGroups; ++g) {
@@ -682,7 +687,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               const int need = grp_a(sa) > grp_b(tb) ? grp_a(sa) : grp_b(tb);
               while (ready < need) {
                 ++ready;
-                OZ_WAIT(full + stage * kGroups + ready, phase, 2 + ready);
+                if (kPair)
+                  OZ_WAIT_REMOTE(full + stage * kGroups + ready, phase, 2 + ready);
+                else
+                  OZ_WAIT(full + stage * kGroups + ready, phase, 2 + ready);
                 tc::tc_fence_after();
               }
               const int cnt = (kS - sa - tb) < 4 ? (kS - sa - tb) : 4;

@@ -46,6 +46,21 @@ TC_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// For barriers completed by ANOTHER CTA of the cluster (multicast TMA bytes, multicast commits): try_wait without
+// the suspend-time hint.  Measured on B200: with the hint a thread waiting on remote arrivals was not woken before
+// the hint ran out (the CTA-pair GEMM crawled for minutes); without it the pair matches the spin-wait watchdog build.
+TC_DEV void mbar_wait_remote(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // ----------------------------------------------------------------------- TMA
 TC_DEV void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
