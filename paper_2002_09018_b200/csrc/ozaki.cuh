@@ -490,62 +490,6 @@ TC_DEV void oz_decode(const OzArgs& a, int per_mat, int64_t tile, int& mat, int&
   mat = a.act ? a.act[pos] : pos;
 }
 
-// Debug watchdog for the microbenchmark (OZ_WATCHDOG builds only): a bounded barrier wait that records which wait
-// timed out in g_oz_watchdog (bit `code`) and gives up instead of hanging.
-#ifdef OZ_WATCHDOG
-__device__ unsigned long long g_oz_watchdog;
-TC_DEV void oz_wait(uint64_t* bar, uint32_t phase, int code) {
-  const uint32_t addr = tc::smem_u32(bar);
-  for (long it = 0; it < (1L << 24); ++it) {
-    uint32_t ok;
-    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-                 "selp.b32 %0, 1, 0, P1;\n\t}\n" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
-    if (ok) return;
-  }
-  atomicOr(&g_oz_watchdog, 1ull << code);
-}
-#define OZ_WAIT(bar, phase, code) oz_wait(bar, phase, code)
-#define OZ_WAIT_REMOTE(bar, phase, code) oz_wait(bar, phase, code)
-#else
-#define OZ_WAIT(bar, phase, code) tc::mbar_wait(bar, phase)
-#define OZ_WAIT_REMOTE(bar, phase, code) tc::mbar_wait_remote(bar, phase)
-#endif
-
-// CTA pairs (kPair): the two CTAs of a cluster compute the tiles (ti, tj) and (ti, tj + 1) of one row block, so
-// they share the A planes: each CTA loads half of them and multicasts them into both (one L2 read of A per pair,
-// round 2).  A pair item = (matrix, job, ti, first tj); with an odd tile count in a row the second CTA's tile is a
-// dummy (tj >= tiles_n: zero-filled B, computed, not stored).
-TC_DEV int oz_pairs_per_mat(const OzArgs& a) {
-  if (!a.sym) return a.tiles_m * ((a.tiles_n + 1) / 2);
-  int t = 0;
-  for (int ti = 0; ti < a.tiles_m; ++ti) t += (max(0, a.tiles_n - 2 * ti) + 1) / 2;
-  return t;
-}
-
-TC_DEV void oz_decode_pair(const OzArgs& a, int per_mat, int64_t item, int rank, int& mat, int& job, int& ti,
-                           int& tj, bool& dummy) {
-  const int64_t per = (int64_t)per_mat * a.jobs;
-  const int pos = (int)(item / per);
-  int rem = (int)(item - (int64_t)pos * per);
-  job = rem % a.jobs;
-  int t = rem / a.jobs;
-  if (a.sym) {
-    int i = 0;
-    while (t >= (a.tiles_n - 2 * i + 1) / 2) {
-      t -= (a.tiles_n - 2 * i + 1) / 2;
-      ++i;
-    }
-    ti = i;
-    tj = 2 * i + 2 * t + rank;
-  } else {
-    const int pr = (a.tiles_n + 1) / 2;
-    ti = t / pr;
-    tj = 2 * (t - ti * pr) + rank;
-  }
-  dummy = tj >= a.tiles_n;
-  mat = a.act ? a.act[pos] : pos;
-}
-
 // Each stage's planes arrive in 4 groups with their own full barriers, in the
 // order the MMAs consume them, so the first MMAs of a stage start while the
 // rest of its 84 KB is in flight: A plane sa in group gA(sa), B planes 0-3 in
@@ -564,7 +508,7 @@ __host__ __device__ constexpr int grp_bytes(int g) {
   return b;
 }
 
-template <int S, int BK, bool kPair = false>
+template <int S, int BK>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
                                                           const CUtensorMap* __restrict__ maps) {
   using C = Cfg<S, BK>;
@@ -575,20 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int na = a.act ? *a.nact : a.batch;
   if (na == 0) return;
   const int kcheck = a.kdev ? *a.kdev + 1 : a.kcheck;
-  const int per_mat = kPair ? oz_pairs_per_mat(a) : oz_tiles_per_mat(a);
-  const int64_t total = (int64_t)na * per_mat * a.jobs;  // items: tiles, or tile pairs (kPair)
-  const int rank = kPair ? (int)tc::cluster_ctarank() : 0;
-  const int64_t item0 = kPair ? (int64_t)tc::cluster_id_x() : (int64_t)blockIdx.x;
-  const int64_t istep = kPair ? (int64_t)tc::nclusters_x() : (int64_t)gridDim.x;
-  // the tile of `item` for this CTA (dummy: the second tile of an odd row, computed but not stored)
-  auto decode = [&](int64_t item, int& mat, int& job, int& ti, int& tj, bool& dummy) {
-    if (kPair) {
-      oz_decode_pair(a, per_mat, item, rank, mat, job, ti, tj, dummy);
-    } else {
-      oz_decode(a, per_mat, item, mat, job, ti, tj);
-      dummy = false;
-    }
-  };
+  const int per_mat = oz_tiles_per_mat(a);
+  const int64_t total = (int64_t)na * per_mat * a.jobs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);  // [stage][group]
@@ -600,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       for (int g = 0; g < kGroups; ++g) tc::mbar_init(full + s * kGroups + g, 1);
-      tc::mbar_init(empty + s, kPair ? 2 : 1);  // kPair: both CTAs' MMAs must have read the stage
+      tc::mbar_init(empty + s, 1);
     }
     tc::mbar_init(tmem_full, 1);
     tc::mbar_init(tmem_empty, 32 * kEpiWarps);
@@ -609,7 +541,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 1) tc::tmem_alloc<kTmemCols>(tmem_base_slot);
   tc::tc_fence_before();
   __syncthreads();
-  if (kPair) tc::cluster_sync();  // the peer's barriers exist before any multicast or commit reaches them
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   const int k_chunks = (a.n + kBK - 1) / kBK;
@@ -620,17 +551,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int q = 0; q < 2 * a.jobs; ++q) tc::tma_acquire(maps + (q & 1 ? a.job[q >> 1].b_map : a.job[q >> 1].a_map));
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = item0; tile < total; tile += istep) {
+      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
         int mat, job, ti, tj;
-        bool dummy;
-        decode(tile, mat, job, ti, tj, dummy);
+        oz_decode(a, per_mat, tile, mat, job, ti, tj);
         const CUtensorMap* am = maps + a.job[job].a_map;
         const CUtensorMap* bm = maps + a.job[job].b_map;
         for (int kc = 0; kc < k_chunks; ++kc) {
-          if (kPair)
-            OZ_WAIT_REMOTE(empty + stage, phase ^ 1, 0);
-          else
-            OZ_WAIT(empty + stage, phase ^ 1, 0);
+          tc::mbar_wait(empty + stage, phase ^ 1);
           uint8_t* st = smem + stage * kStageBytes;
 #pragma unroll
           for (int g = 0; g < kGroups; ++g) {
@@ -642,12 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             tc::mbar_arrive_expect_tx(fb, grp_bytes<S, BK>(g));
 #pragma unroll
             for (int s = 0; s < kS; ++s) {
-              if (grp_a(s) == g) {
-                if (!kPair)
-                  tc::tma_load_3d(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kSMax + s);
-                else if ((s & 1) == rank)  // this CTA's half of the shared A planes, into both CTAs
-                  tc::tma_load_3d_mc(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kSMax + s, (uint16_t)3);
-              }
+              if (grp_a(s) == g) tc::tma_load_3d(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kSMax + s);
               if (grp_b(s) == g)
                 tc::tma_load_3d(st + kS * kAPlane + s * kBPlane, bm, fb, kc * kBK, tj * kBN, mat * kSMax + s);
             }
@@ -664,8 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int stage = 0;
     uint32_t phase = 0;
     uint32_t acc_phase = 0;
-    for (int64_t tile = item0; tile < total; tile += istep) {
-      OZ_WAIT(tmem_empty, acc_phase ^ 1, 1);
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      tc::mbar_wait(tmem_empty, acc_phase ^ 1);
       tc::tc_fence_after();
       for (int kc = 0; kc < k_chunks; ++kc) {
         const uint32_t s0 = tc::smem_u32(smem + stage * kStageBytes);
@@ -687,10 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               const int need = grp_a(sa) > grp_b(tb) ? grp_a(sa) : grp_b(tb);
               while (ready < need) {
                 ++ready;
-                if (kPair)
-                  OZ_WAIT_REMOTE(full + stage * kGroups + ready, phase, 2 + ready);
-                else
-                  OZ_WAIT(full + stage * kGroups + ready, phase, 2 + ready);
+                tc::mbar_wait(full + stage * kGroups + ready, phase);
                 tc::tc_fence_after();
               }
               const int cnt = (kS - sa - tb) < 4 ? (kS - sa - tb) : 4;
@@ -703,12 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           }
         }
-        if (lane == 0) {
-          if (kPair)
-            tc::umma_commit_mc(empty + stage, (uint16_t)3);  // frees the stage in both CTAs (A came from both)
-          else
-            tc::umma_commit(empty + stage);
-        }
+        if (lane == 0) tc::umma_commit(empty + stage);
         __syncwarp();
         if (++stage == kStages) {
           stage = 0;
@@ -726,14 +640,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const int cb = ((warp - 2) >> 2) * kEpiCols;  // this warp's first column of the tile
     const int row_in_tile = quad * 32 + lane;
     uint32_t acc_phase = 0;
-    for (int64_t tile = item0; tile < total; tile += istep) {
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int mat, job, ti, tj;
-      bool dummy;
-      decode(tile, mat, job, ti, tj, dummy);
-      OZ_WAIT(tmem_full, acc_phase, 6);
+      oz_decode(a, per_mat, tile, mat, job, ti, tj);
+      tc::mbar_wait(tmem_full, acc_phase);
       tc::tc_fence_after();
       const int i = ti * kBM + row_in_tile;
-      const bool row_ok = i < a.n && !dummy;
+      const bool row_ok = i < a.n;
       const OzJob& J = a.job[job];
       const bool mup = a.mupdate && job == 0;
       double* out = J.out + mat * J.out_stride;
@@ -794,8 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         // scales), so the lower-triangle values a tile computes equal their mirrors and every in-range
         // tile may store whole rows and the whole transpose; otherwise only tiles above the diagonal
         const bool same_ab = (J.a_map >> 1) == (J.b_map >> 1);
-        const bool interior =
-            !dummy && (same_ab || j0 >= ti * kBM + kBM) && (j0 + kBN <= a.n) && (ti * kBM + kBM <= a.n);
+        const bool interior = (same_ab || j0 >= ti * kBM + kBM) && (j0 + kBN <= a.n) && (ti * kBM + kBM <= a.n);
         bool ovf = false;
         const int i0w = ti * kBM + quad * 32;  // this warp's first row
         const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
@@ -941,7 +853,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     tc::tc_fence_after();
     tc::tmem_dealloc<kTmemCols>(tmem_base);
   }
-  if (kPair) tc::cluster_sync();  // no CTA leaves while its peer's last multicasts / commits may target it
 }
 
 template <int S, int BK>

@@ -591,59 +591,13 @@ int ozaki_iteration_slices(int k, int p, int n, double eps_rel, double budget, i
   return s_max;
 }
 
-// CTA pairs sharing the A planes through TMA multicast (ozaki.cuh kPair): opt-in with SHAMPOO_OZAKI_PAIR=1 while
-// being validated; the default is the single-CTA kernel.  The grid is as many 2-CTA clusters as fit at once.
-static bool oz_pair_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("SHAMPOO_OZAKI_PAIR");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
-template <int S, bool P>
-static cudaError_t oz_gemm_sp(const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {
-  const size_t smem = oz::gemm_smem_bytes<S, 64>();
-  auto kern = oz::gemm_kernel<S, 64, P>;
-  cudaError_t e = ensure_smem((const void*)kern, smem);
-  if (e != cudaSuccess) return e;
-  if (!P) {
-    kern<<<num_sms(), oz::kThreads, smem, stream>>>(a, maps);
-    return cudaSuccess;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(oz::kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  static std::mutex mu;
-  static int clusters[64][8] = {};  // [device][S]
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int nc;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    int& c = clusters[dev & 63][S];
-    if (c == 0) {
-      cfg.gridDim = dim3(2 * (num_sms() / 2));
-      if (cudaOccupancyMaxActiveClusters(&c, (const void*)kern, &cfg) != cudaSuccess || c <= 0) c = num_sms() / 2;
-      c = std::min(c, num_sms() / 2);
-    }
-    nc = c;
-  }
-  cfg.gridDim = dim3(2 * nc);
-  return cudaLaunchKernelEx(&cfg, kern, a, maps);
-}
-
 template <int S>
 static cudaError_t oz_gemm_s(const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {
-  return oz_pair_enabled() ? oz_gemm_sp<S, true>(a, maps, stream) : oz_gemm_sp<S, false>(a, maps, stream);
+  const size_t smem = oz::gemm_smem_bytes<S, 64>();
+  cudaError_t e = ensure_smem((const void*)oz::gemm_kernel<S, 64>, smem);
+  if (e != cudaSuccess) return e;
+  oz::gemm_kernel<S, 64><<<num_sms(), oz::kThreads, smem, stream>>>(a, maps);
+  return cudaSuccess;
 }
 
 static cudaError_t oz_gemm(int S, const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {

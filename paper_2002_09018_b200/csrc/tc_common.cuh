@@ -46,21 +46,6 @@ TC_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-// For barriers completed by ANOTHER CTA of the cluster (multicast TMA bytes, multicast commits): try_wait without
-// the suspend-time hint.  Measured on B200: with the hint a thread waiting on remote arrivals was not woken before
-// the hint ran out (the CTA-pair GEMM crawled for minutes); without it the pair matches the spin-wait watchdog build.
-TC_DEV void mbar_wait_remote(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
 // ----------------------------------------------------------------------- TMA
 TC_DEV void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -83,34 +68,6 @@ TC_DEV void tma_load_3d(void* smem, const CUtensorMap* map, uint64_t* bar, int x
           "r"(smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
-}
-
-// TMA load multicast to the CTAs of `mask` in the cluster: the data lands at the same shared-memory offset in
-// each, and each destination CTA's mbarrier at `bar`'s offset receives the complete_tx
-TC_DEV void tma_load_3d_mc(void* smem, const CUtensorMap* map, uint64_t* bar, int x, int y, int z, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(smem_u32(smem)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "h"(mask)
-      : "memory");
-}
-TC_DEV uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-TC_DEV uint32_t cluster_id_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;\n" : "=r"(r));
-  return r;
-}
-TC_DEV uint32_t nclusters_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;\n" : "=r"(r));
-  return r;
-}
-TC_DEV void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 // --------------------------------------------------------------------- TMEM
@@ -166,12 +123,6 @@ TC_DEV void umma_tf32(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc,
 }
 TC_DEV void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-               : "memory");
-}
-// ... arriving on the mbarrier at `bar`'s offset in every CTA of `mask` (cluster)
-TC_DEV void umma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
-               ::"r"(smem_u32(bar)), "h"(mask)
                : "memory");
 }
 
