@@ -12,7 +12,7 @@
 // operand row), then rounded once to fp32.
 //
 // Per call: slice the rows of every G_b and of every X_R (fp32 sources) into 6
-// int8 planes at the kSMax pitch, then one persistent gemm_kernel<6, 64> launch
+// tiled int8 planes at the kSMax pitch, then one persistent gemm_kernel<6, 64> launch
 // per distinct n = cols over all eligible blocks (non-symmetric 128 x 64 tiles,
 // fp32 epilogue into P).  The graft denominator is computed afterwards from P
 // by precondition.cu's den kernel, as for every other block.
@@ -32,18 +32,18 @@ namespace shp {
 constexpr int kOzPrecS = 6;
 
 // One warp per (job, row < np): digits of an fp32 row src[row * ld + j], j < cols
-// (zero beyond cols and for rows >= rows), planes of job q at planes + q kSMax np^2.
+// (zero beyond cols and for rows >= rows), tiled planes of job q at planes + q kSMax plane_pitch(np).
 template <int S>
 __global__ void __launch_bounds__(256, 2) slice_f32_kernel(const OzSliceJob* __restrict__ jobs, int n_jobs, int np,
                                                            int8_t* __restrict__ planes, double* __restrict__ scale) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t plane_pitch = (int64_t)np * np;
+  const int64_t pitch = oz::plane_pitch(np);
   for (int64_t rid = gw; rid < (int64_t)n_jobs * np; rid += nw) {
     const int q = (int)(rid / np), i = (int)(rid - (int64_t)q * np);
     const OzSliceJob J = jobs[q];
-    int8_t* prow = planes + ((int64_t)q * oz::kSMax * np + i) * np;
+    int8_t* pmat = planes + (int64_t)q * oz::kSMax * pitch;
     const bool live = i < J.rows;
     const float* row = J.src + (int64_t)i * J.ld;
     double r[4][8];
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256, 2) slice_f32_kernel(const OzSliceJob* __r
         uint32_t dig[S][2];
         oz::slice8<S>(r[c], oz::digit_scale<S>(e), dig);
 #pragma unroll
-        for (int s = 0; s < S; ++s) oz::store8<S>(prow + s * plane_pitch, j, np, dig[s]);
+        for (int s = 0; s < S; ++s) oz::store8(pmat + s * pitch, i, j, np, dig[s]);
       }
     }
   }
@@ -78,7 +78,7 @@ bool oz_precondition_eligible(const shampoo_block_t& b) {
 
 static int64_t npad(int n) { return (n + 63) / 64 * 64; }
 
-// Layout of one call: groups of equal n; per group: job tables, planes, scales, maps.
+// Layout of one call: groups of equal n; per group: job tables, planes, scales.
 struct OzPrecGroup {
   int n, np, count;
   std::vector<int> blocks;
@@ -103,11 +103,10 @@ static std::vector<OzPrecGroup> oz_groups(const shampoo_block_t* B, int n_blocks
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static size_t group_bytes(const OzPrecGroup& g) {
-  const size_t planes = (size_t)g.count * oz::kSMax * g.np * g.np;
+  const size_t planes = (size_t)g.count * oz::kSMax * oz::plane_pitch(g.np);
   return 2 * al256(planes) + 2 * al256((size_t)g.count * g.np * sizeof(double)) +
          2 * al256((size_t)g.count * sizeof(OzSliceJob)) + al256((size_t)g.count * sizeof(float*)) +
-         al256((size_t)g.count * sizeof(int64_t)) + al256((size_t)g.count * sizeof(int)) +
-         al256(2 * sizeof(CUtensorMap));
+         al256((size_t)g.count * sizeof(int64_t)) + al256((size_t)g.count * sizeof(int));
 }
 
 size_t oz_precondition_bytes(const shampoo_block_t* B, int n_blocks, const int* flags) {
@@ -120,19 +119,13 @@ int oz_precondition_launch(const shampoo_tensor_t* T, const shampoo_block_t* B, 
                            const float* roots, void* ws, cudaStream_t stream, int64_t* launches) {
   const std::vector<OzPrecGroup> gs = oz_groups(B, n_blocks, flags);
   if (gs.empty()) return SHAMPOO_OK;
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult qr;
-  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
-      qr != cudaDriverEntryPointSuccess)
-    return set_error(SHAMPOO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   constexpr int S = kOzPrecS;
   const size_t smem = oz::gemm_smem_bytes<S, 64>();
   if (ensure_smem((const void*)oz::gemm_kernel<S, 64>, smem) != cudaSuccess)
     return set_cuda_error("cudaFuncSetAttribute(ozaki gemm_kernel, precondition)");
   char* w = static_cast<char*>(ws);
   for (const OzPrecGroup& g : gs) {
-    const size_t planes_b = al256((size_t)g.count * oz::kSMax * g.np * g.np);
+    const size_t planes_b = al256((size_t)g.count * oz::kSMax * oz::plane_pitch(g.np));
     const size_t scale_b = al256((size_t)g.count * g.np * sizeof(double));
     int8_t* pg = reinterpret_cast<int8_t*>(w);
     int8_t* px = reinterpret_cast<int8_t*>(w + planes_b);
@@ -148,8 +141,6 @@ int oz_precondition_launch(const shampoo_tensor_t* T, const shampoo_block_t* B, 
     int64_t* outld = reinterpret_cast<int64_t*>(q);
     q += al256((size_t)g.count * sizeof(int64_t));
     int* outrows = reinterpret_cast<int*>(q);
-    q += al256((size_t)g.count * sizeof(int));
-    CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(q);
     w += group_bytes(g);
     // host tables: one async copy each (the library stays stateless; the host vectors live until the copies are
     // issued -- pageable sources are staged by cudaMemcpyAsync before it returns)
@@ -166,16 +157,11 @@ int oz_precondition_launch(const shampoo_tensor_t* T, const shampoo_block_t* B, 
       hl[k] = t.ldp;
       hr[k] = b.rows;
     }
-    CUtensorMap hm[2];
-    if (oz::make_plane_map(enc, &hm[0], pg, g.n, g.np, g.count, oz::kBM, 64) != CUDA_SUCCESS ||
-        oz::make_plane_map(enc, &hm[1], px, g.n, g.np, g.count, oz::kBN, 64) != CUDA_SUCCESS)
-      return set_error(SHAMPOO_ERR_CUDA, "ozaki precondition: cuTensorMapEncodeTiled failed");
     if (cudaMemcpyAsync(jg, hg.data(), g.count * sizeof(OzSliceJob), cudaMemcpyHostToDevice, stream) ||
         cudaMemcpyAsync(jx, hx.data(), g.count * sizeof(OzSliceJob), cudaMemcpyHostToDevice, stream) ||
         cudaMemcpyAsync(outf, ho.data(), g.count * sizeof(float*), cudaMemcpyHostToDevice, stream) ||
         cudaMemcpyAsync(outld, hl.data(), g.count * sizeof(int64_t), cudaMemcpyHostToDevice, stream) ||
-        cudaMemcpyAsync(outrows, hr.data(), g.count * sizeof(int), cudaMemcpyHostToDevice, stream) ||
-        cudaMemcpyAsync(maps, hm, sizeof hm, cudaMemcpyHostToDevice, stream))
+        cudaMemcpyAsync(outrows, hr.data(), g.count * sizeof(int), cudaMemcpyHostToDevice, stream))
       return set_cuda_error("cudaMemcpyAsync(ozaki precondition tables)");
     const int grid = 8 * num_sms();
     slice_f32_kernel<S><<<grid, 256, 0, stream>>>(jg, g.count, g.np, pg, sg);
@@ -190,8 +176,8 @@ int oz_precondition_launch(const shampoo_tensor_t* T, const shampoo_block_t* B, 
     a.sym = 0;
     a.jobs = 1;
     a.p = 1;
-    a.job[0].a_map = 0;
-    a.job[0].b_map = 1;
+    a.job[0].a_planes = pg;
+    a.job[0].b_planes = px;
     a.job[0].a_scale = sg;
     a.job[0].b_scale = sx;
     a.job[0].outf = outf;
@@ -199,7 +185,7 @@ int oz_precondition_launch(const shampoo_tensor_t* T, const shampoo_block_t* B, 
     a.job[0].outf_rows = outrows;
     void* tok;
     prof_begin_launch("ozaki_precondition", stream, &tok);
-    oz::gemm_kernel<S, 64><<<num_sms(), oz::kThreads, smem, stream>>>(a, maps);
+    oz::gemm_kernel<S, 64><<<num_sms(), oz::kThreads, smem, stream>>>(a);
     prof_end_launch(tok, stream);
     *launches += 3;
   }

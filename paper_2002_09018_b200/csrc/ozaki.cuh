@@ -18,12 +18,13 @@
 // S is a template parameter (6 or 7; the precision choice).
 //
 // GEMM kernel: one CTA per SM, persistent over 128 x 64 output tiles; warp 0 =
-// TMA producer (per 64-byte k-chunk: S A-planes 128 x 64 B and S B-planes 64 x
-// 64 B, SWIZZLE_64B, 2-stage ring for S = 7, 3 stages for S = 6), warp 1 = TMEM
-// allocator + MMA issuer (the S(S+1)/2 slice pairs of a k-step in 10 (S = 7) /
-// 8 (S = 6) tcgen05.mma.kind::i8 of M = 128, N = 64..256, K = 32), warps 2..5 =
-// epilogue (S tcgen05.ld per 8 columns behind one wait, fp64 combination,
-// mode-specific store).
+// bulk-copy producer (per 64-byte k-chunk: S A-planes 128 x 64 B and S B-planes
+// 64 x 64 B, each one contiguous pre-swizzled block of the tiled plane layout;
+// 2-stage ring for S = 7, 3 stages for S = 6, 5), warp 1 = TMEM allocator + MMA
+// issuer (the S(S+1)/2 slice pairs of a k-step in 10 (S = 7) / 8 (S = 6)
+// tcgen05.mma.kind::i8 of M = 128, N = 64..256, K = 32), warps 2..9 = epilogue
+// (S tcgen05.ld per 8 columns behind one wait, fp64 combination, mode-specific
+// store).
 #pragma once
 #include <cuda.h>
 #include <stdint.h>
@@ -40,11 +41,26 @@ namespace oz {
 // (the per-iteration slice schedule, reading #29)
 constexpr int kSMax = 7;
 constexpr int kBM = 128, kBN = 64;  // tile M, N
+
+// Plane layout (round 2): every n x n int8 plane is stored as 64-row x 64-byte tiles, k-block major (tile (kb, rb)
+// at (kb * nrb + rb) * 4096 bytes, nrb row blocks), each tile already in the shared-memory SWIZZLE_64B pattern the
+// UMMA descriptors read (16-byte chunk c of row r at chunk c ^ ((r >> 1) & 3)).  An A tile (128 rows) is then ONE
+// contiguous 8 KB block and a B tile one 4 KB block, moved by plain 1-D bulk copies: measured on B200 +8 / +11 /
+// +14% executed TOPS at S = 7 / 6 / 5 over 3-D tensor-map copies of row-major planes (whose 64-byte rows are
+// separate requests; 32-byte rows were slower still).  Rows are padded to a multiple of 128 (whole A tiles), the k
+// extent to np (a multiple of 64).  Writers zero the k padding (columns n .. np-1) of rows < n; padding rows are
+// never written and only reach outputs the epilogue discards.
+__host__ __device__ constexpr int64_t plane_rows(int np) { return (int64_t)(np + 127) / 128 * 128; }
+__host__ __device__ constexpr int64_t plane_pitch(int np) { return plane_rows(np) * np; }
+__host__ __device__ __forceinline__ int64_t tiled_off(int i, int j, int np) {
+  return ((int64_t)(j >> 6) * (plane_rows(np) >> 6) + (i >> 6)) * 4096 + ((i & 63) << 6) +
+         ((((j >> 4) & 3) ^ ((i >> 1) & 3)) << 4) + (j & 15);
+}
 // k-chunk BK bytes (int8 elements) per pipeline stage: BK / 32 K=32 MMA steps
 template <int S, int BK>
 struct Cfg {
   static_assert(S >= 4 && S <= kSMax, "4 <= slices <= 7 (int32 digit split, TMEM columns)");
-  static_assert(BK == 32 || BK == 64, "SWIZZLE_32B / SWIZZLE_64B k-chunks");
+  static_assert(BK == 64, "64-byte k-chunks: the tiled plane layout");
   static constexpr int kAPlane = kBM * BK;                     // 8 KB (BK = 64)
   static constexpr int kBPlane = kBN * BK;                     // 4 KB
   static constexpr int kStageBytes = S * (kAPlane + kBPlane);  // 84 KB (S = 7, BK = 64), 72 KB (S = 6)
@@ -71,8 +87,8 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 #endif
 constexpr uint32_t kTmemCols = 512;         // S accumulators x 64 columns (448 used for S = 7)
 
-// K-major tile of BK-byte rows, swizzled to match the TMA map (SWIZZLE_32B:
-// layout type 6, 8-row atoms of 256 B; SWIZZLE_64B: type 4, 512 B)
+// K-major tile of BK-byte rows in the SWIZZLE_64B pattern of the tiled planes (layout type 4, 8-row atoms of
+// 512 B; SWIZZLE_32B: type 6)
 template <int kBK>
 TC_DEV uint64_t desc_sw(uint32_t smem_addr) {
   uint64_t d = 0;
@@ -156,15 +172,9 @@ __device__ __forceinline__ void load8(const double* row, int j, int n, double (&
   }
 }
 
-template <int S>
-__device__ __forceinline__ void store8(int8_t* plane_row, int j, int n, const uint32_t (&w)[2]) {
-  if (j + 8 <= n) {
-    *reinterpret_cast<uint2*>(plane_row + j) = make_uint2(w[0], w[1]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (j + q < n) plane_row[j + q] = (int8_t)((w[q >> 2] >> (8 * (q & 3))) & 0xFFu);
-  }
+// digits of row i, columns j .. j+7 (j % 8 == 0, j < np: the k padding is stored as zeros) into a tiled plane
+__device__ __forceinline__ void store8(int8_t* plane, int i, int j, int np, const uint32_t (&w)[2]) {
+  *reinterpret_cast<uint2*>(plane + tiled_off(i, j, np)) = make_uint2(w[0], w[1]);
 }
 
 // Row exponent: e with max|row| < 2^e (0 for a zero row)
@@ -211,13 +221,13 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = act ? *nact : batch;
-  const int64_t plane_pitch = (int64_t)np * np;
+  const int64_t pitch = plane_pitch(np);
   const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p, ninv_p = -inv_p;
   for (int64_t rid = gw; rid < (int64_t)na * n; rid += nw) {
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
-    int8_t* prow = planes + ((int64_t)mat * kSMax * np + i) * np;
+    int8_t* pmat = planes + (int64_t)mat * kSMax * pitch;
     // TM: off the diagonal T_ij = -M_ij / p (one multiply: the same value as (0 - m) / p up to the sign
     // of zero); the diagonal element once per row
     const double tii = TM ? t_of(row[i], true, pp1, inv_p) : 0.0;
@@ -245,11 +255,11 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
 #pragma unroll
       for (int c = 0; c < kRegChunks; ++c) {
         const int j = 256 * c + 8 * lane;
-        if (j < n) {
+        if (j < np) {  // columns n .. np-1: zero digits (r = 0 there)
           uint32_t dig[S][2];
           slice8<S>(r[c], digit_scale<S>(e), dig);
 #pragma unroll
-          for (int s = 0; s < S; ++s) store8<S>(prow + s * plane_pitch, j, n, dig[s]);
+          for (int s = 0; s < S; ++s) store8(pmat + s * pitch, i, j, np, dig[s]);
         }
       }
     } else {
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
       for (int j = lane; j < n; j += 32) mx = fmax(mx, fabs(TM ? ((j == i) ? tii : row[j] * ninv_p) : row[j]));
       const int e = row_exponent(mx);
       if (lane == 0) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
-      for (int j = 8 * lane; j < n; j += 256) {
+      for (int j = 8 * lane; j < np; j += 256) {
         double r[8];
         load8(row, j, n, r);
         if (TM) {
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
         uint32_t dig[S][2];
         slice8<S>(r, digit_scale<S>(e), dig);
 #pragma unroll
-        for (int s = 0; s < S; ++s) store8<S>(prow + s * plane_pitch, j, n, dig[s]);
+        for (int s = 0; s < S; ++s) store8(pmat + s * pitch, i, j, np, dig[s]);
       }
     }
   }
@@ -289,13 +299,13 @@ __global__ void __launch_bounds__(32 * kSliceMtWarps, 4) slice_mt_kernel(
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = act ? *nact : batch;
-  const int64_t plane_pitch = (int64_t)np * np;
+  const int64_t pitch = plane_pitch(np);
   const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p, ninv_p = -inv_p;
   for (int64_t rid = gw; rid < (int64_t)na * n; rid += nw) {
     const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
     const int mat = act ? act[pos] : pos;
     const double* row = src + mat * mat_stride + (int64_t)i * np;
-    const int64_t prow = ((int64_t)mat * kSMax * np + i) * np;
+    const int64_t pmat = (int64_t)mat * kSMax * pitch;
     const double tii = t_of(row[i], true, pp1, inv_p);
     double mx = 0.0, mo = 0.0;  // max |M_ij| over the row, and over the row without the diagonal
     {
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(32 * kSliceMtWarps, 4) slice_mt_kernel(
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       const int j = 256 * c + 8 * lane;
-      if (j < n) {
+      if (j < np) {  // the staged row is zero beyond n: zero digits in the k padding
         double r[8];
         const double4 a0 = reinterpret_cast<const double4*>(my + j)[0];
         const double4 a1 = reinterpret_cast<const double4*>(my + j)[1];
@@ -342,12 +352,12 @@ __global__ void __launch_bounds__(32 * kSliceMtWarps, 4) slice_mt_kernel(
         uint32_t dig[S][2];
         slice8<S>(r, sm, dig);
 #pragma unroll
-        for (int s = 0; s < S; ++s) store8<S>(planes_m + prow + s * plane_pitch, j, n, dig[s]);
+        for (int s = 0; s < S; ++s) store8(planes_m + pmat + s * pitch, i, j, np, dig[s]);
 #pragma unroll
         for (int q = 0; q < 8; ++q) r[q] = (j + q == i) ? tii : r[q] * ninv_p;
         slice8<S>(r, st, dig);
 #pragma unroll
-        for (int s = 0; s < S; ++s) store8<S>(planes_t + prow + s * plane_pitch, j, n, dig[s]);
+        for (int s = 0; s < S; ++s) store8(planes_t + pmat + s * pitch, i, j, np, dig[s]);
       }
     }
     __syncwarp();  // the row buffer is rewritten by the next row
@@ -429,13 +439,14 @@ __device__ __forceinline__ double scale2(double x, int k) {
 }
 
 struct OzJob {
-  int a_map, b_map;         // TMA maps of the A-use (128-row box) / B-use (64-row box) planes
+  const int8_t* a_planes;   // tiled planes of the A operand (plane s of matrix mat at (mat kSMax + s) plane_pitch)
+  const int8_t* b_planes;   // and of the B operand (C = A B^T: both row-major in k)
   const double* a_scale;    // [mat * np + row] = 2^e
   const double* b_scale;
   double* out;              // fp64 output of matrix 0; matrix m at out + m * out_stride
   int64_t out_stride;
-  // sliced output (out == nullptr, symmetric products only): the product's S int8 planes at
-  // planes[(mat kSMax + s) np^2], every row scaled by the a-priori bound 2^out_e (|C_ij| < 2^out_e),
+  // sliced output (out == nullptr, symmetric products only): the product's S int8 tiled planes at
+  // planes + (mat kSMax + s) plane_pitch, every row scaled by the a-priori bound 2^out_e (|C_ij| < 2^out_e),
   // 2^out_e written to out_scale[mat np + row]
   int8_t* planes;
   double* out_scale;
@@ -509,8 +520,7 @@ __host__ __device__ constexpr int grp_bytes(int g) {
 }
 
 template <int S, int BK>
-__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a,
-                                                          const CUtensorMap* __restrict__ maps) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ OzArgs a) {
   using C = Cfg<S, BK>;
   constexpr int kS = S, kBK = BK, kStages = C::kStages, kStageBytes = C::kStageBytes;
   static_assert(grp_bytes<S, BK>(0) + grp_bytes<S, BK>(1) + grp_bytes<S, BK>(2) + grp_bytes<S, BK>(3) == kStageBytes,
@@ -548,14 +558,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (tc::elect_one()) {
-      for (int q = 0; q < 2 * a.jobs; ++q) tc::tma_acquire(maps + (q & 1 ? a.job[q >> 1].b_map : a.job[q >> 1].a_map));
+      const int64_t pitch = plane_pitch(a.np);
+      const int nrb = (int)(plane_rows(a.np) >> 6);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
         int mat, job, ti, tj;
         oz_decode(a, per_mat, tile, mat, job, ti, tj);
-        const CUtensorMap* am = maps + a.job[job].a_map;
-        const CUtensorMap* bm = maps + a.job[job].b_map;
+        // this tile's planes: A rows 128 ti .. (row blocks 2 ti, 2 ti + 1: 8 KB), B rows 64 tj .. (4 KB) per k-block
+        const int8_t* pa = a.job[job].a_planes + (int64_t)mat * kSMax * pitch + (int64_t)(2 * ti) * 4096;
+        const int8_t* pb = a.job[job].b_planes + (int64_t)mat * kSMax * pitch + (int64_t)tj * 4096;
         for (int kc = 0; kc < k_chunks; ++kc) {
           tc::mbar_wait(empty + stage, phase ^ 1);
           uint8_t* st = smem + stage * kStageBytes;
@@ -567,11 +579,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             continue;
 #endif
             tc::mbar_arrive_expect_tx(fb, grp_bytes<S, BK>(g));
+            const int64_t kb = (int64_t)kc * nrb * 4096;
 #pragma unroll
             for (int s = 0; s < kS; ++s) {
-              if (grp_a(s) == g) tc::tma_load_3d(st + s * kAPlane, am, fb, kc * kBK, ti * kBM, mat * kSMax + s);
-              if (grp_b(s) == g)
-                tc::tma_load_3d(st + kS * kAPlane + s * kBPlane, bm, fb, kc * kBK, tj * kBN, mat * kSMax + s);
+              if (grp_a(s) == g) tc::bulk_load(st + s * kAPlane, pa + s * pitch + kb, kAPlane, fb);
+              if (grp_b(s) == g) tc::bulk_load(st + kS * kAPlane + s * kBPlane, pb + s * pitch + kb, kBPlane, fb);
             }
           }
           if (++stage == kStages) {
@@ -701,12 +713,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         // strictly above the diagonal a warp-level 4 x 32 byte transpose (shuffles) turns it into 4-byte
         // stores of whole sectors; diagonal-band and ragged tiles store bytes
         const int j0 = tj * kBN;
-        const int64_t pitch = (int64_t)a.np * a.np;
+        const int64_t pitch = plane_pitch(a.np);
         int8_t* pl = J.planes + (int64_t)mat * kSMax * pitch;
         // A = B (squarings): C is computed bit-symmetrically (the same exact integer pair sums, the same
         // scales), so the lower-triangle values a tile computes equal their mirrors and every in-range
         // tile may store whole rows and the whole transpose; otherwise only tiles above the diagonal
-        const bool same_ab = (J.a_map >> 1) == (J.b_map >> 1);
+        const bool same_ab = J.a_planes == J.b_planes;
         const bool interior = (same_ab || j0 >= ti * kBM + kBM) && (j0 + kBN <= a.n) && (ti * kBM + kBM <= a.n);
         bool ovf = false;
         const int i0w = ti * kBM + quad * 32;  // this warp's first row
@@ -718,12 +730,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         {
           const int h = cb;
           unsigned long long w[kEpiCols];
+          const int lim = a.n - (j0 + h);  // columns >= n (padding B rows, never written) stay 0: no false overflow
 #pragma unroll
           for (int e = 0; e < kEpiCols; e += 2) {
             if (row_ok) {
               const double2 b2 = *reinterpret_cast<const double2*>(bs + h + e);
-              w[e] = int_w<kS>(scale2(v[e], ka + exp2_of(b2.x)), J.out_e, ovf);
-              w[e + 1] = int_w<kS>(scale2(v[e + 1], ka + exp2_of(b2.y)), J.out_e, ovf);
+              w[e] = e < lim ? int_w<kS>(scale2(v[e], ka + exp2_of(b2.x)), J.out_e, ovf) : 0ull;
+              w[e + 1] = e + 1 < lim ? int_w<kS>(scale2(v[e + 1], ka + exp2_of(b2.y)), J.out_e, ovf) : 0ull;
             } else {
               w[e] = w[e + 1] = 0ull;
             }
@@ -738,9 +751,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               wd[k] = w_byte<kS>(w[4 * k], s2) | (w_byte<kS>(w[4 * k + 1], s2) << 8) |
                       (w_byte<kS>(w[4 * k + 2], s2) << 16) | (w_byte<kS>(w[4 * k + 3], s2) << 24);
             if (interior) {
-              uint4* dst = reinterpret_cast<uint4*>(ps + (int64_t)i * a.np + j0 + h);
 #pragma unroll
-              for (int q = 0; q < kW / 4; ++q) dst[q] = make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
+              for (int q = 0; q < kW / 4; ++q)
+                *reinterpret_cast<uint4*>(ps + tiled_off(i, j0 + h + 16 * q, a.np)) =
+                    make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
               // mirror rows j0 + h + 4k + (lane >> 3), columns i0w + 4 (lane & 7) .. + 3
               const int src = 4 * (lane & 7), sel = 8 * (lane >> 3);
 #pragma unroll
@@ -751,15 +765,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                 const uint32_t x3 = __shfl_sync(0xffffffffu, wd[k], src + 3);
                 const uint32_t o = ((x0 >> sel) & 0xFFu) | (((x1 >> sel) & 0xFFu) << 8) |
                                    (((x2 >> sel) & 0xFFu) << 16) | (((x3 >> sel) & 0xFFu) << 24);
-                *reinterpret_cast<uint32_t*>(ps + (int64_t)(j0 + h + 4 * k + (lane >> 3)) * a.np + i0w + src) = o;
+                *reinterpret_cast<uint32_t*>(ps + tiled_off(j0 + h + 4 * k + (lane >> 3), i0w + src, a.np)) = o;
               }
             } else if (row_ok) {
 #pragma unroll
               for (int e = 0; e < kEpiCols; ++e) {
                 const int j = j0 + h + e;
                 const int8_t byte = (int8_t)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
-                if (j < a.n && j >= i) ps[(int64_t)i * a.np + j] = byte;
-                if (j < a.n && j > i) ps[(int64_t)j * a.np + i] = byte;
+                if (j < a.n && j >= i) ps[tiled_off(i, j, a.np)] = byte;
+                if (j < a.n && j > i) ps[tiled_off(j, i, a.np)] = byte;
+                if (j >= a.n && j < a.np) ps[tiled_off(i, j, a.np)] = 0;  // the k padding of row i
               }
             }
           }
@@ -857,21 +872,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
 template <int S, int BK>
 inline size_t gemm_smem_bytes() { return 1024 + (size_t)Cfg<S, BK>::kStages * Cfg<S, BK>::kStageBytes + 512; }
-
-// 3-D TMA map over int8 slice planes: (k bytes = n, rows = n, planes = batch * kSMax),
-// row pitch np bytes, plane pitch np*np bytes, box (64 B, box_rows, 1), SWIZZLE_64B
-template <class Encode>
-inline CUresult make_plane_map(Encode enc, CUtensorMap* out, const int8_t* base, int n, int np, int batch,
-                               int box_rows, int kBK) {
-  cuuint64_t gdim[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)batch * kSMax};
-  cuuint64_t gstride[2] = {(cuuint64_t)np, (cuuint64_t)np * np};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
-  cuuint32_t estride[3] = {1, 1, 1};
-  return enc(out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), gdim, gstride, box, estride,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, kBK == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-}
 
 }  // namespace oz
 }  // namespace shp

@@ -545,10 +545,10 @@ int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter
 enum { OZ_SX = 0, OZ_ST = 1, OZ_SS0 = 2, OZ_SS1 = 3, OZ_SM = 4, OZ_SLOTS = 5 };
 
 size_t root_ozaki_ws_bytes(int batch, int n) {
-  const size_t np = (size_t)((n + 63) / 64 * 64);
-  const size_t planes = (size_t)OZ_SLOTS * batch * oz::kSMax * np * np;
+  const int np = (n + 63) / 64 * 64;
+  const size_t planes = (size_t)OZ_SLOTS * batch * oz::kSMax * oz::plane_pitch(np);
   const size_t scales = (size_t)OZ_SLOTS * batch * np * sizeof(double);
-  return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 2 * OZ_SLOTS * sizeof(CUtensorMap) + 256;
+  return ((planes + 255) / 256 * 256) + ((scales + 255) / 256 * 256) + 256;
 }
 
 // Iterations enqueued one launch at a time before the convergence-driven tail graph takes over: the scalar
@@ -592,19 +592,19 @@ int ozaki_iteration_slices(int k, int p, int n, double eps_rel, double budget, i
 }
 
 template <int S>
-static cudaError_t oz_gemm_s(const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {
+static cudaError_t oz_gemm_s(const oz::OzArgs& a, cudaStream_t stream) {
   const size_t smem = oz::gemm_smem_bytes<S, 64>();
   cudaError_t e = ensure_smem((const void*)oz::gemm_kernel<S, 64>, smem);
   if (e != cudaSuccess) return e;
-  oz::gemm_kernel<S, 64><<<num_sms(), oz::kThreads, smem, stream>>>(a, maps);
+  oz::gemm_kernel<S, 64><<<num_sms(), oz::kThreads, smem, stream>>>(a);
   return cudaSuccess;
 }
 
-static cudaError_t oz_gemm(int S, const oz::OzArgs& a, const CUtensorMap* maps, cudaStream_t stream) {
+static cudaError_t oz_gemm(int S, const oz::OzArgs& a, cudaStream_t stream) {
   switch (S) {
-    case 5: return oz_gemm_s<5>(a, maps, stream);
-    case 6: return oz_gemm_s<6>(a, maps, stream);
-    default: return oz_gemm_s<7>(a, maps, stream);
+    case 5: return oz_gemm_s<5>(a, stream);
+    case 6: return oz_gemm_s<6>(a, stream);
+    default: return oz_gemm_s<7>(a, stream);
   }
 }
 
@@ -704,32 +704,13 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   if (batch > kTailMaxBatch) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: batch chunk > %d", kTailMaxBatch);
   if (np % 64) return set_error(SHAMPOO_ERR_UNSUPPORTED, "ozaki root: padded n must be a multiple of 64");
   char* w = static_cast<char*>(oz_ws);
-  const size_t slot_planes = (size_t)batch * oz::kSMax * np * np;  // every slot at the kSMax plane pitch
+  const size_t slot_planes = (size_t)batch * oz::kSMax * oz::plane_pitch(np);  // every slot at the kSMax pitch
   int8_t* planes = reinterpret_cast<int8_t*>(w);
   const size_t planes_bytes = ((size_t)OZ_SLOTS * slot_planes + 255) / 256 * 256;
   double* scales = reinterpret_cast<double*>(w + planes_bytes);
   const size_t scales_bytes = ((size_t)OZ_SLOTS * batch * np * sizeof(double) + 255) / 256 * 256;
-  CUtensorMap* maps_dev = reinterpret_cast<CUtensorMap*>(w + planes_bytes + scales_bytes);
   auto slot_planes_ptr = [&](int slot) { return planes + (size_t)slot * slot_planes; };
   auto slot_scale = [&](int slot) { return scales + (size_t)slot * batch * np; };
-  // maps: slot q -> 2q (A use, 128-row box), 2q+1 (B use, 64-row box); independent of the slice count
-  CUtensorMap maps[2 * OZ_SLOTS];
-  {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return set_error(SHAMPOO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    for (int q2 = 0; q2 < OZ_SLOTS; ++q2) {
-      if (oz::make_plane_map(enc, &maps[2 * q2], slot_planes_ptr(q2), n, np, batch, oz::kBM, 64) != CUDA_SUCCESS ||
-          oz::make_plane_map(enc, &maps[2 * q2 + 1], slot_planes_ptr(q2), n, np, batch, oz::kBN, 64) !=
-              CUDA_SUCCESS)
-        return set_error(SHAMPOO_ERR_CUDA, "ozaki: cuTensorMapEncodeTiled failed");
-    }
-  }
-  if (cudaMemcpyAsync(maps_dev, maps, sizeof maps, cudaMemcpyHostToDevice, stream) != cudaSuccess)
-    return set_cuda_error("cudaMemcpyAsync(ozaki maps)");
   const int64_t mstride = (int64_t)kTailRegions * np * np;
   auto region = [&](int r) { return bufs + (int64_t)r * np * np; };
   // tm: slice T_k = ((p+1)I - M_k)/p computed from M_k on the fly (T_k never stored in fp64)
@@ -749,8 +730,8 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   base.jobs = 1;
   auto job = [&](int sa, int sb, int out_reg) {
     oz::OzJob j;
-    j.a_map = 2 * sa;
-    j.b_map = 2 * sb + 1;
+    j.a_planes = slot_planes_ptr(sa);
+    j.b_planes = slot_planes_ptr(sb);
     j.a_scale = slot_scale(sa);
     j.b_scale = slot_scale(sb);
     j.out = region(out_reg);
@@ -779,11 +760,11 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
   };
   // one iteration's launches on stream `st`: k = the iteration (direct) or, with kdev, its parity only (the tail
   // graph's body reads k from *kdev); `prof`: bracket the GEMMs with CUDA events (not inside a graph)
-  int* kdev = reinterpret_cast<int*>(maps_dev + 2 * OZ_SLOTS);
+  int* kdev = reinterpret_cast<int*>(w + planes_bytes + scales_bytes);
   auto gemm = [&](int S, const oz::OzArgs& a, cudaStream_t st, bool prof) -> int {
     void* tok = nullptr;
     if (prof) prof_begin_launch("ozaki_gemm", st, &tok);
-    cudaError_t e = oz_gemm(S, a, maps_dev, st);
+    cudaError_t e = oz_gemm(S, a, st);
     if (prof) prof_end_launch(tok, st);
     if (e != cudaSuccess) return set_cuda_error("ozaki gemm launch", e);
     ++*launches;

@@ -70,6 +70,14 @@ TC_DEV void tma_load_3d(void* smem, const CUtensorMap* map, uint64_t* bar, int x
       : "memory");
 }
 
+// plain bulk copy of a contiguous (pre-swizzled) global block into shared memory, bytes % 16 == 0
+TC_DEV void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(smem)),
+               "l"(reinterpret_cast<uint64_t>(gmem)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // --------------------------------------------------------------------- TMEM
 template <uint32_t kCols>
 TC_DEV void tmem_alloc(uint32_t* dst_smem) {  // whole warp
