@@ -283,84 +283,139 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const double* __restrict_
   }
 }
 
-// M_k and T_k = ((p+1)I - M_k)/p sliced in ONE pass over M_k (rows of n <= 1024): saves the second 8 MB read
-// per matrix of separate M and T slicers.  Each warp stages its row in shared memory (8 KB; one HBM pass, all
-// of the row's loads in flight at once), then slices M and T chunk by chunk from there: only 8 elements live in
-// registers at a time (round 1 held the whole row in registers and spilled; 50-55% of HBM bandwidth).
-constexpr int kSliceMtWarps = 4;
-template <int S>
-__global__ void __launch_bounds__(32 * kSliceMtWarps, 4) slice_mt_kernel(
+// Row-pair slicer (rows of n <= 1024): one warp per pair of rows (i0, i0 + 1), i0 even, staged in shared memory by
+// ONE bulk copy (the two rows are adjacent in HBM), then sliced from there.  Lanes 0-7 / 8-15 take 64 columns of row
+// i0 / i0 + 1 in the same k-block, lanes 16-31 the next k-block, so every 8-byte-per-lane store instruction writes
+// two WHOLE 128-byte lines of the tiled planes (rows i0, i0 + 1 of a tile are adjacent).  One row per warp wrote
+// half lines: 3.5 vs 5.9 TB/s for the M/T slicer at S = 7 (tools/microbench/slice_layout.cu, r02ze).
+// MODE 0: A = src;  MODE 1: T_k = ((p+1)I - M_k)/p from src = M_k (T_k is never stored in fp64);  MODE 2: both M_k
+// (planes / scale) and T_k (planes_t / scale_t) in one pass over M_k.  Columns n .. np-1 get zero digits.
+// W warps per CTA, B pair buffers (16 KB each) per warp: the next B - 1 pairs' copies are in flight while a pair is
+// sliced.
+constexpr int kPairWarps = 4, kPairBufs = 1;
+template <int W, int B>
+constexpr size_t pair_smem() { return (size_t)W * B * 2048 * sizeof(double) + (size_t)W * B * sizeof(uint64_t); }
+constexpr size_t kPairSmem = pair_smem<kPairWarps, kPairBufs>();
+template <int S, int MODE, int W = kPairWarps, int B = kPairBufs>
+__global__ void __launch_bounds__(32 * W) slice_pair_kernel(
     const double* __restrict__ src, int64_t mat_stride, int n, int np, int batch, const int* __restrict__ act,
-    const int* nact, int8_t* __restrict__ planes_m, double* __restrict__ scale_m, int8_t* __restrict__ planes_t,
+    const int* nact, int8_t* __restrict__ planes, double* __restrict__ scale, int8_t* __restrict__ planes_t,
     double* __restrict__ scale_t, int p) {
-  __shared__ __align__(16) double srow[kSliceMtWarps][1024];
+  extern __shared__ __align__(128) uint8_t pair_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* my = srow[wib];
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double* bufs = reinterpret_cast<double*>(pair_smem) + (size_t)wib * B * 2048;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pair_smem + (size_t)W * B * 2048 * sizeof(double)) + wib * B;
+  if (lane == 0) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) tc::mbar_init(bars + b, 1);
+    tc::fence_barrier_init();
+  }
+  __syncwarp();
   const int na = act ? *nact : batch;
+  const int per_mat = (n + 1) >> 1;
+  const int64_t total = (int64_t)na * per_mat;
+  const int64_t gw = (int64_t)blockIdx.x * W + wib, nw = (int64_t)gridDim.x * W;
+  // lane 0: the bulk copy of pair pid's two rows (adjacent in HBM; only the first n of the second) into buffer b
+  auto issue = [&](int64_t pid, int b) {
+    const int pos = (int)(pid / per_mat), i0 = 2 * (int)(pid - (int64_t)pos * per_mat);
+    const int mat = act ? act[pos] : pos;
+    const uint32_t bytes = (uint32_t)(((i0 + 1 < n ? np + n : n) * 8 + 15) & ~15);  // within the rows' padding
+    tc::mbar_arrive_expect_tx(bars + b, bytes);
+    tc::bulk_load(bufs + (size_t)b * 2048, src + mat * mat_stride + (int64_t)i0 * np, bytes, bars + b);
+  };
+  if (lane == 0)
+    for (int b = 0; b < B; ++b)
+      if (gw + b * nw < total) issue(gw + b * nw, b);
   const int64_t pitch = plane_pitch(np);
   const double pp1 = (double)(p + 1), inv_p = 1.0 / (double)p, ninv_p = -inv_p;
-  for (int64_t rid = gw; rid < (int64_t)na * n; rid += nw) {
-    const int pos = (int)(rid / n), i = (int)(rid - (int64_t)pos * n);
+  const int r = (lane >> 3) & 1;        // this lane's row of the pair
+  const int cl = 64 * (lane >> 4) + 8 * (lane & 7);  // its first column in each 128-column step
+  const int steps = (np + 127) >> 7;
+  int b = 0;
+  uint32_t phase = 0;  // of buffer b (all buffers flip together, once per round of B pairs)
+  for (int64_t pid = gw; pid < total; pid += nw) {
+    const int pos = (int)(pid / per_mat), i0 = 2 * (int)(pid - (int64_t)pos * per_mat);
     const int mat = act ? act[pos] : pos;
-    const double* row = src + mat * mat_stride + (int64_t)i * np;
-    const int64_t pmat = (int64_t)mat * kSMax * pitch;
-    const double tii = t_of(row[i], true, pp1, inv_p);
-    double mx = 0.0, mo = 0.0;  // max |M_ij| over the row, and over the row without the diagonal
-    {
-      double r[4][8];
+    double* buf = bufs + (size_t)b * 2048;
+    tc::mbar_wait(bars + b, phase);
+    const int i = i0 + r;
+    const bool live = i < n;
+    const double* my = buf + r * np;
+    const double mii = live ? my[i] : 0.0;
+    const double tii = t_of(mii, true, pp1, inv_p);
+    // row maxima over the 16 lanes of this row: |A| (MODE 0), |M| and |M| off the diagonal (MODE 1, 2)
+    double mx = 0.0, mo = 0.0;
+    for (int c = 0; c < steps; ++c) {
+      const int j = 128 * c + cl;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int j = 256 * c + 8 * lane;
-        if (j < n) {
-          load8(row, j, n, r[c]);
+      for (int q = 0; q < 8; ++q) {
+        const double v = (live && j + q < n) ? my[j + q] : 0.0;
+        mx = fmax(mx, fabs(v));
+        mo = fmax(mo, (j + q == i) ? 0.0 : fabs(v));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      if (o == 8) continue;
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mo = fmax(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+    }
+    int e = 0, et = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    e = max(e, -960);
+    {
+      const double mt = fmax(fabs(tii), mo * inv_p);  // max |T_ij|: fl(x inv_p) is monotone in x
+      if (mt > 0.0) frexp(mt, &et);
+      et = max(et, -960);
+    }
+    if ((lane & 23) == 0 && live) {  // lanes 0 and 8
+      if (MODE != 1) scale[(int64_t)mat * np + i] = ldexp(1.0, e);
+      if (MODE == 1) scale[(int64_t)mat * np + i] = ldexp(1.0, et);
+      if (MODE == 2) scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
+    }
+    const double sa = digit_scale<S>(e), st = digit_scale<S>(et);
+    int8_t* pa = planes + (int64_t)mat * kSMax * pitch;
+    int8_t* pt = MODE == 2 ? planes_t + (int64_t)mat * kSMax * pitch : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < steps; ++c) {
+      const int j = 128 * c + cl;
+      if (j < np) {
+        double v[8];
+        if (live && j + 8 <= n) {
+          const double4 a0 = *reinterpret_cast<const double4*>(my + j);
+          const double4 a1 = *reinterpret_cast<const double4*>(my + j + 4);
+          v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
         } else {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) r[c][q] = 0.0;
+          for (int q = 0; q < 8; ++q) v[q] = (live && j + q < n) ? my[j + q] : 0.0;
         }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int j = 256 * c + 8 * lane;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          mx = fmax(mx, fabs(r[c][q]));
-          mo = fmax(mo, (j + q == i) ? 0.0 : fabs(r[c][q]));
-        }
-        reinterpret_cast<double4*>(my + j)[0] = make_double4(r[c][0], r[c][1], r[c][2], r[c][3]);
-        reinterpret_cast<double4*>(my + j)[1] = make_double4(r[c][4], r[c][5], r[c][6], r[c][7]);
-      }
-    }
-    const int e = row_exponent(mx);
-    // max |T_ij| = max(|T_ii|, max_{j != i} |M_ij| / p): fl(x * inv_p) is monotone in x
-    const int et = row_exponent(fmax(fabs(tii), mo * inv_p));  // the same value as the TM slicer's
-    if (lane == 0) {
-      scale_m[(int64_t)mat * np + i] = ldexp(1.0, e);
-      scale_t[(int64_t)mat * np + i] = ldexp(1.0, et);
-    }
-    const double sm = digit_scale<S>(e), st = digit_scale<S>(et);
-    __syncwarp();
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      const int j = 256 * c + 8 * lane;
-      if (j < np) {  // the staged row is zero beyond n: zero digits in the k padding
-        double r[8];
-        const double4 a0 = reinterpret_cast<const double4*>(my + j)[0];
-        const double4 a1 = reinterpret_cast<const double4*>(my + j)[1];
-        r[0] = a0.x; r[1] = a0.y; r[2] = a0.z; r[3] = a0.w; r[4] = a1.x; r[5] = a1.y; r[6] = a1.z; r[7] = a1.w;
         uint32_t dig[S][2];
-        slice8<S>(r, sm, dig);
+        if (MODE != 1) {
+          slice8<S>(v, sa, dig);
 #pragma unroll
-        for (int s = 0; s < S; ++s) store8(planes_m + pmat + s * pitch, i, j, np, dig[s]);
+          for (int s = 0; s < S; ++s) store8(pa + s * pitch, i, j, np, dig[s]);
+        }
+        if (MODE != 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) r[q] = (j + q == i) ? tii : r[q] * ninv_p;
-        slice8<S>(r, st, dig);
+          for (int q = 0; q < 8; ++q) v[q] = (j + q == i) ? tii : v[q] * ninv_p;  // beyond n: -0 (zero digits)
+          slice8<S>(v, st, dig);
+          int8_t* dst = MODE == 2 ? pt : pa;
 #pragma unroll
-        for (int s = 0; s < S; ++s) store8(planes_t + pmat + s * pitch, i, j, np, dig[s]);
+          for (int s = 0; s < S; ++s) store8(dst + s * pitch, i, j, np, dig[s]);
+        }
       }
     }
-    __syncwarp();  // the row buffer is rewritten by the next row
+    // the pair B ahead overwrites this buffer: order these generic reads before its bulk copy (async proxy)
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (pid + B * nw < total) issue(pid + B * nw, b);
+    }
+    __syncwarp();
+    if (++b == B) {
+      b = 0;
+      phase ^= 1;
+    }
   }
 }
 

@@ -608,6 +608,17 @@ static cudaError_t oz_gemm(int S, const oz::OzArgs& a, cudaStream_t stream) {
   }
 }
 
+// M_k and T_k (n <= 1024): the row-pair slicer (whole-line stores: 2.47 vs 3.42 ms for the one-row-per-warp slicer at
+// S = 7, 528 matrices); X_k and the rest: slice_kernel (one register-resident row per warp, 16 warps per SM: its
+// write share is half the M/T slicer's, and the pair slicer's 12 warps per SM lose there -- 1.51 vs 1.11 ms, r02zf)
+template <int S, int MODE>
+static void oz_slice_pair(const double* src, int64_t mstride, int n, int np, int batch, const int* act,
+                          const int* nact, int8_t* pa, double* sa, int8_t* pt, double* st, int p, cudaStream_t stream) {
+  ensure_smem((const void*)oz::slice_pair_kernel<S, MODE>, oz::kPairSmem);
+  oz::slice_pair_kernel<S, MODE><<<3 * num_sms(), 32 * oz::kPairWarps, oz::kPairSmem, stream>>>(
+      src, mstride, n, np, batch, act, nact, pa, sa, pt, st, p);
+}
+
 template <int S>
 static void oz_slice_s(bool tm, const double* src, int64_t mstride, int n, int np, int batch, const int* act,
                        const int* nact, int8_t* planes, double* scale, int p, cudaStream_t stream) {
@@ -627,18 +638,13 @@ static void oz_slice(int S, bool tm, const double* src, int64_t mstride, int n, 
   }
 }
 
-template <int S>
-static void oz_slice_mt_s(const double* src, int64_t mstride, int n, int np, int batch, const int* act,
-                          const int* nact, int8_t* pm, double* sm, int8_t* pt, double* st, int p, cudaStream_t stream) {
-  oz::slice_mt_kernel<S><<<4 * num_sms(), 32 * oz::kSliceMtWarps, 0, stream>>>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p);
-}
-
+// M_k and T_k in one pass over M_k (n <= 1024)
 static void oz_slice_mt(int S, const double* src, int64_t mstride, int n, int np, int batch, const int* act,
                         const int* nact, int8_t* pm, double* sm, int8_t* pt, double* st, int p, cudaStream_t stream) {
   switch (S) {
-    case 5: oz_slice_mt_s<5>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
-    case 6: oz_slice_mt_s<6>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
-    default: oz_slice_mt_s<7>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
+    case 5: oz_slice_pair<5, 2>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
+    case 6: oz_slice_pair<6, 2>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
+    default: oz_slice_pair<7, 2>(src, mstride, n, np, batch, act, nact, pm, sm, pt, st, p, stream); break;
   }
 }
 
