@@ -62,11 +62,13 @@ def _int8_peak():
     except (OSError, ValueError):
         pass
     return 2 * 1687.1, "burst (earlier measurement; MEASURED_PEAKS.json absent)", 2 * 1687.1
-# dram read + write per Ozaki GEMM launch per 1024^2 matrix: the mean over the four product launches of one
-# iteration, from the ncu --set full capture of the round-2 kernel (profiles/r02/r02a_ncu_gemm7_full_summary.txt, 148
-# matrices): X T 3.377 GB, T T sliced 2.130 GB, T^2 T^2 sliced 2.132 GB, T^4 M 3.379 GB -> 22.8 / 14.4 / 14.4 / 22.8 MB per
-# matrix = the algorithmic planes + output (no re-reads); measured at S = 7 (fewer planes move at S = 5, 6)
-OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = (3.377 + 2.130 + 2.132 + 3.379) / 4 * 1e9 / 148
+# dram read + write per Ozaki GEMM launch per 1024^2 matrix: the mean over the four product launches of one S = 5
+# iteration (the schedule's majority: 55 of the 88 GEMM launches of a 528-root call), from the ncu --set full capture
+# of the final kernel with tiled planes (profiles/r02/r02zb_ncu_gemm5_full_tiled_summary.txt, 148 matrices): X T
+# 2.751 GB, T T sliced 1.515 GB, T^2 T^2 sliced 1.518 GB, T^4 M 2.764 GB -> 18.6 / 10.2 / 10.3 / 18.7 MB per matrix =
+# the algorithmic planes + output (18 / 10 / 10 / 18 MB: no re-reads).  S = 7 launches move 22.8 / 14.4 / 14.4 / 22.8
+# MB (r02a_ncu_gemm7_full_summary.txt).
+OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE = (2.751 + 1.515 + 1.518 + 2.764) / 4 * 1e9 / 148
 # the arithmetic of the dominant phase (the roots): fp64 iterates, products per the root precision
 DTYPE = {"auto": "f64 iterates, int8 Ozaki products S=7..5 per iteration (exact int32 accumulation)",
          "auto7": "f64 iterates, int8 Ozaki S=7 products (exact int32 accumulation)",
@@ -434,8 +436,8 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
                 "frac": achieved / peak, "traffic": OZAKI_TRAFFIC_BYTES_PER_MATRIX_STAGE * cnt,
                 "traffic_note": "dram read+write bytes per GEMM launch (mean of the 4 product launches of an "
-                                "iteration at S = 7), ncu --set full of the same kernel (148 matrices) scaled to "
-                                "this batch: the algorithmic planes + output, no re-reads",
+                                "S = 5 iteration, the schedule's majority), ncu --set full of the same kernel (148 "
+                                "matrices, r02zb) scaled to this batch: the algorithmic planes + output, no re-reads",
                 "kernel": f"oz::gemm_kernel (INT8 tcgen05 Ozaki products, batch {cnt} x {n}^2, p=4)",
                 "kernel_ms": float(working.mean()) if working.size else None,
                 "kernel_launches": int(working.size), "kernel_launches_total": gemm_launches,
