@@ -2,9 +2,10 @@
 T=${1:-r02z}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
-timeout 600 python bench.py --steps 5 --warmup 3 > $O/bench_n1.json 2> $O/bench_n1.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_root528.csv \
-  python tools/profile_root.py --batch 528 --hybrid -9 --reps 1 > $O/launches_root528.log 2>&1
+for g in 0 8 16 24 36; do
+  SHAMPOO_PI_GROUP=$g timeout 300 python tools/profile_root.py --batch 528 --hybrid -9 --reps 2 --digest >> $O/pi_group.log 2>&1
+  SHAMPOO_PI_GROUP=$g timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:root_kernel \
+     --log-file $O/pi_group_$g.csv python tools/profile_root.py --batch 528 --hybrid -9 --reps 1 > /dev/null 2>&1
+done
+timeout 300 python tools/profile_root.py --batch 528 --hybrid -9 --reps 2 --digest >> $O/pi_group.log 2>&1
 echo done > $O/DONE

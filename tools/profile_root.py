@@ -23,6 +23,7 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--max-iter", type=int, default=100)
 ap.add_argument("--power-iters", type=int, default=100)
 ap.add_argument("--slices", type=int, default=0, help="Ozaki slices with --hybrid -9 (0: the slice schedule)")
+ap.add_argument("--digest", action="store_true", help="print a sha256 of the roots and lambda_max (bit-identity checks)")
 ap.add_argument("--hybrid", type=int, default=None,
                 help="fp64 iterations before the 3xTF32 tail (-1 = auto); -9 = the Ozaki INT8 root")
 args = ap.parse_args()
@@ -45,3 +46,7 @@ flops = float(inf["iters"].sum()) * prods * n * n * (n + 1)
 print(f"{'fp64' if args.hybrid is None else (f"ozaki{args.slices or ''}" if args.hybrid == -9 else 'hybrid')} batch {args.batch} n {n} p {args.p}: {ms:.2f} ms, iters mean {inf['iters'].mean():.2f}, "
       f"status {set(inf['status'].tolist())}, {flops / ms / 1e9:.2f} TFLOP/s (sym-minimal), "
       f"{args.batch / ms * 1e3:.1f} roots/s")
+if args.digest:
+    import hashlib
+    h = hashlib.sha256(X.cpu().numpy().tobytes() + inf["lambda_max"].tobytes()).hexdigest()
+    print(f"digest {h} SHAMPOO_PI_GROUP={os.environ.get('SHAMPOO_PI_GROUP', '(default)')}")
