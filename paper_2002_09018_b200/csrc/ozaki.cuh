@@ -347,11 +347,19 @@ __global__ void __launch_bounds__(32 * W) slice_pair_kernel(
     double mx = 0.0, mo = 0.0;
     for (int c = 0; c < steps; ++c) {
       const int j = 128 * c + cl;
+      double v[8];
+      if (live && j + 8 <= n) {
+        const double4 a0 = *reinterpret_cast<const double4*>(my + j);
+        const double4 a1 = *reinterpret_cast<const double4*>(my + j + 4);
+        v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = (live && j + q < n) ? my[j + q] : 0.0;
+      }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const double v = (live && j + q < n) ? my[j + q] : 0.0;
-        mx = fmax(mx, fabs(v));
-        mo = fmax(mo, (j + q == i) ? 0.0 : fabs(v));
+        mx = fmax(mx, fabs(v[q]));
+        if (MODE != 0) mo = fmax(mo, (j + q == i) ? 0.0 : fabs(v[q]));
       }
     }
 #pragma unroll

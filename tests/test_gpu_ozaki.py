@@ -75,6 +75,18 @@ def test_ozaki_1024_p2(shp, mode, bar):
         assert inf[i]["status"] == io.status == 0 and abs(int(inf[i]["iters"]) - io.iters) <= 1
 
 
+def test_ozaki_940_tiled_padding(shp):
+    """The vocabulary remainder block (33708 = 32 x 1024 + 940): np = 960 and the tiled planes' row padding to 1024
+    (the last A tile's second row block is padding), k padding 940 .. 959 zeroed by every writer."""
+    As = synth.psd_batch(940, 2, synth.BASE_SEED + 940, "mixed")
+    for p in (4, 2):
+        Xg, inf, outs = _both(shp, As, p, mode="ozaki")
+        for i, (Xo, io) in enumerate(outs):
+            print(f"n=940 p={p} matrix {i}: root rel err {rel(Xg[i], Xo):.3e}")
+            assert rel(Xg[i], Xo) < 2e-6
+            assert inf[i]["status"] == io.status == 0 and abs(int(inf[i]["iters"]) - io.iters) <= 1
+
+
 @pytest.mark.parametrize("mode,bar", [("ozaki7", 1e-6), ("ozaki", 2e-6)])
 def test_ozaki_2048(shp, mode, bar):
     """n > 1024: the two-pass slicing path and 32 k-chunks per tile (config 5's b = 2048 blocks).  The slice

@@ -150,25 +150,18 @@ int main(int argc, char** argv) {
   cudaMemset(pm, 0, batch * mat * oz::kSMax);
   cudaMemset(pt, 0, batch * mat * oz::kSMax);
   run<7, 0>(src, pm, pt, sm, st, batch);
-  run<7, 1>(src, pm, pt, sm, st, batch);
-  run<5, 0>(src, pm, pt, sm, st, batch);
   runp<7, 2, 4, 1>(src, pm, pt, sm, st, batch);
-  runp<7, 2, 2, 2>(src, pm, pt, sm, st, batch);
-  runp<7, 2, 3, 2>(src, pm, pt, sm, st, batch);
-  runp<7, 2, 2, 3>(src, pm, pt, sm, st, batch);
-  runp<7, 2, 4, 2>(src, pm, pt, sm, st, batch);
-  runp<7, 2, 1, 4>(src, pm, pt, sm, st, batch);
-  runp<7, 2, 1, 2>(src, pm, pt, sm, st, batch);
+  runp<7, 2, 8, 1>(src, pm, pt, sm, st, batch);
+  runp<7, 2, 10, 1>(src, pm, pt, sm, st, batch);
+  runp<7, 2, 12, 1>(src, pm, pt, sm, st, batch);
+  runp<6, 2, 4, 1>(src, pm, pt, sm, st, batch);
+  runp<6, 2, 8, 1>(src, pm, pt, sm, st, batch);
+  runp<6, 2, 12, 1>(src, pm, pt, sm, st, batch);
   runp<5, 2, 4, 1>(src, pm, pt, sm, st, batch);
-  runp<5, 2, 2, 2>(src, pm, pt, sm, st, batch);
-  runp<5, 2, 3, 2>(src, pm, pt, sm, st, batch);
-  runp<5, 2, 2, 3>(src, pm, pt, sm, st, batch);
-  runp<5, 0, 4, 1>(src, pm, pt, sm, st, batch);
-  runp<5, 0, 2, 2>(src, pm, pt, sm, st, batch);
-  runp<5, 0, 3, 2>(src, pm, pt, sm, st, batch);
-  runp<5, 0, 2, 3>(src, pm, pt, sm, st, batch);
-  runp<5, 0, 1, 4>(src, pm, pt, sm, st, batch);
-  runp<5, 0, 1, 2>(src, pm, pt, sm, st, batch);
+  runp<5, 2, 8, 1>(src, pm, pt, sm, st, batch);
+  runp<5, 2, 12, 1>(src, pm, pt, sm, st, batch);
+  runp<5, 0, 8, 1>(src, pm, pt, sm, st, batch);
+  runp<5, 0, 12, 1>(src, pm, pt, sm, st, batch);
   printf("done\n");
   return 0;
 }
