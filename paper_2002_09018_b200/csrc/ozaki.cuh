@@ -82,6 +82,8 @@ static_assert(kEpiWarps == 8 || kEpiWarps == 16, "two or four epilogue warps per
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 // Bound probes for tools/microbench/ozaki_test.cu only (the library builds with 0):
 // 1 = no MMAs (TMA data movement + barriers + epilogue), 2 = no TMA loads (MMAs on stale tiles),
+// 4 = no loads and no epilogue (MMAs and the accumulator hand-off only), 5 = no epilogue (loads + MMAs),
+// 6 = the drain (phase 1) but no scaling or stores, 7 = fp64 epilogue without its stores,
 #ifndef OZ_PROBE
 #define OZ_PROBE 0
 #endif
@@ -450,6 +452,19 @@ __device__ __forceinline__ unsigned long long int_w(double c, int e_out, bool& o
   return (unsigned long long)(V + kC);
 }
 
+// 256-bit store of eight words (32-byte aligned; sm_100 STG.E.256)
+__device__ __forceinline__ void st_v8(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e, uint32_t f,
+                                      uint32_t g, uint32_t h) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d),
+               "r"(e), "r"(f), "r"(g), "r"(h)
+               : "memory");
+}
+// 256-bit evict-first store of four doubles (32-byte aligned; sm_100 STG.E.EF.256)
+__device__ __forceinline__ void st_cs_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+
 // fp32 round-to-nearest-even of a double on the integer pipe (normal fp32 results and zeros; anything else
 // -- subnormal fp32 results, inf, NaN -- through the out-of-line conversion)
 static __device__ __noinline__ float f32_of_slow(double x) { return __double2float_rn(x); }
@@ -637,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int g = 0; g < kGroups; ++g) {
             uint64_t* fb = full + stage * kGroups + g;
-#if OZ_PROBE == 2
+#if OZ_PROBE == 2 || OZ_PROBE == 4
             tc::mbar_arrive(fb);
             continue;
 #endif
@@ -718,14 +733,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int mat, job, ti, tj;
       oz_decode(a, per_mat, tile, mat, job, ti, tj);
-      tc::mbar_wait(tmem_full, acc_phase);
-      tc::tc_fence_after();
+      // the tile's scales are loaded while its MMAs run: this lane's row scale, and ONE column-scale exponent per
+      // lane (column j0 + cb + lane; phase 2 takes column e's from lane e - cb by a shuffle).  Round 2 loaded the
+      // column scales in phase 2, after the release, where every load waited behind the epilogue's stores: the
+      // stall samples sat on their first use (ncu r02zb)
       const int i = ti * kBM + row_in_tile;
       const bool row_ok = i < a.n;
       const OzJob& J = a.job[job];
+      const double sa = row_ok ? J.a_scale[(int64_t)mat * a.np + i] : 0.0;
+      const int bexp = exp2_of(J.b_scale[(int64_t)mat * a.np + tj * kBN + cb + lane]);
+      tc::mbar_wait(tmem_full, acc_phase);
+      tc::tc_fence_after();
+#if OZ_PROBE >= 4  // no epilogue: release the accumulators at once
+      tc::tc_fence_before();
+      tc::mbar_arrive(tmem_empty);
+      acc_phase ^= 1;
+      continue;
+#endif
       const bool mup = a.mupdate && job == 0;
       double* out = J.out + mat * J.out_stride;
-      const double sa = row_ok ? J.a_scale[(int64_t)mat * a.np + i] : 0.0;
       // phase 1: drain the S accumulators of all 64 columns, then release TMEM so
       // the next tile's MMAs overlap this tile's scaling and stores.  Per
       // 8-column chunk the S loads are issued back to back behind ONE wait.
@@ -765,6 +791,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int e = 0; e < kEpiCols; ++e) dep |= (uint32_t)(__double_as_longlong(v[e]) >> 32);
       tc::tc_fence_before();
       tc::mbar_arrive(tmem_empty + ((dep == 0xFFFFFFFFu && a.n < 0) ? 1 : 0));
+#if OZ_PROBE == 6  // drain only: no scaling, no stores
+      acc_phase ^= 1;
+      continue;
+#endif
       // phase 2: scale by 2^(e_i + f_j - 12 - 7(S-1)) (exponent arithmetic), store
       // row-major (16-byte vectors) and mirrored, evict-first (st.global.cs: the
       // outputs must not push the operand planes other tiles still read out of L2); M-update: max|M - I| on the
@@ -785,7 +815,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const bool interior = (same_ab || j0 >= ti * kBM + kBM) && (j0 + kBN <= a.n) && (ti * kBM + kBM <= a.n);
         bool ovf = false;
         const int i0w = ti * kBM + quad * 32;  // this warp's first row
-        const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
         const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
         if (row_ok && tj == 2 * ti && cb == 0)
           J.out_scale[(int64_t)mat * a.np + i] = __longlong_as_double((long long)(J.out_e + 1023) << 52);
@@ -796,10 +825,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int lim = a.n - (j0 + h);  // columns >= n (padding B rows, never written) stay 0: no false overflow
 #pragma unroll
           for (int e = 0; e < kEpiCols; e += 2) {
+            const int bx0 = __shfl_sync(0xffffffffu, bexp, e), bx1 = __shfl_sync(0xffffffffu, bexp, e + 1);
             if (row_ok) {
-              const double2 b2 = *reinterpret_cast<const double2*>(bs + h + e);
-              w[e] = e < lim ? int_w<kS>(scale2(v[e], ka + exp2_of(b2.x)), J.out_e, ovf) : 0ull;
-              w[e + 1] = e + 1 < lim ? int_w<kS>(scale2(v[e + 1], ka + exp2_of(b2.y)), J.out_e, ovf) : 0ull;
+              w[e] = e < lim ? int_w<kS>(scale2(v[e], ka + bx0), J.out_e, ovf) : 0ull;
+              w[e + 1] = e + 1 < lim ? int_w<kS>(scale2(v[e + 1], ka + bx1), J.out_e, ovf) : 0ull;
             } else {
               w[e] = w[e + 1] = 0ull;
             }
@@ -814,10 +843,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               wd[k] = w_byte<kS>(w[4 * k], s2) | (w_byte<kS>(w[4 * k + 1], s2) << 8) |
                       (w_byte<kS>(w[4 * k + 2], s2) << 16) | (w_byte<kS>(w[4 * k + 3], s2) << 24);
             if (interior) {
-#pragma unroll
-              for (int q = 0; q < kW / 4; ++q)
-                *reinterpret_cast<uint4*>(ps + tiled_off(i, j0 + h + 16 * q, a.np)) =
-                    make_uint4(wd[4 * q], wd[4 * q + 1], wd[4 * q + 2], wd[4 * q + 3]);
+              static_assert(kW == 8, "one 32-byte row segment per lane and plane");
+              // the row's 32 bytes are the 16-byte chunks c, c+1 (c even) of one tile row, swizzled to the aligned
+              // pair {c ^ x, (c+1) ^ x}, x = (i >> 1) & 3: one whole-sector 32-byte store, halves swapped for odd x
+              int8_t* dst = ps + (tiled_off(i, j0 + h, a.np) & ~(int64_t)31);
+              if ((i >> 1) & 1)
+                st_v8(dst, wd[4], wd[5], wd[6], wd[7], wd[0], wd[1], wd[2], wd[3]);
+              else
+                st_v8(dst, wd[0], wd[1], wd[2], wd[3], wd[4], wd[5], wd[6], wd[7]);
               // mirror rows j0 + h + 4k + (lane >> 3), columns i0w + 4 (lane & 7) .. + 3
               const int src = 4 * (lane & 7), sel = 8 * (lane >> 3);
 #pragma unroll
@@ -847,21 +880,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                     0x7FF8000000000000ull);
       } else if (J.outf) {
         // fp32 output (a8, one-sided blocks: P_b = G_b X_R; non-symmetric tiles, no mirror)
-        if (row_ok && i < J.outf_rows[mat]) {
+        {
+          const bool live = row_ok && i < J.outf_rows[mat];
           const int j0 = tj * kBN;
-          const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
-          float* orow = J.outf[mat] + (int64_t)i * J.outf_ld[mat] + j0;
+          float* orow = live ? J.outf[mat] + (int64_t)i * J.outf_ld[mat] + j0 : nullptr;
           const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
           const bool vec = j0 + cb + kEpiCols <= a.n && ((reinterpret_cast<uintptr_t>(orow) & 15) == 0);
 #pragma unroll
           for (int e = cb; e < cb + kEpiCols; e += 4) {
-            const double2 b01 = *reinterpret_cast<const double2*>(bs + e);
-            const double2 b23 = *reinterpret_cast<const double2*>(bs + e + 2);
-            const float f0 = f32_of(scale2(v[e - cb], ka + exp2_of(b01.x)));
-            const float f1 = f32_of(scale2(v[e - cb + 1], ka + exp2_of(b01.y)));
-            const float f2 = f32_of(scale2(v[e - cb + 2], ka + exp2_of(b23.x)));
-            const float f3 = f32_of(scale2(v[e - cb + 3], ka + exp2_of(b23.y)));
-            if (vec) {
+            const float f0 = f32_of(scale2(v[e - cb], ka + __shfl_sync(0xffffffffu, bexp, e - cb)));
+            const float f1 = f32_of(scale2(v[e - cb + 1], ka + __shfl_sync(0xffffffffu, bexp, e - cb + 1)));
+            const float f2 = f32_of(scale2(v[e - cb + 2], ka + __shfl_sync(0xffffffffu, bexp, e - cb + 2)));
+            const float f3 = f32_of(scale2(v[e - cb + 3], ka + __shfl_sync(0xffffffffu, bexp, e - cb + 3)));
+            if (!live) {
+            } else if (vec) {
               __stcs(reinterpret_cast<float4*>(orow + e), make_float4(f0, f1, f2, f3));
             } else {
               if (j0 + e < a.n) orow[e] = f0;
@@ -871,20 +903,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           }
         }
-      } else if (row_ok) {
+      } else {
         const int j0 = tj * kBN;
-        const double* bs = J.b_scale + (int64_t)mat * a.np + j0;
         double* orow = out + (int64_t)i * a.np + j0;
         const bool full_row = j0 + cb + kEpiCols <= a.n && (!a.sym || j0 + cb >= i);
         const int ka = exp2_of(sa) - (12 + 7 * (kS - 1));
 #pragma unroll
         for (int e = cb; e < cb + kEpiCols; e += 2) {
-          const double2 b2 = *reinterpret_cast<const double2*>(bs + e);
-          const double c0 = scale2(v[e - cb], ka + exp2_of(b2.x)), c1 = scale2(v[e - cb + 1], ka + exp2_of(b2.y));
+          const double c0 = scale2(v[e - cb], ka + __shfl_sync(0xffffffffu, bexp, e - cb));
+          const double c1 = scale2(v[e - cb + 1], ka + __shfl_sync(0xffffffffu, bexp, e - cb + 1));
           v[e - cb] = c0;
           v[e - cb + 1] = c1;
+          if (!row_ok) continue;
           if (full_row) {
-            __stcs(reinterpret_cast<double2*>(orow + e), make_double2(c0, c1));
+            // one 32-byte store per lane (a whole sector; STG.256): the row segments of 32 lanes are 32 rows apart,
+            // so 16-byte stores left every sector half-written per instruction
+#if OZ_PROBE != 7
+            if ((e - cb) & 2) st_cs_v4(orow + e - 2, v[e - cb - 2], v[e - cb - 1], c0, c1);
+#endif
           } else {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -905,14 +941,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
         // the one fp64 subtraction of the M-update, once per row of a diagonal tile
-        if (mup && i >= j0 + cb && i < j0 + cb + kEpiCols)
+        if (mup && row_ok && i >= j0 + cb && i < j0 + cb + kEpiCols)
           emax_bits = umax64(emax_bits, abs_bits(__longlong_as_double((long long)diag_bits) - 1.0));
-        if (a.sym) {  // mirror: lanes are consecutive rows -> coalesced
+        if (a.sym && row_ok) {  // mirror: lanes are consecutive rows -> coalesced
 #pragma unroll
           for (int e = cb; e < cb + kEpiCols; ++e) {
             const int j = j0 + e;
             if (j >= a.n || j <= i) continue;
+#if OZ_PROBE == 7  // compute but no stores: one dependent store per lane keeps the values alive
+            if (__double_as_longlong(v[e - cb]) == 0x7FF0000000000001ll) __stcs(out + (int64_t)j * a.np + i, v[e - cb]);
+#else
             __stcs(out + (int64_t)j * a.np + i, v[e - cb]);
+#endif
           }
         }
       }
