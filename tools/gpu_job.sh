@@ -2,9 +2,9 @@
 T=${1:-r02z}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 900 python bench.py --max-precond-dim 4096 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_config3p.json 2> $O/bench_config3p.err
-bash tools/sweep_blocks.sh > $O/block_sweep.jsonl 2> $O/block_sweep.err
-timeout 900 python tools/bench_workloads.py --workload config2 > $O/config2.json 2> $O/config2.err
-timeout 900 python tools/bench_workloads.py --workload config4 > $O/config4.json 2> $O/config4.err
-timeout 900 python tools/bench_workloads.py --workload resnet50 > $O/resnet50.json 2> $O/resnet50.err
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_root528.csv \
+  python tools/profile_root.py --batch 528 --hybrid -9 --reps 1 > $O/launches_root528.log 2>&1
+timeout 600 python bench.py --steps 5 --warmup 3 > $O/bench_n1.json 2> $O/bench_n1.err
 echo done > $O/DONE
