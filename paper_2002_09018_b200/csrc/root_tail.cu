@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(1024) root_tail_decide_graph_kernel(int* act, 
 
 // Final decisions of the handed-off matrices (res.x == -3) and the fp32 output:
 // X_k lives in pair TX[(k - k_sw) & 1]; the stored hi IS the fp32 iterate.
-__global__ void __launch_bounds__(128) root_tail_finish_kernel(double* bufs, const int4* res, const double* errh,
+__global__ void __launch_bounds__(256) root_tail_finish_kernel(double* bufs, const int4* res, const double* errh,
                                                                shampoo_root_info_t* info, float* X, int64_t ldx,
                                                                int64_t stride_x, int batch, int n, int np,
                                                                int max_iter, int k_sw, double tol, double stag,
@@ -429,9 +429,24 @@ __global__ void __launch_bounds__(128) root_tail_finish_kernel(double* bufs, con
   const double* src64 = bufs + ((int64_t)mat * kTailRegions + s_buf) * (int64_t)np * np;
   const float* src = reinterpret_cast<const float*>(src64);
   float* out = X + (int64_t)mat * stride_x;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)n * n; idx += blockDim.x) {
-    const int64_t i = idx / n, j = idx - i * n;
-    out[i * ldx + j] = fp64 ? __double2float_rn(src64[i * np + j]) : src[i * np + j];
+  // one warp per row; fp64 rows of 4 elements per lane (32-byte loads, 16-byte stores) when the output rows are
+  // 16-byte aligned (round 2: one element per thread of a 128-thread CTA ran at ~1.3 TB/s)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const bool vec = fp64 && (ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  for (int i = warp; i < n; i += nwarps) {
+    const double* r64 = src64 + (int64_t)i * np;
+    float* o = out + (int64_t)i * ldx;
+    if (vec) {
+      int j = 4 * lane;
+      for (; j + 4 <= n; j += 128) {
+        const double4 d = *reinterpret_cast<const double4*>(r64 + j);
+        *reinterpret_cast<float4*>(o + j) =
+            make_float4(__double2float_rn(d.x), __double2float_rn(d.y), __double2float_rn(d.z), __double2float_rn(d.w));
+      }
+      for (int jj = j; jj < n && jj < j + 4; ++jj) o[jj] = __double2float_rn(r64[jj]);  // the row tail
+    } else {
+      for (int j = lane; j < n; j += 32) o[j] = fp64 ? __double2float_rn(r64[j]) : src[(int64_t)i * np + j];
+    }
   }
 }
 
@@ -530,7 +545,7 @@ int root_tail_launch(double* bufs, int batch, int n, int np, int p, int max_iter
     root_tail_decide_kernel<<<1, 1024, 0, stream>>>(act, nact, errh, max_iter, ttol, 0.5, k + 1);
     ++*launches;
   }
-  root_tail_finish_kernel<<<batch, 128, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
+  root_tail_finish_kernel<<<batch, 256, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
                                                      k_sw, ttol, 0.5, R(TX0), R(TX1), 0);
   ++*launches;
   cudaError_t e = cudaGetLastError();
@@ -893,7 +908,7 @@ int root_ozaki_launch(double* bufs, int batch, int n, int np, int p, int max_ite
     });
     if (rc) return rc;
   }
-  root_tail_finish_kernel<<<batch, 128, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
+  root_tail_finish_kernel<<<batch, 256, 0, stream>>>(bufs, res, errh, info, X, ldx, stride_x, batch, n, np, max_iter,
                                                      0, tol, 1.0, RX0, RX1, 1);
   ++*launches;
   cudaError_t e = cudaGetLastError();
