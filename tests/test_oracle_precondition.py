@@ -159,3 +159,29 @@ def test_momentum_zero_preconditioned_gradient():
     eta = opre.momentum_step_block(W, np.zeros_like(W), np.zeros_like(W), _blk((2, 3), 41), np.ones((2, 3)),
                                    np.zeros((2, 3)), 0.0, 1.0, True)
     assert eta == 0.0 and np.array_equal(W, W0)
+
+
+def test_graft_numerator_closed_forms():
+    """num_b = sum g^2 / max(D_new, 1e-30) with D_new = D + g^2, pinned by closed forms
+    rather than by restating it: from D = 0 every nonzero entry contributes g^2/g^2 = 1 (so num = nnz; a division
+    by the OLD accumulator would hit the 1e-30 floor, a sqrt would give sum |g|), zeros contribute 0 (the floor keeps
+    0/0 out); the same gradient again halves every term; (2^k G, 4^k D) leaves num unchanged."""
+    rng = np.random.default_rng(5)
+    G = np.ldexp(1.0, rng.integers(-8, 8, size=(7, 9))).astype(np.float32)  # powers of two: exact fp32 squares
+    G *= rng.choice([-1.0, 1.0], size=G.shape).astype(np.float32)
+    G[rng.random(G.shape) < 0.3] = 0.0
+    nnz = int(np.count_nonzero(G))
+    D = np.zeros_like(G)
+    assert ostats.diag_update(G, 0, 0, 7, 9, D) == float(nnz)
+    np.testing.assert_array_equal(D, G * G)
+    assert ostats.diag_update(G, 0, 0, 7, 9, D) == nnz / 2.0
+    # scale equivariance, bit-exact for a power-of-two scale, on a general gradient and accumulator
+    G2 = gaussian((5, 6), 11)
+    D2 = (np.abs(gaussian((5, 6), 12)) + 0.05).astype(np.float32)
+    a = ostats.diag_update(G2, 0, 0, 5, 6, D2.copy())
+    b = ostats.diag_update((G2 * 8).astype(np.float32), 0, 0, 5, 6, (D2 * 64).astype(np.float32))
+    assert a == b
+    # a block view: the 2 x 2 block grid's numerators sum to the whole (from D = 0, powers of two: exact)
+    Dz = np.zeros_like(G)
+    parts = [ostats.diag_update(G, r0, c0, rr, cc, Dz) for r0, rr in ((0, 3), (3, 4)) for c0, cc in ((0, 4), (4, 5))]
+    assert sum(parts) == float(nnz)
