@@ -3,6 +3,6 @@
 T=${1:-r02z}
 O=gpurun_out/$T
 mkdir -p $O
-rm -f tools/microbench/bin/ozaki_test   # the test must build it
-timeout 1200 python -m pytest tests/test_gpu_ozaki_gemm.py -q -s > $O/pytest_gemm.log 2>&1; echo "pytest exit $?" >> $O/pytest_gemm.log
+timeout 900 ncu --set full --clock-control none -k regex:"slice|root_kernel" -c 4 -f -o $O/slices148 \
+  python tools/profile_root.py --batch 148 --hybrid -9 --reps 1 > $O/ncu_slices148.log 2>&1
 echo done > $O/DONE
