@@ -3,6 +3,5 @@
 T=${1:-r02z}
 O=gpurun_out/$T
 mkdir -p $O
-timeout 900 ncu --set full --clock-control none -k regex:"slice|root_kernel" -c 4 -f -o $O/slices148 \
-  python tools/profile_root.py --batch 148 --hybrid -9 --reps 1 > $O/ncu_slices148.log 2>&1
+timeout 600 tools/microbench/bin/slice_layout 528 > $O/slice_layout.log 2>&1; echo "exit $?" >> $O/slice_layout.log
 echo done > $O/DONE
